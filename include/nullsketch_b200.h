@@ -1,0 +1,179 @@
+/*
+ * nullsketch_b200.h -- C ABI of the B200-native sketch-and-solve hot path.
+ *
+ * Drop-in boundary for the reference's C++ API (paths relative to
+ * /root/reference/proj):
+ *
+ *   reference symbol                                       replaced by
+ *   ---------------------------------------------------   ---------------------------
+ *   SketchOperator::draw(kind, s, m, seed)  sketch.hpp:42   nsk_op_draw
+ *   SketchOperator::descriptor()            sketch.hpp:48   nsk_op_descriptor
+ *   SketchOperator::from_descriptor(json)   sketch.hpp:47   nsk_op_from_descriptor
+ *   SketchOperator::{kind,s,m,seed,id}()    sketch.hpp:50-59 nsk_op_info
+ *   (the sorted sample R, sketch.hpp:77)                    nsk_op_sample_indices
+ *   apply(S, A)                             sketch.hpp:89   nsk_apply / nsk_apply_host
+ *   solve_k(A, k, S)                        nullspace.hpp:24 nsk_solve_k / nsk_solve_k_host
+ *   solve_tol(A, eps, S)                    nullspace.hpp:30 nsk_solve_tol / nsk_solve_tol_host
+ *   residual_certificate(A, W)              nullspace.hpp:33 nsk_residual_fro
+ *   svd(SA) -> trailing V block             kernels.hpp:24 + nullspace.cpp:10-19
+ *                                                           nsk_svd_trailing
+ *   (no reference: row-sharded multi-GPU partial S_g A_g)   nsk_apply_shard
+ *
+ * Conventions (matrix.hpp:13-18, 32-105 of the reference):
+ *   - dense column-major storage, leading dimension in elements;
+ *   - NSK_REAL = IEEE double, NSK_COMPLEX = interleaved (re, im) doubles
+ *     (std::complex<double> / Eigen::MatrixXcd layout);
+ *   - srft output is always complex; gaussian keeps the input kind; srdct,
+ *     srht and countsketch reject complex input (sketch.cpp:219-221);
+ *   - the caller owns every buffer; the library owns only the opaque
+ *     operator (its descriptor state: kind, s, m, seed, and the sorted
+ *     sample).  Gaussian S, signs and hash buckets are regenerated on the
+ *     device from the counter-based stream and never stored.
+ *   - "device" entry points take device pointers and a cudaStream_t (passed
+ *     as void*); they are stream-ordered and do not synchronise unless a
+ *     host result is returned (nsk_solve_tol's k, nsk_residual_fro's value).
+ *     "_host" entry points take host pointers (the reference's value
+ *     semantics) and return when the results are in host memory.
+ *
+ * Errors: C++ exceptions of the reference become status codes
+ *   std::invalid_argument -> NSK_EINVAL, std::out_of_range -> NSK_ERANGE,
+ *   SvdConvergenceError (kernels.hpp:18-20) -> NSK_ENOCONV,
+ *   CUDA failures -> NSK_ECUDA, allocation failure -> NSK_ENOMEM;
+ *   nsk_last_error() returns the thread-local message of the last failure.
+ *   No entry point returns NaN silently (kernels.hpp:22-23).
+ *
+ * Threading: an operator is immutable after draw; concurrent calls on the
+ * same operator from several threads/streams are safe.
+ * Results are bit-identical across re-runs on the same GPU model and launch
+ * configuration: every reduction has a fixed order (no float atomics).
+ */
+#ifndef NULLSKETCH_B200_H
+#define NULLSKETCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nsk_operator nsk_operator;
+
+enum nsk_kind {
+  NSK_GAUSSIAN = 0,    /* dense N(0,1) G scaled by 1/sqrt(s)            sketch.hpp:24 */
+  NSK_SRFT = 1,        /* sqrt(m/s) R F^* D, complex                     sketch.hpp:25-26 */
+  NSK_SRDCT = 2,       /* sqrt(m/s) R C_III^T D, real                     sketch.hpp:27 */
+  NSK_SRHT = 3,        /* sqrt(m/s) R H D, m a power of two (no reference) */
+  NSK_COUNTSKETCH = 4  /* SA[h(i),:] += sigma(i) A[i,:]   (no reference) */
+};
+
+enum nsk_scalar { NSK_REAL = 0, NSK_COMPLEX = 1 };
+
+enum nsk_status {
+  NSK_OK = 0,
+  NSK_EINVAL = 1,
+  NSK_ERANGE = 2,
+  NSK_ENOCONV = 3,
+  NSK_ECUDA = 4,
+  NSK_ENOMEM = 5
+};
+
+/* Thread-local message describing the last non-OK status. */
+const char* nsk_last_error(void);
+
+/* Library version string and the CUDA architecture it was compiled for. */
+const char* nsk_version(void);
+
+/* ---- operator lifecycle (sketch.hpp:42-59) ------------------------------ */
+
+/* SketchOperator::draw.  s >= 1, m >= 1; s <= m for srft/srdct/srht; srht
+ * additionally needs m to be a power of two.  Draws the sample indices
+ * (Fisher-Yates over stream (seed, 0) after the m sign words) on the host. */
+int nsk_op_draw(int kind, int64_t s, int64_t m, uint64_t seed, nsk_operator** out);
+
+void nsk_op_destroy(nsk_operator* op);
+
+int nsk_op_info(const nsk_operator* op, int* kind, int64_t* s, int64_t* m, uint64_t* seed,
+                uint64_t* id);
+
+/* Sorted sample R (s indices) for srft/srdct/srht; NSK_EINVAL otherwise. */
+int nsk_op_sample_indices(const nsk_operator* op, int64_t* idx_host);
+
+/* JSON descriptor {"format":1,"kind":..,"s":..,"m":..,"seed":..,"appended":0,
+ * "zeroed_rows":[]} (sketch.cpp:303-313).  Writes at most cap bytes including
+ * the terminating NUL; *len receives the length without NUL. */
+int nsk_op_descriptor(const nsk_operator* op, char* buf, size_t cap, size_t* len);
+
+/* SketchOperator::from_descriptor (sketch.cpp:315-337).  Only appended = 0
+ * and no zeroed rows are accepted by this build. */
+int nsk_op_from_descriptor(const char* json, nsk_operator** out);
+
+/* ---- apply (sketch.hpp:89) ---------------------------------------------- */
+
+/* SA (s x n) = S A (m x n) on the device.  ldsa >= s.  For srft with
+ * NSK_REAL input, SA is complex (interleaved) as in the reference. */
+int nsk_apply(const nsk_operator* op, int scalar, int64_t m, int64_t n, const void* A,
+              int64_t lda, void* SA, int64_t ldsa, void* stream);
+
+/* Row shard of apply for multi-GPU: the caller holds local rows
+ * j = 0..mloc-1 of A, which are global rows row0 + rstep*j.  Writes the
+ * partial SA_g = S[:, rows] A_g; the sum of the partials over a partition of
+ * the rows is apply(S, A).  gaussian/countsketch/srht need rstep == 1
+ * (contiguous shards); srft/srdct accept any rstep (cyclic shards). */
+int nsk_apply_shard(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep,
+                    int64_t mloc, int64_t n, const void* A, int64_t lda, void* SA,
+                    int64_t ldsa, void* stream);
+
+/* ---- solve (nullspace.hpp:24-33) ---------------------------------------- */
+
+/* Trailing k right singular vectors of a sketch SA (s x n, s >= n > k >= 0)
+ * by on-device one-sided Jacobi: W (n x k, column k-1 belongs to the
+ * smallest singular value) and all n singular values, non-increasing, into
+ * sigma (device, n doubles).  W has the scalar kind of SA. */
+int nsk_svd_trailing(int scalar, int64_t s, int64_t n, const void* SA, int64_t ldsa, int64_t k,
+                     void* W, int64_t ldw, double* sigma, void* stream);
+
+/* solve_k: apply, then nsk_svd_trailing.  Device pointers. */
+int nsk_solve_k(const nsk_operator* op, int scalar, int64_t m, int64_t n, const void* A,
+                int64_t lda, int64_t k, void* W, int64_t ldw, double* sigma, void* stream);
+
+/* solve_tol: k = number of sketched singular values below eps; selecting
+ * all n is NSK_EINVAL.  W must hold n x (n-1) entries; *k_out (host) is
+ * written after the stream has been synchronised. */
+int nsk_solve_tol(const nsk_operator* op, int scalar, int64_t m, int64_t n, const void* A,
+                  int64_t lda, double eps, int64_t* k_out, void* W, int64_t ldw, double* sigma,
+                  void* stream);
+
+/* ||A W||_F in one pass over A (device pointers; *out on the host). */
+int nsk_residual_fro(int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k,
+                     const void* W, int64_t ldw, double* out, void* stream);
+
+/* ---- host-buffer entry points (the reference's value semantics) --------- */
+
+int nsk_apply_host(const nsk_operator* op, int scalar, int64_t m, int64_t n, const void* A,
+                   int64_t lda, void* SA, int64_t ldsa);
+
+int nsk_solve_k_host(const nsk_operator* op, int scalar, int64_t m, int64_t n, const void* A,
+                     int64_t lda, int64_t k, void* W, int64_t ldw, double* sigma);
+
+int nsk_solve_tol_host(const nsk_operator* op, int scalar, int64_t m, int64_t n, const void* A,
+                       int64_t lda, double eps, int64_t* k_out, void* W, int64_t ldw,
+                       double* sigma);
+
+/* ---- instrumentation (bench.py; no effect on results) ------------------- */
+
+/* Number of CUDA kernels this library has launched in this process. */
+int64_t nsk_kernel_launches(void);
+
+/* When enabled, every apply records CUDA events around its dominant kernel
+ * (gaussian_sketch / srht / countsketch / srtt main kernel) on the caller's
+ * stream; nsk_timing_collect synchronises those events, returns the summed
+ * duration and count since the last collect, and clears them. */
+void nsk_timing_enable(int on);
+int nsk_timing_collect(double* total_ms, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NULLSKETCH_B200_H */

@@ -1,0 +1,356 @@
+"""CPU restatement (oracle) of the reference's sketch-and-solve hot path.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs import this module,
+and only as the checker or the CPU baseline.  The product package
+``paper_2206_00975_b200`` never imports it and fails loudly when its CUDA
+library is missing.
+
+What it restates (file:line relative to /root/reference):
+
+* draws                 proj/src/sketch.cpp:103-128, proj/include/nullsketch/rng.hpp
+                        (bit-exact, via the plain-C restatement nsk_oracle.c,
+                        itself pinned against the compiled reference header)
+* apply, gaussian       proj/src/sketch.cpp:195-205 (+ real_times_complex 18-25)
+* apply, srft           proj/src/sketch.cpp:206-217 + transforms.cpp:17-36
+                        (FFTW_BACKWARD then 1/sqrt(m)  ==  numpy.fft.ifft(norm="ortho"))
+* apply, srdct          proj/src/sketch.cpp:218-229 + transforms.cpp:38-64
+                        (pre-scaled REDFT01  ==  scipy.fft.dct(type=3, norm="ortho"))
+* solve_k / solve_tol   proj/src/nullspace.cpp:10-53 (Eigen BDCSVD -> LAPACK gesdd)
+* residual_certificate  proj/src/nullspace.cpp:55-62
+* canonical angles      proj/src/kernels.cpp:121-167 (complement projection)
+* make_test_matrix      proj/src/kernels.cpp:169-203
+
+Kinds with no reference implementation (SPEC.md:15,210 list them as
+non-goals) -- parity for these is *unpinned* beyond their draws:
+
+* srht         SA = sqrt(m/s) R H D A, H the normalised Sylvester Hadamard
+               matrix, m a power of two, draws identical to srdct.
+* countsketch  SA[h(i), :] += sigma(i) A[i, :]; sigma(i) = next_sign() #i and
+               h(i) = next_below(s) #i issued after the m signs on stream
+               (seed, 0).
+
+Third-party arithmetic the reference delegates (absent here, so restated by
+its published definition): Eigen >= 3.4 (GEMM, BDCSVD, HouseholderQR) and FFTW3
+(REDFT01, BACKWARD DFT) -- CMakeLists.txt:131,133, versions unpinned upstream.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+_REF = None
+
+KINDS = ("gaussian", "srft", "srdct", "srht", "countsketch")
+
+c_u64 = ctypes.c_uint64
+c_i64 = ctypes.c_int64
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int64)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+
+def build():
+    """Compile the C restatement (and the reference RNG harness where possible)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "libnsk_oracle.so")
+        if not os.path.exists(path):
+            build()
+        L = ctypes.CDLL(path)
+        L.nsko_words.argtypes = [c_u64, c_u64, c_u64, c_u64, _u32p]
+        L.nsko_gaussians.argtypes = [c_u64, c_u64, c_u64, c_u64, _dp]
+        L.nsko_signs.argtypes = [c_u64, c_i64, _dp]
+        L.nsko_sample_indices.argtypes = [c_u64, c_i64, c_i64, _ip]
+        L.nsko_sample_indices.restype = ctypes.c_int
+        L.nsko_countsketch_draw.argtypes = [c_u64, c_i64, c_i64, _i32p, _dp]
+        L.nsko_countsketch_apply.argtypes = [c_u64, c_i64, c_i64, c_i64, _dp, c_i64, _dp, c_i64]
+        L.nsko_gaussian_block.argtypes = [c_u64, c_u64, c_i64, c_i64, c_i64, _dp, ctypes.c_int]
+        L.nsko_srht_apply.argtypes = [_dp, _ip, c_i64, c_i64, c_i64, _dp, c_i64, _dp, c_i64,
+                                      c_i64, c_i64, ctypes.c_int]
+        L.nsko_fwht.argtypes = [_dp, c_i64]
+        _LIB = L
+    return _LIB
+
+
+def ref_lib():
+    """The reference's own rng.hpp compiled unmodified (oracle/_ref), or None."""
+    global _REF
+    if _REF is None:
+        path = os.path.join(_HERE, "_ref", "libnsk_ref.so")
+        if not os.path.exists(path):
+            return None
+        L = ctypes.CDLL(path)
+        L.nskref_words.argtypes = [c_u64, c_u64, c_u64, _u32p]
+        L.nskref_gaussians.argtypes = [c_u64, c_u64, c_u64, _dp]
+        L.nskref_doubles.argtypes = [c_u64, c_u64, c_u64, _dp]
+        L.nskref_gaussian_G.argtypes = [c_u64, c_i64, c_i64, _dp]
+        L.nskref_srtt_draw.argtypes = [c_u64, c_i64, c_i64, _dp, _ip]
+        L.nskref_countsketch_draw.argtypes = [c_u64, c_i64, c_i64, _i32p, _dp]
+        L.nskref_update_gaussians.argtypes = [c_u64, c_i64, c_i64, _dp]
+        _REF = L
+    return _REF
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+# ----------------------------------------------------------------------------- draws
+
+def words(seed, stream, first, count):
+    out = np.empty(count, dtype=np.uint32)
+    lib().nsko_words(seed, stream, first, count, _p(out, _u32p))
+    return out
+
+
+def gaussians(seed, stream, first, count):
+    out = np.empty(count, dtype=np.float64)
+    lib().nsko_gaussians(seed, stream, first, count, _p(out, _dp))
+    return out
+
+
+def signs(seed, m):
+    out = np.empty(m, dtype=np.float64)
+    lib().nsko_signs(seed, m, _p(out, _dp))
+    return out
+
+
+def sample_indices(seed, m, s):
+    out = np.empty(s, dtype=np.int64)
+    rc = lib().nsko_sample_indices(seed, m, s, _p(out, _ip))
+    if rc != 0:
+        raise ValueError("sample_indices: need 0 <= s <= m")
+    return out
+
+
+def countsketch_draw(seed, m, s):
+    b = np.empty(m, dtype=np.int32)
+    g = np.empty(m, dtype=np.float64)
+    lib().nsko_countsketch_draw(seed, m, s, _p(b, _i32p), _p(g, _dp))
+    return b, g
+
+
+def gaussian_block(seed, s, j0, j1, stream=0, nthreads=None):
+    """Columns j0..j1-1 of the s x m Gaussian G (sketch.cpp:117-121), s x (j1-j0)."""
+    out = np.empty((j1 - j0) * s, dtype=np.float64)
+    lib().nsko_gaussian_block(seed, stream, s, j0, j1, _p(out, _dp), nthreads or os.cpu_count())
+    return out.reshape(j1 - j0, s).T
+
+
+class OracleOperator:
+    """Mirror of SketchOperator's draw state (sketch.hpp:40-81) for the oracle."""
+
+    def __init__(self, kind, s, m, seed):
+        if kind not in KINDS:
+            raise ValueError(f"unknown sketch kind: {kind}")
+        if s < 1 or m < 1:
+            raise ValueError("sketch draw: s and m must be positive")
+        if kind in ("srft", "srdct", "srht") and s > m:
+            raise ValueError("sketch draw: subsampled transforms need s <= m")
+        if kind == "srht" and (m & (m - 1)) != 0:
+            raise ValueError("sketch draw: srht needs m to be a power of two")
+        self.kind, self.s, self.m, self.seed = kind, s, m, seed
+        self.signs = self.idx = self.bucket = None
+        if kind in ("srft", "srdct", "srht"):
+            self.signs = signs(seed, m)
+            self.idx = sample_indices(seed, m, s)
+        elif kind == "countsketch":
+            self.bucket, self.signs = countsketch_draw(seed, m, s)
+
+    def dense(self):
+        """Explicit s x m matrix (small sizes only), as SketchOperator::dense (sketch.cpp:162-172)."""
+        eye = np.eye(self.m)
+        return apply(self, eye)
+
+
+def draw(kind, s, m, seed):
+    return OracleOperator(kind, s, m, seed)
+
+
+# ----------------------------------------------------------------------------- apply
+
+def apply(op: OracleOperator, A, col_range=None):
+    """SA = S A for every kind (sketch.cpp:184-232)."""
+    A = np.asarray(A)
+    if A.ndim == 1:
+        A = A[:, None]
+    if A.shape[0] != op.m:
+        raise ValueError(f"sketch apply: matrix has {A.shape[0]} rows, operator expects {op.m}")
+    s, m = op.s, op.m
+    if op.kind == "gaussian":
+        inv = 1.0 / math.sqrt(s)
+        out = np.zeros((s, A.shape[1]), dtype=A.dtype)
+        blk = max(1, min(m, (1 << 26) // max(s, 1)))
+        for j0 in range(0, m, blk):  # streamed: G is regenerated by column blocks
+            j1 = min(m, j0 + blk)
+            G = gaussian_block(op.seed, s, j0, j1)
+            if np.iscomplexobj(A):  # real_times_complex (sketch.cpp:18-25)
+                out += G @ A[j0:j1].real + 1j * (G @ A[j0:j1].imag)
+            else:
+                out += G @ A[j0:j1]
+        return inv * out
+    if op.kind == "srft":
+        top = op.signs[:, None] * A.astype(np.complex128)
+        top = np.fft.ifft(top, axis=0, norm="ortho")
+        return math.sqrt(m / s) * top[op.idx]
+    if op.kind == "srdct":
+        if np.iscomplexobj(A):
+            raise ValueError("srdct sketch is defined for real matrices only")
+        import scipy.fft
+        top = scipy.fft.dct(op.signs[:, None] * A, type=3, norm="ortho", axis=0)
+        return math.sqrt(m / s) * top[op.idx]
+    if op.kind == "srht":
+        if np.iscomplexobj(A):
+            raise ValueError("srht sketch is defined for real matrices only")
+        A = np.asfortranarray(A, dtype=np.float64)
+        n = A.shape[1]
+        c0, c1 = col_range or (0, n)
+        SA = np.zeros((s, n), dtype=np.float64, order="F")
+        lib().nsko_srht_apply(_p(op.signs, _dp), _p(op.idx, _ip), s, m, n, _p(A, _dp), m,
+                              _p(SA, _dp), s, c0, c1, os.cpu_count())
+        return SA
+    if op.kind == "countsketch":
+        if np.iscomplexobj(A):
+            raise ValueError("countsketch is defined for real matrices only")
+        A = np.asfortranarray(A, dtype=np.float64)
+        n = A.shape[1]
+        SA = np.zeros((s, n), dtype=np.float64, order="F")
+        lib().nsko_countsketch_apply(op.seed, s, m, n, _p(A, _dp), m, _p(SA, _dp), s)
+        return SA
+    raise ValueError(op.kind)
+
+
+# ----------------------------------------------------------------------------- solve
+
+def svd(a):
+    """Thin SVD, S non-increasing (kernels.cpp:14-22, 54-70); V returned (not V^*)."""
+    if a.size == 0:
+        raise ValueError("svd: matrix is empty")
+    u, sv, vh = np.linalg.svd(a, full_matrices=False)
+    return u, sv, vh.conj().T
+
+
+def from_sketch_svd(sa, k):
+    n = sa.shape[1]
+    if k < 0 or k >= n:
+        raise ValueError(f"nullspace: k must satisfy 0 <= k < n, got k = {k}, n = {n}")
+    _, sv, v = svd(sa)
+    return v[:, n - k:], sv
+
+
+def solve_k(A, k, op):
+    """W = trailing k right singular vectors of SA; all n sketched sigmas (nullspace.cpp:23-32)."""
+    if A.shape[0] != op.m:
+        raise ValueError("nullspace: matrix rows do not match the sketch operator")
+    if op.s < A.shape[1]:
+        raise ValueError(f"nullspace: sketch size s = {op.s} is smaller than n = {A.shape[1]}")
+    return from_sketch_svd(apply(op, A), k)
+
+
+def solve_tol(A, eps, op):
+    """k = number of sketched singular values below eps (nullspace.cpp:34-53)."""
+    if not (eps >= 0.0):
+        raise ValueError("nullspace: eps must be non-negative")
+    if A.shape[0] != op.m:
+        raise ValueError("nullspace: matrix rows do not match the sketch operator")
+    if op.s < A.shape[1]:
+        raise ValueError("nullspace: sketch size is smaller than n")
+    sa = apply(op, A)
+    _, sv, v = svd(sa)
+    n = sa.shape[1]
+    k = 0
+    while k < n and sv[n - 1 - k] < eps:
+        k += 1
+    if k == n:
+        raise ValueError("nullspace: eps selects every singular value")
+    return v[:, n - k:], sv, k
+
+
+def residual_certificate(A, W):
+    """||A W||_F (nullspace.cpp:55-62)."""
+    if A.shape[1] != W.shape[0]:
+        raise ValueError("residual_certificate: dimension mismatch")
+    return float(np.linalg.norm(A @ W))
+
+
+# ----------------------------------------------------------------------------- angles
+
+def complement_sines(big, small):
+    """Singular values of small - big (big^* small), descending (kernels.cpp:121-128)."""
+    cross = big.conj().T @ small
+    resid = small - big @ cross
+    return np.linalg.svd(resid, compute_uv=False)
+
+
+def sin_theta(U, V):
+    """sin of the largest canonical angle, spectral (kernels.cpp:153-167)."""
+    if U.shape[1] == 0 or V.shape[1] == 0:
+        return 0.0
+    big, small = (U, V) if U.shape[1] >= V.shape[1] else (V, U)
+    return float(min(1.0, complement_sines(big, small)[0]))
+
+
+def canonical_angles(U, V):
+    """Canonical angles ascending (kernels.cpp:132-151)."""
+    big, small = (U, V) if U.shape[1] >= V.shape[1] else (V, U)
+    k = small.shape[1]
+    if k == 0:
+        return np.zeros(0)
+    cos = np.linalg.svd(big.conj().T @ small, compute_uv=False)
+    sin = complement_sines(big, small)
+    out = np.empty(k)
+    for i in range(k):
+        c = min(1.0, max(0.0, cos[i]))
+        s_ = min(1.0, max(0.0, sin[k - 1 - i]))
+        out[i] = math.asin(s_) if c >= math.sqrt(0.5) else math.acos(c)
+    return out
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def thin_qr(a):
+    """Householder thin QR with diag(R) made non-negative (kernels.cpp:32-50)."""
+    q, r = np.linalg.qr(a, mode="reduced")
+    d = np.sign(np.diag(r))
+    d[d == 0] = 1.0
+    return q * d, (r.T * d).T
+
+
+def make_test_matrix(m, n, spectrum, seed, left="haar"):
+    """U diag(spectrum) V^T (kernels.cpp:169-203): U = Q of stream-1 Gaussians
+    (column-major, m x n), V = Q of stream-2 Gaussians (n x n)."""
+    spectrum = np.asarray(spectrum, dtype=np.float64)
+    if m < n:
+        raise ValueError("make_test_matrix: need m >= n")
+    if left == "coherent":
+        u = np.zeros((m, n))
+        u[:n, :n] = np.eye(n)
+    else:
+        g = gaussians(seed, 1, 0, m * n).reshape(n, m).T
+        u = thin_qr(g)[0]
+    gv = gaussians(seed, 2, 0, n * n).reshape(n, n).T
+    v = thin_qr(gv)[0]
+    return np.asfortranarray((u * spectrum) @ v.T)
+
+
+def random_real(m, n, seed):
+    """Test fixture of the reference (tests/test_support.hpp:18-24): stream 77."""
+    return np.asfortranarray(gaussians(seed, 77, 0, m * n).reshape(n, m).T)
+
+
+def random_complex(m, n, seed):
+    """Test fixture of the reference (tests/test_support.hpp:26-33): stream 78, (re, im) pairs."""
+    g = gaussians(seed, 78, 0, 2 * m * n).reshape(n, m, 2)
+    return np.asfortranarray((g[..., 0] + 1j * g[..., 1]).T)

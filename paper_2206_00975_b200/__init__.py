@@ -1,0 +1,12 @@
+"""nullsketch-b200: B200-native sketch-and-solve null-space hot path.
+
+Public API mirrors the reference's sketch / nullspace modules
+(/root/reference/proj/include/nullsketch/sketch.hpp, nullspace.hpp); the
+compute runs in libnullsketch_b200.so (hand-written sm_100a CUDA) through the
+C ABI declared in include/nullsketch_b200.h.
+"""
+from .sketch import (KINDS, NullspaceResult, SketchedMatrix, SketchOperator, SvdConvergenceError, apply,
+                     apply_shard, default_sketch_size, residual_certificate, solve_k, solve_tol, svd_trailing)
+
+__all__ = ["KINDS", "NullspaceResult", "SketchedMatrix", "SketchOperator", "SvdConvergenceError", "apply",
+           "apply_shard", "default_sketch_size", "residual_certificate", "solve_k", "solve_tol", "svd_trailing"]

@@ -1,0 +1,405 @@
+// capi.cpp -- the extern "C" boundary (include/nullsketch_b200.h).
+//
+// Argument validation and error texts follow the reference
+// (/root/reference/proj/src/sketch.cpp:103-107,184-188,219-221;
+//  nullspace.cpp:10-53; kernels.cpp:54-57): std::invalid_argument becomes
+// NSK_EINVAL, SvdConvergenceError NSK_ENOCONV, with nsk_last_error() holding
+// the message.  No CPU fallback exists: every compute entry point launches
+// the CUDA kernels of this library or fails.
+#include <cinttypes>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nullsketch_b200.h"
+#include "nsk_internal.hpp"
+
+using nsk::Operator;
+
+namespace nsk {
+const char* last_error();
+}
+
+namespace {
+
+inline Operator* OP(nsk_operator* h) { return reinterpret_cast<Operator*>(h); }
+inline const Operator* OP(const nsk_operator* h) { return reinterpret_cast<const Operator*>(h); }
+inline cudaStream_t ST(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_op(const nsk_operator* h) {
+  if (!h) return nsk::fail(nsk::EINVAL_, "null sketch operator");
+  return nsk::OK;
+}
+
+// Output scalar kind of apply(): srft -> complex, gaussian keeps the input kind,
+// the rest are real-only (sketch.hpp:86-88).
+int out_ncomp(const Operator& op, int in_ncomp) {
+  if (op.kind == nsk::SRFT) return 2;
+  return in_ncomp;
+}
+
+int validate_apply(const Operator& op, int scalar, int64_t m, int64_t n, const void* A, int64_t lda,
+                   const void* SA, int64_t ldsa, bool shard) {
+  if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "unknown scalar kind");
+  if (!shard && m != op.m)
+    return nsk::fail(nsk::EINVAL_, "sketch apply: matrix has " + std::to_string(m) + " rows, operator expects " +
+                                       std::to_string(op.m));
+  if (n < 0 || m < 0) return nsk::fail(nsk::EINVAL_, "sketch apply: negative dimension");
+  if (scalar == NSK_COMPLEX && op.kind == nsk::SRDCT)
+    return nsk::fail(nsk::EINVAL_, "srdct sketch is defined for real matrices only");
+  if (scalar == NSK_COMPLEX && op.kind == nsk::SRHT)
+    return nsk::fail(nsk::EINVAL_, "srht sketch is defined for real matrices only");
+  if (scalar == NSK_COMPLEX && op.kind == nsk::COUNTSKETCH)
+    return nsk::fail(nsk::EINVAL_, "countsketch is defined for real matrices only");
+  if (lda < (m > 1 ? m : 1)) return nsk::fail(nsk::EINVAL_, "sketch apply: lda < rows");
+  if (ldsa < op.s) return nsk::fail(nsk::EINVAL_, "sketch apply: ldsa < s");
+  if (n > 0 && m > 0 && !A) return nsk::fail(nsk::EINVAL_, "sketch apply: null A");
+  if (n > 0 && !SA) return nsk::fail(nsk::EINVAL_, "sketch apply: null SA");
+  return nsk::OK;
+}
+
+int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
+                   double* SA, int64_t ldsa, cudaStream_t st) {
+  switch (op.kind) {
+    case nsk::GAUSSIAN: return nsk::gaussian_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+    case nsk::SRFT:
+    case nsk::SRDCT: return nsk::srtt_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+    case nsk::SRHT: return nsk::srht_apply(op, rows, n, A, lda, SA, ldsa, st);
+    case nsk::COUNTSKETCH: return nsk::countsketch_apply(op, rows, n, A, lda, SA, ldsa, st);
+  }
+  return nsk::fail(nsk::EINVAL_, "unknown sketch kind");
+}
+
+// Minimal JSON field readers for the descriptor (flat object, known keys).
+bool json_find(const std::string& js, const std::string& key, size_t& pos) {
+  const std::string pat = "\"" + key + "\"";
+  size_t p = js.find(pat);
+  if (p == std::string::npos) return false;
+  p = js.find(':', p + pat.size());
+  if (p == std::string::npos) return false;
+  ++p;
+  while (p < js.size() && (js[p] == ' ' || js[p] == '\t' || js[p] == '\n' || js[p] == '\r')) ++p;
+  pos = p;
+  return p < js.size();
+}
+bool json_u64(const std::string& js, const std::string& key, uint64_t& out, bool& neg) {
+  size_t p;
+  if (!json_find(js, key, p)) return false;
+  neg = false;
+  if (js[p] == '-') {
+    neg = true;
+    ++p;
+  }
+  if (p >= js.size() || js[p] < '0' || js[p] > '9') return false;
+  uint64_t v = 0;
+  while (p < js.size() && js[p] >= '0' && js[p] <= '9') v = v * 10 + static_cast<uint64_t>(js[p++] - '0');
+  out = v;
+  return true;
+}
+bool json_str(const std::string& js, const std::string& key, std::string& out) {
+  size_t p;
+  if (!json_find(js, key, p) || js[p] != '"') return false;
+  size_t e = js.find('"', p + 1);
+  if (e == std::string::npos) return false;
+  out = js.substr(p + 1, e - p - 1);
+  return true;
+}
+
+int kind_from_name(const std::string& k) {
+  for (int i = 0; i <= nsk::COUNTSKETCH; ++i)
+    if (k == nsk::kind_name(i)) return i;
+  return -1;
+}
+
+// A per-thread non-blocking stream for the host-buffer entry points.
+cudaStream_t host_stream() {
+  thread_local cudaStream_t st = nullptr;
+  thread_local int dev = -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (!st || dev != cur) {
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    dev = cur;
+  }
+  return st;
+}
+
+int copy_in(const void* host, int64_t rows, int64_t cols, int64_t ld, int ncomp, double** dev, nsk::Scratch& s,
+            cudaStream_t st) {
+  const size_t elem = sizeof(double) * ncomp;
+  NSK_CUDA_OK(s.alloc(elem * (rows > 0 ? rows : 1) * (cols > 0 ? cols : 1), st));
+  *dev = s.as<double>();
+  if (rows > 0 && cols > 0)
+    NSK_CUDA_OK(cudaMemcpy2DAsync(*dev, elem * rows, host, elem * ld, elem * rows, cols, cudaMemcpyHostToDevice, st));
+  return nsk::OK;
+}
+
+int copy_out(void* host, int64_t ld, const double* dev, int64_t rows, int64_t cols, int ncomp, cudaStream_t st) {
+  const size_t elem = sizeof(double) * ncomp;
+  if (rows > 0 && cols > 0)
+    NSK_CUDA_OK(cudaMemcpy2DAsync(host, elem * ld, dev, elem * rows, elem * rows, cols, cudaMemcpyDeviceToHost, st));
+  return nsk::OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nsk_last_error(void) { return nsk::last_error(); }
+
+const char* nsk_version(void) { return "nullsketch-b200 0.1 (sm_100a, FP64 DMMA + CUDA cores)"; }
+
+int nsk_op_draw(int kind, int64_t s, int64_t m, uint64_t seed, nsk_operator** out) {
+  Operator* op = nullptr;
+  int rc = nsk::draw_operator(kind, s, m, seed, &op);
+  if (out) *out = reinterpret_cast<nsk_operator*>(op);
+  return rc;
+}
+
+void nsk_op_destroy(nsk_operator* op) { delete OP(op); }
+
+int nsk_op_info(const nsk_operator* h, int* kind, int64_t* s, int64_t* m, uint64_t* seed, uint64_t* id) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (kind) *kind = op.kind;
+  if (s) *s = op.s;
+  if (m) *m = op.m;
+  if (seed) *seed = op.seed;
+  if (id) *id = op.id;
+  return nsk::OK;
+}
+
+int nsk_op_sample_indices(const nsk_operator* h, int64_t* idx_host) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (op.idx.empty()) return nsk::fail(nsk::EINVAL_, "sample indices exist for srft/srdct/srht only");
+  if (!idx_host) return nsk::fail(nsk::EINVAL_, "null output");
+  std::memcpy(idx_host, op.idx.data(), op.idx.size() * sizeof(int64_t));
+  return nsk::OK;
+}
+
+// nlohmann::json::dump() order (keys sorted) as in sketch.cpp:303-313.
+int nsk_op_descriptor(const nsk_operator* h, char* buf, size_t cap, size_t* len) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  char tmp[256];
+  int nw = std::snprintf(tmp, sizeof tmp,
+                         "{\"appended\":0,\"format\":1,\"kind\":\"%s\",\"m\":%" PRId64 ",\"s\":%" PRId64
+                         ",\"seed\":%" PRIu64 ",\"zeroed_rows\":[]}",
+                         nsk::kind_name(op.kind), op.m, op.s, op.seed);
+  if (len) *len = static_cast<size_t>(nw);
+  if (!buf || cap < static_cast<size_t>(nw) + 1)
+    return nsk::fail(nsk::ERANGE_, "descriptor: buffer too small (" + std::to_string(nw + 1) + " bytes needed)");
+  std::memcpy(buf, tmp, static_cast<size_t>(nw) + 1);
+  return nsk::OK;
+}
+
+int nsk_op_from_descriptor(const char* json, nsk_operator** out) {
+  if (out) *out = nullptr;
+  if (!json) return nsk::fail(nsk::EINVAL_, "sketch descriptor: null text");
+  const std::string js(json);
+  uint64_t fmt = 0, s = 0, m = 0, seed = 0, app = 0;
+  bool neg = false;
+  if (!json_u64(js, "format", fmt, neg) || neg || fmt != 1)
+    return nsk::fail(nsk::EINVAL_, "sketch descriptor: unsupported format");
+  std::string kind;
+  if (!json_str(js, "kind", kind)) return nsk::fail(nsk::EINVAL_, "sketch descriptor: missing kind");
+  const int k = kind_from_name(kind);
+  if (k < 0) return nsk::fail(nsk::EINVAL_, "unknown sketch kind: " + kind);
+  bool n1 = false, n2 = false, n3 = false;
+  if (!json_u64(js, "s", s, n1) || !json_u64(js, "m", m, n2) || !json_u64(js, "seed", seed, n3) || n1 || n2 || n3)
+    return nsk::fail(nsk::EINVAL_, "sketch descriptor: missing or negative s/m/seed");
+  if (!json_u64(js, "appended", app, neg)) return nsk::fail(nsk::EINVAL_, "sketch descriptor: missing appended");
+  if (neg) return nsk::fail(nsk::EINVAL_, "sketch descriptor: bad appended count");
+  size_t p;
+  if (!json_find(js, "zeroed_rows", p) || js[p] != '[')
+    return nsk::fail(nsk::EINVAL_, "sketch descriptor: missing zeroed_rows");
+  size_t q = js.find(']', p);
+  std::string inner = js.substr(p + 1, q == std::string::npos ? 0 : q - p - 1);
+  bool has_rows = inner.find_first_not_of(" \t\r\n") != std::string::npos;
+  if (has_rows) {
+    // Validate like from_descriptor (sketch.cpp:330-335) before rejecting:
+    // an out-of-range row is a malformed descriptor either way.
+    long long z = std::atoll(inner.c_str());
+    if (z < 0 || static_cast<uint64_t>(z) >= m + app)
+      return nsk::fail(nsk::EINVAL_, "sketch descriptor: bad zeroed row " + std::to_string(z));
+  }
+  if (app != 0 || has_rows)
+    return nsk::fail(nsk::EINVAL_, "sketch descriptor: row updates/downdates are not supported by this build");
+  Operator* op = nullptr;
+  int rc = nsk::draw_operator(k, static_cast<int64_t>(s), static_cast<int64_t>(m), seed, &op);
+  if (out) *out = reinterpret_cast<nsk_operator*>(op);
+  return rc;
+}
+
+int nsk_apply(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, void* SA,
+              int64_t ldsa, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (int rc = validate_apply(op, scalar, m, n, A, lda, SA, ldsa, false)) return rc;
+  nsk::RowMap rows{0, 1, m};
+  return dispatch_apply(op, scalar == NSK_COMPLEX ? 2 : 1, rows, n, static_cast<const double*>(A), lda,
+                        static_cast<double*>(SA), ldsa, ST(stream));
+}
+
+int nsk_apply_shard(const nsk_operator* h, int scalar, int64_t row0, int64_t rstep, int64_t mloc, int64_t n,
+                    const void* A, int64_t lda, void* SA, int64_t ldsa, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (int rc = validate_apply(op, scalar, mloc, n, A, lda, SA, ldsa, true)) return rc;
+  if (rstep < 1 || row0 < 0) return nsk::fail(nsk::EINVAL_, "apply_shard: bad row map");
+  if (mloc > 0 && row0 + rstep * (mloc - 1) >= op.m)
+    return nsk::fail(nsk::ERANGE_, "apply_shard: rows beyond the operator's m");
+  nsk::RowMap rows{row0, rstep, mloc};
+  return dispatch_apply(op, scalar == NSK_COMPLEX ? 2 : 1, rows, n, static_cast<const double*>(A), lda,
+                        static_cast<double*>(SA), ldsa, ST(stream));
+}
+
+int nsk_svd_trailing(int scalar, int64_t s, int64_t n, const void* SA, int64_t ldsa, int64_t k, void* W,
+                     int64_t ldw, double* sigma, void* stream) {
+  if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "unknown scalar kind");
+  if (s < 1 || n < 1) return nsk::fail(nsk::EINVAL_, "svd: matrix is empty");
+  if (k < 0 || k >= n)
+    return nsk::fail(nsk::EINVAL_, "nullspace: k must satisfy 0 <= k < n, got k = " + std::to_string(k) +
+                                       ", n = " + std::to_string(n));
+  if (s < n) return nsk::fail(nsk::EINVAL_, "svd_trailing: needs s >= n");
+  if (ldsa < s || (k > 0 && ldw < n)) return nsk::fail(nsk::EINVAL_, "svd_trailing: bad leading dimension");
+  if (!SA || !sigma || (k > 0 && !W)) return nsk::fail(nsk::EINVAL_, "svd_trailing: null pointer");
+  return nsk::jacobi_trailing(scalar == NSK_COMPLEX ? 2 : 1, s, n, static_cast<const double*>(SA), ldsa, k,
+                              static_cast<double*>(W), ldw, sigma, ST(stream));
+}
+
+static int solve_common(const Operator& op, int scalar, int64_t m, int64_t n, const void* A, int64_t lda,
+                        nsk::Scratch& sa_buf, int& nc_out, cudaStream_t st) {
+  if (m != op.m) return nsk::fail(nsk::EINVAL_, "nullspace: matrix rows do not match the sketch operator");
+  if (op.s < n)
+    return nsk::fail(nsk::EINVAL_, "nullspace: sketch size s = " + std::to_string(op.s) + " is smaller than n = " +
+                                       std::to_string(n));
+  if (int rc = validate_apply(op, scalar, m, n, A, lda, reinterpret_cast<const void*>(1), op.s, false)) return rc;
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1;
+  nc_out = out_ncomp(op, nc_in);
+  NSK_CUDA_OK(sa_buf.alloc(sizeof(double) * op.s * n * nc_out, st));
+  nsk::RowMap rows{0, 1, m};
+  return dispatch_apply(op, nc_in, rows, n, static_cast<const double*>(A), lda, sa_buf.as<double>(), op.s, st);
+}
+
+int nsk_solve_k(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k,
+                void* W, int64_t ldw, double* sigma, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (n < 1) return nsk::fail(nsk::EINVAL_, "nullspace: matrix has no columns");
+  if (k < 0 || k >= n)
+    return nsk::fail(nsk::EINVAL_, "nullspace: k must satisfy 0 <= k < n, got k = " + std::to_string(k) +
+                                       ", n = " + std::to_string(n));
+  cudaStream_t st = ST(stream);
+  nsk::Scratch sa;
+  int nc = 1;
+  if (int rc = solve_common(op, scalar, m, n, A, lda, sa, nc, st)) return rc;
+  return nsk::jacobi_trailing(nc, op.s, n, sa.as<double>(), op.s, k, static_cast<double*>(W), ldw, sigma, st);
+}
+
+int nsk_solve_tol(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, double eps,
+                  int64_t* k_out, void* W, int64_t ldw, double* sigma, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (!(eps >= 0.0)) return nsk::fail(nsk::EINVAL_, "nullspace: eps must be non-negative");
+  if (n < 1) return nsk::fail(nsk::EINVAL_, "nullspace: matrix has no columns");
+  cudaStream_t st = ST(stream);
+  nsk::Scratch sa, wf;
+  int nc = 1;
+  if (int rc = solve_common(op, scalar, m, n, A, lda, sa, nc, st)) return rc;
+  const int64_t kf = n - 1;
+  NSK_CUDA_OK(wf.alloc(sizeof(double) * n * (kf > 0 ? kf : 1) * nc, st));
+  if (int rc = nsk::jacobi_trailing(nc, op.s, n, sa.as<double>(), op.s, kf, wf.as<double>(), n, sigma, st)) return rc;
+  std::vector<double> sv(static_cast<size_t>(n));
+  NSK_CUDA_OK(cudaMemcpyAsync(sv.data(), sigma, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  int64_t k = 0;
+  while (k < n && sv[static_cast<size_t>(n - 1 - k)] < eps) ++k;
+  if (k == n)
+    return nsk::fail(nsk::EINVAL_,
+                     "nullspace: eps selects every singular value; the trailing subspace would be the whole space");
+  if (k_out) *k_out = k;
+  if (k > 0) {
+    const size_t elem = sizeof(double) * nc;
+    NSK_CUDA_OK(cudaMemcpy2DAsync(W, elem * ldw, wf.as<double>() + (kf - k) * n * nc, elem * n, elem * n, k,
+                                  cudaMemcpyDeviceToDevice, st));
+  }
+  return nsk::OK;
+}
+
+int nsk_residual_fro(int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k, const void* W,
+                     int64_t ldw, double* out, void* stream) {
+  if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "unknown scalar kind");
+  if (!out) return nsk::fail(nsk::EINVAL_, "residual_certificate: null output");
+  if (m < 0 || n < 0 || k < 0 || lda < m || (k > 0 && ldw < n))
+    return nsk::fail(nsk::EINVAL_, "residual_certificate: bad dimensions");
+  return nsk::residual_fro(scalar == NSK_COMPLEX ? 2 : 1, m, n, static_cast<const double*>(A), lda, k,
+                           static_cast<const double*>(W), ldw, out, ST(stream));
+}
+
+int nsk_apply_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, void* SA,
+                   int64_t ldsa) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (int rc = validate_apply(op, scalar, m, n, A, lda, SA, ldsa, false)) return rc;
+  cudaStream_t st = host_stream();
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc_out = out_ncomp(op, nc_in);
+  nsk::Scratch a, sa;
+  double* dA = nullptr;
+  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
+  NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * (n > 0 ? n : 1) * nc_out, st));
+  nsk::RowMap rows{0, 1, m};
+  if (int rc = dispatch_apply(op, nc_in, rows, n, dA, m, sa.as<double>(), op.s, st)) return rc;
+  if (int rc = copy_out(SA, ldsa, sa.as<double>(), op.s, n, nc_out, st)) return rc;
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return nsk::OK;
+}
+
+int nsk_solve_k_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k,
+                     void* W, int64_t ldw, double* sigma) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (lda < m) return nsk::fail(nsk::EINVAL_, "solve_k: lda < rows");
+  if (k < 0 || k >= n)
+    return nsk::fail(nsk::EINVAL_, "nullspace: k must satisfy 0 <= k < n, got k = " + std::to_string(k) +
+                                       ", n = " + std::to_string(n));
+  cudaStream_t st = host_stream();
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc_out = out_ncomp(op, nc_in);
+  nsk::Scratch a, w, sg;
+  double* dA = nullptr;
+  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
+  NSK_CUDA_OK(w.alloc(sizeof(double) * n * (k > 0 ? k : 1) * nc_out, st));
+  NSK_CUDA_OK(sg.alloc(sizeof(double) * n, st));
+  if (int rc = nsk_solve_k(h, scalar, m, n, dA, m, k, w.as<double>(), n, sg.as<double>(), st)) return rc;
+  if (int rc = copy_out(W, ldw, w.as<double>(), n, k, nc_out, st)) return rc;
+  NSK_CUDA_OK(cudaMemcpyAsync(sigma, sg.as<double>(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return nsk::OK;
+}
+
+int nsk_solve_tol_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, double eps,
+                       int64_t* k_out, void* W, int64_t ldw, double* sigma) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (lda < m) return nsk::fail(nsk::EINVAL_, "solve_tol: lda < rows");
+  if (n < 1) return nsk::fail(nsk::EINVAL_, "nullspace: matrix has no columns");
+  cudaStream_t st = host_stream();
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc_out = out_ncomp(op, nc_in);
+  nsk::Scratch a, w, sg;
+  double* dA = nullptr;
+  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
+  NSK_CUDA_OK(w.alloc(sizeof(double) * n * n * nc_out, st));
+  NSK_CUDA_OK(sg.alloc(sizeof(double) * n, st));
+  int64_t k = 0;
+  if (int rc = nsk_solve_tol(h, scalar, m, n, dA, m, eps, &k, w.as<double>(), n, sg.as<double>(), st)) return rc;
+  if (int rc = copy_out(W, ldw, w.as<double>(), n, k, nc_out, st)) return rc;
+  NSK_CUDA_OK(cudaMemcpyAsync(sigma, sg.as<double>(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  if (k_out) *k_out = k;
+  return nsk::OK;
+}
+
+}  // extern "C"

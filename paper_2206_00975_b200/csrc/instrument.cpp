@@ -1,0 +1,69 @@
+// instrument.cpp -- launch counter and optional CUDA-event timing of the
+// dominant kernel of each apply (used by bench.py for the roofline figure).
+#include <atomic>
+#include <vector>
+
+#include "../../include/nullsketch_b200.h"
+#include "nsk_internal.hpp"
+
+namespace nsk {
+namespace {
+std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_timing{0};
+struct EvPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+thread_local std::vector<EvPair> t_pending;
+thread_local std::vector<EvPair> t_free;
+}  // namespace
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+KernelTimer::KernelTimer(cudaStream_t s) : st(s) {
+  if (!g_timing.load(std::memory_order_relaxed)) return;
+  EvPair p;
+  if (!t_free.empty()) {
+    p = t_free.back();
+    t_free.pop_back();
+  } else {
+    cudaEventCreate(&p.a);
+    cudaEventCreate(&p.b);
+  }
+  cudaEventRecord(p.a, st);
+  t_pending.push_back(p);
+  pair = &t_pending.back();
+}
+
+void KernelTimer::stop() {
+  if (!pair) return;
+  cudaEventRecord(t_pending.back().b, st);
+  pair = nullptr;
+}
+
+}  // namespace nsk
+
+extern "C" {
+
+int64_t nsk_kernel_launches(void) { return nsk::g_launches.load(); }
+
+void nsk_timing_enable(int on) { nsk::g_timing.store(on ? 1 : 0); }
+
+int nsk_timing_collect(double* total_ms, int64_t* count) {
+  double tot = 0.0;
+  int64_t c = 0;
+  for (auto& p : nsk::t_pending) {
+    cudaError_t e = cudaEventSynchronize(p.b);
+    if (e != cudaSuccess) return nsk::cuda_fail(e, "timing collect");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    tot += ms;
+    ++c;
+    nsk::t_free.push_back(p);
+  }
+  nsk::t_pending.clear();
+  if (total_ms) *total_ms = tot;
+  if (count) *count = c;
+  return nsk::OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,196 @@
+// operator.cpp -- SketchOperator state: draw, descriptor, device tables.
+//
+// Mirrors SketchOperator::draw / descriptor / from_descriptor of the
+// reference (/root/reference/proj/src/sketch.cpp:103-128, 303-337).  The
+// Gaussian matrix is never materialised (the reference stores s*m doubles,
+// sketch.cpp:117-121); signs and hash buckets are regenerated on the device
+// from stream (seed, 0).  Only the sorted sample of s indices is stored.
+#include <algorithm>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+
+#include "nsk_internal.hpp"
+
+namespace nsk {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_next_id{1};
+
+inline uint32_t host_philox_word(PhiloxKey key, uint64_t i) {
+  uint64_t ctr = i >> 2;
+  uint32_t c0 = static_cast<uint32_t>(ctr), c1 = static_cast<uint32_t>(ctr >> 32), c2 = 0, c3 = 0;
+  uint32_t k0 = key.k0, k1 = key.k1;
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = 0xD2511F53ULL * c0, p1 = 0xCD9E8D57ULL * c2;
+    uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ k0;
+    uint32_t n1 = static_cast<uint32_t>(p1);
+    uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ k1;
+    uint32_t n3 = static_cast<uint32_t>(p0);
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint32_t w[4] = {c0, c1, c2, c3};
+  return w[i & 3];
+}
+}  // namespace
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(ECUDA, std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                         cudaGetErrorString(e) + ") in " + what);
+}
+
+const char* last_error() { return g_last_error.c_str(); }
+
+const char* kind_name(int kind) {
+  switch (kind) {
+    case GAUSSIAN: return "gaussian";
+    case SRFT: return "srft";
+    case SRDCT: return "srdct";
+    case SRHT: return "srht";
+    case COUNTSKETCH: return "countsketch";
+  }
+  return "unknown";
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+// rng.hpp:108-121 with the O(m) iota array replaced by a map of the touched
+// positions: position p holds p unless it was swapped.  Step i draws the u64
+// made of stream words m+2i (low) and m+2i+1 (high) -- the m sign words come
+// first (sketch.cpp:122-126).
+std::vector<int64_t> sample_without_replacement(PhiloxKey key, int64_t m, int64_t s) {
+  std::unordered_map<int64_t, int64_t> moved;
+  moved.reserve(static_cast<size_t>(2 * s + 1));
+  auto get = [&](int64_t p) {
+    auto it = moved.find(p);
+    return it == moved.end() ? p : it->second;
+  };
+  for (int64_t i = 0; i < s; ++i) {
+    const uint64_t w = static_cast<uint64_t>(m) + 2u * static_cast<uint64_t>(i);
+    const uint64_t u = (static_cast<uint64_t>(host_philox_word(key, w + 1)) << 32) |
+                       host_philox_word(key, w);
+    const uint64_t below = static_cast<uint64_t>(
+        (static_cast<unsigned __int128>(u) * static_cast<uint64_t>(m - i)) >> 64);
+    const int64_t j = i + static_cast<int64_t>(below);
+    const int64_t vi = get(i), vj = get(j);
+    moved[i] = vj;
+    moved[j] = vi;
+  }
+  std::vector<int64_t> out(static_cast<size_t>(s));
+  for (int64_t i = 0; i < s; ++i) out[static_cast<size_t>(i)] = get(i);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out) {
+  if (!out) return fail(EINVAL_, "sketch draw: null output handle");
+  *out = nullptr;
+  if (kind < GAUSSIAN || kind > COUNTSKETCH)
+    return fail(EINVAL_, "unknown sketch kind: " + std::to_string(kind));
+  if (s < 1 || m < 1) return fail(EINVAL_, "sketch draw: s and m must be positive");
+  if ((kind == SRFT || kind == SRDCT || kind == SRHT) && s > m)
+    return fail(EINVAL_, "sketch draw: subsampled transforms need s <= m");
+  if (kind == SRHT && (m & (m - 1)) != 0)
+    return fail(EINVAL_, "sketch draw: srht needs m to be a power of two (no zero padding)");
+  if (s > (int64_t(1) << 31) || m > (int64_t(1) << 40))
+    return fail(EINVAL_, "sketch draw: sizes beyond the supported range");
+  Operator* op = new (std::nothrow) Operator();
+  if (!op) return fail(ENOMEM_, "sketch draw: out of host memory");
+  op->kind = kind;
+  op->s = s;
+  op->m = m;
+  op->seed = seed;
+  op->id = g_next_id.fetch_add(1);
+  op->key0 = make_key(seed, 0);
+  op->key1 = make_key(seed, 1);
+  if (kind == SRFT || kind == SRDCT || kind == SRHT) {
+    op->idx = sample_without_replacement(op->key0, m, s);
+  }
+  if (kind == SRHT) {
+    int lb = 0;
+    while ((int64_t(1) << lb) < m && lb < 10) ++lb;
+    op->srht_lo_bits = lb;
+    std::vector<int32_t> order(static_cast<size_t>(s));
+    for (int64_t r = 0; r < s; ++r) order[static_cast<size_t>(r)] = static_cast<int32_t>(r);
+    const int64_t mask = (int64_t(1) << lb) - 1;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return (op->idx[a] & mask) < (op->idx[b] & mask);
+    });
+    op->srht_slot.resize(static_cast<size_t>(s));
+    op->srht_row.resize(static_cast<size_t>(s));
+    for (int64_t t = 0; t < s; ++t) {
+      op->srht_row[static_cast<size_t>(t)] = order[static_cast<size_t>(t)];
+      op->srht_slot[static_cast<size_t>(t)] =
+          static_cast<uint32_t>(op->idx[static_cast<size_t>(order[static_cast<size_t>(t)])]);
+    }
+  }
+  *out = op;
+  return OK;
+}
+
+const DeviceTables* Operator::tables() const {
+  int devno = 0;
+  if (cudaGetDevice(&devno) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& t : dev)
+    if (t.device == devno) return &t;
+  DeviceTables t;
+  t.device = devno;
+  auto up = [](void** dst, const void* src, size_t bytes) {
+    if (bytes == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  cudaError_t e = cudaSuccess;
+  if (!idx.empty()) e = up(reinterpret_cast<void**>(&t.idx), idx.data(), idx.size() * 8);
+  if (e == cudaSuccess && !srht_slot.empty())
+    e = up(reinterpret_cast<void**>(&t.srht_slot), srht_slot.data(), srht_slot.size() * 4);
+  if (e == cudaSuccess && !srht_row.empty())
+    e = up(reinterpret_cast<void**>(&t.srht_row), srht_row.data(), srht_row.size() * 4);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "operator table upload");
+    return nullptr;
+  }
+  if (kind == SRHT && m >= 1024 && build_sign_mask(key0, m, &t.sign_mask) != OK) return nullptr;
+  if (kind == COUNTSKETCH && s <= 65536 && build_cs_table(key0, m, s, &t.cs_table) != OK) return nullptr;
+  dev.push_back(t);
+  return &dev.back();
+}
+
+Operator::~Operator() {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& t : dev) {
+    cudaSetDevice(t.device);
+    if (t.idx) cudaFree(t.idx);
+    if (t.srht_slot) cudaFree(t.srht_slot);
+    if (t.srht_row) cudaFree(t.srht_row);
+    if (t.sign_mask) cudaFree(t.sign_mask);
+    if (t.cs_table) cudaFree(t.cs_table);
+  }
+  cudaSetDevice(cur);
+}
+
+}  // namespace nsk

@@ -1,0 +1,272 @@
+// srht_sketch.cu -- K2b: SA = sqrt(m/s) R H D A, H the normalised Hadamard matrix.
+//
+// No reference implementation exists (SPEC.md:15,210 list H-RHT as a
+// non-goal); the draw protocol is the reference's srdct one
+// (sketch.cpp:122-126): D = sign of stream word i, R = sorted Fisher-Yates
+// sample.  With H_m[r, j] = (-1)^popcount(r & j) / sqrt(m):
+//     SA[r, c] = (1/sqrt s) * sum_j (-1)^popcount(idx_r & j) d_j A[j, c].
+//
+// B200 design (HBM-bound, one pass over A):
+//   * split j = j_lo + 1024 j_hi and idx = r_lo + 1024 r_hi, so the sign
+//     factorises: (-1)^popc(r_lo & j_lo) * (-1)^popc(r_hi & j_hi).
+//   * one warp owns a (column, j_hi) block of 1024 contiguous rows (8 KiB):
+//     coalesced 256 B loads, 5 butterfly stages in registers (row bits 5-9),
+//     a padded shared-memory transpose, 5 more stages (row bits 0-4): a full
+//     length-1024 FWHT with no block-wide barrier.
+//   * the warp then gathers the s sampled rows r_lo from shared memory (the
+//     output slots are pre-sorted by r_lo so the gather is nearly
+//     sequential) and accumulates (-1)^popc(r_hi & j_hi) Z[r_lo] in registers.
+//   * persistent warps walk a contiguous range of (column, j_hi) blocks; the
+//     per-warp partial sums are reduced in fixed order by a second kernel.
+//   * the sign diagonal is expanded once per operator into an m-bit mask laid
+//     out so that lane l's 32 rows {l + 32 t} are the bits of one u32.
+#include "nsk_internal.hpp"
+
+namespace nsk {
+
+// ---- sign mask (m/8 bytes), built once per operator and device ------------
+// word[b*32 + l] bit t = (stream word (b*1024 + l + 32 t)) & 1.
+__global__ void build_sign_mask_kernel(PhiloxKey key, int64_t nblocks, uint32_t* __restrict__ out) {
+  const int64_t total = nblocks * 32;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < total;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = w >> 5;
+    const int l = static_cast<int>(w & 31);
+    uint32_t bits = 0;
+#pragma unroll 4
+    for (int t = 0; t < 32; ++t) {
+      const uint64_t row = static_cast<uint64_t>(b) * 1024u + static_cast<uint64_t>(l + 32 * t);
+      bits |= (stream_word(key, row) & 1u) << t;
+    }
+    out[w] = bits;
+  }
+}
+
+int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out) {
+  const int64_t nblocks = m / 1024;
+  *out = nullptr;
+  if (nblocks == 0) return OK;
+  NSK_CUDA_OK(cudaMalloc(out, sizeof(uint32_t) * nblocks * 32));
+  const int64_t total = nblocks * 32;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+  build_sign_mask_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, nblocks, *out);
+  count_launch();
+  NSK_CUDA_OK(cudaGetLastError());
+  NSK_CUDA_OK(cudaDeviceSynchronize());
+  return OK;
+}
+
+namespace {
+
+constexpr int WARPS_PER_CTA = 4;
+constexpr int PADDED = 1024 + 32;  // one pad double per 32: conflict-free transpose
+
+struct SrhtParams {
+  const double* A;
+  int64_t lda;
+  int64_t n;
+  int64_t nb;          // 1024-row blocks per column (local)
+  int64_t jhi0;        // global j_hi of local block 0
+  int64_t total;       // n * nb work items
+  int64_t per;         // items per warp
+  const uint32_t* mask;  // sign mask, global block index
+  const uint32_t* slot;  // s_pass slot values (idx), sorted by r_lo
+  int nslots;
+  double* P;           // partials [warp*2 + seg][NQ*32]
+};
+
+__device__ __forceinline__ void bfly(double& a, double& b) {
+  const double x = a, y = b;
+  a = x + y;
+  b = x - y;
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, 3) srht_kernel(SrhtParams p) {
+  __shared__ double zbuf[WARPS_PER_CTA][PADDED];
+  __shared__ uint32_t sslot[NQ * 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x)
+    sslot[t] = t < p.nslots ? p.slot[t] : 0u;
+  __syncthreads();
+
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * WARPS_PER_CTA + wib;
+  int64_t it = warp * p.per;
+  int64_t end = it + p.per;
+  if (end > p.total) end = p.total;
+  double* z = zbuf[wib];
+
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  int seg = 0;
+  int64_t cur_col = it < end ? it / p.nb : -1;
+
+  for (; it < end; ++it) {
+    const int64_t col = it / p.nb, blk = it - col * p.nb;
+    if (col != cur_col) {  // column boundary: flush segment 0
+      double* P = p.P + (warp * 2 + seg) * (NQ * 32);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        P[q * 32 + lane] = acc[q];
+        acc[q] = 0.0;
+      }
+      seg = 1;
+      cur_col = col;
+    }
+    const double* a = p.A + col * p.lda + blk * 1024 + lane;
+    double x[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) x[t] = __ldcs(a + 32 * t);  // streamed once: evict-first
+    const int64_t jhi = p.jhi0 + blk;
+    const uint32_t sm = __ldg(p.mask + jhi * 32 + lane);
+    // D: flip the sign where the stream bit is 0 (rng.hpp:57).
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const uint32_t flip = ((~sm) >> t) & 1u;
+      x[t] = __hiloint2double(__double2hiint(x[t]) ^ static_cast<int>(flip << 31), __double2loint(x[t]));
+    }
+    // Stages on row bits 5..9 (register index t).
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if ((t & h) == 0) bfly(x[t], x[t + h]);
+    // Transpose through shared memory: row j at j + j/32.
+#pragma unroll
+    for (int t = 0; t < 32; ++t) z[lane + 33 * t] = x[t];
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 32; ++u) x[u] = z[33 * lane + u];
+    // Stages on row bits 0..4 (register index u); lane now holds rows 32*lane + u.
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if ((u & h) == 0) bfly(x[u], x[u + h]);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 32; ++u) z[33 * lane + u] = x[u];
+    __syncwarp();
+    // Sampled second stage.
+    const uint32_t jh = static_cast<uint32_t>(jhi);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t v = sslot[q * 32 + lane];
+      const uint32_t rlo = v & 1023u, rhi = v >> 10;
+      const double zz = z[rlo + (rlo >> 5)];
+      acc[q] += (__popc(rhi & jh) & 1) ? -zz : zz;
+    }
+    __syncwarp();
+  }
+  if (cur_col >= 0) {
+    double* P = p.P + (warp * 2 + seg) * (NQ * 32);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) P[q * 32 + lane] = acc[q];
+  }
+}
+
+// SA[row(t), c] = scale * sum over the warps that touched column c, in warp order.
+__global__ void srht_reduce(const double* __restrict__ P, int64_t nb, int64_t per, int64_t n, int nslots,
+                            int slot_stride, const int32_t* __restrict__ row_of_slot, double scale,
+                            double* __restrict__ SA, int64_t ldsa, int slot_base) {
+  const int64_t total = n * nslots;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / nslots;
+    const int t = static_cast<int>(e % nslots);
+    const int64_t first = c * nb, last = (c + 1) * nb - 1;
+    const int64_t w0 = first / per, w1 = last / per;
+    double v = 0.0;
+    for (int64_t w = w0; w <= w1; ++w) {
+      const int64_t wstart = w * per;
+      const int seg = (wstart / nb == c) ? 0 : 1;
+      v += P[(w * 2 + seg) * slot_stride + t];
+    }
+    SA[row_of_slot[slot_base + t] + c * ldsa] = scale * v;
+  }
+}
+
+// Small or misaligned shards: direct evaluation, O(s * mloc) per column.
+__global__ void srht_direct(const double* __restrict__ A, int64_t lda, int64_t mloc, int64_t row0,
+                            int64_t n, const int64_t* __restrict__ idx, int64_t s, PhiloxKey key,
+                            double scale, double* __restrict__ SA, int64_t ldsa) {
+  const int64_t total = s * n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / s, r = e % s;
+    const uint64_t ir = static_cast<uint64_t>(idx[r]);
+    double v = 0.0;
+    for (int64_t j = 0; j < mloc; ++j) {
+      const uint64_t g = static_cast<uint64_t>(row0 + j);
+      double a = apply_sign(A[j + c * lda], stream_word(key, g));
+      v += (__popcll(ir & g) & 1) ? -a : a;
+    }
+    SA[r + c * ldsa] = scale * v;
+  }
+}
+
+template <int NQ>
+int launch_srht(SrhtParams p, int64_t warps, cudaStream_t st) {
+  const int64_t ctas = (warps + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  KernelTimer tm(st);
+  srht_kernel<NQ><<<static_cast<unsigned>(ctas), WARPS_PER_CTA * 32, 0, st>>>(p);
+  tm.stop();
+  count_launch();
+  NSK_CUDA_OK(cudaGetLastError());
+  return OK;
+}
+
+}  // namespace
+
+int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+               double* SA, int64_t ldsa, cudaStream_t st) {
+  const int64_t s = op.s, mloc = rows.mloc;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(s));
+  if (n == 0) return OK;
+  const DeviceTables* tb = op.tables();
+  if (!tb) return ECUDA;
+  if (rows.rstep != 1) return fail(EINVAL_, "srht shard: rows must be contiguous (rstep 1)");
+  const bool blocked = op.m >= 1024 && mloc >= 1024 && (mloc % 1024) == 0 && (rows.row0 % 1024) == 0 &&
+                       tb->sign_mask != nullptr;
+  if (!blocked) {
+    int64_t blocks = (s * n + 127) / 128;
+    if (blocks > 16L * sm_count()) blocks = 16L * sm_count();
+    srht_direct<<<static_cast<unsigned>(blocks), 128, 0, st>>>(A, lda, mloc, rows.row0, n, tb->idx, s, op.key0,
+                                                               scale, SA, ldsa);
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+    return OK;
+  }
+  const int64_t nb = mloc / 1024;
+  const int64_t total = n * nb;
+  const int64_t max_warps = static_cast<int64_t>(sm_count()) * 3 * WARPS_PER_CTA;
+  int64_t warps = total < max_warps ? total : max_warps;
+  int64_t per = (total + warps - 1) / warps;
+  if (per > nb) per = nb;  // a warp touches at most two columns
+  warps = (total + per - 1) / per;
+  // Outputs in passes of at most 1024 slots (one register accumulator each).
+  for (int64_t base = 0; base < s; base += 1024) {
+    const int ns = static_cast<int>((s - base) < 1024 ? (s - base) : 1024);
+    const int nq = (ns + 31) / 32;
+    const int NQ = nq <= 8 ? 8 : (nq <= 16 ? 16 : 32);
+    Scratch part;
+    NSK_CUDA_OK(part.alloc(sizeof(double) * warps * 2 * NQ * 32, st));
+    SrhtParams p{A, lda, n, nb, rows.row0 / 1024, total, per, tb->sign_mask, tb->srht_slot + base, ns,
+                 part.as<double>()};
+    int rc = NQ == 8 ? launch_srht<8>(p, warps, st) : (NQ == 16 ? launch_srht<16>(p, warps, st)
+                                                                : launch_srht<32>(p, warps, st));
+    if (rc != OK) return rc;
+    int64_t blocks = (n * ns + 255) / 256;
+    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+    srht_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double>(), nb, per, n, ns, NQ * 32,
+                                                               tb->srht_row, scale, SA, ldsa,
+                                                               static_cast<int>(base));
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+  }
+  return OK;
+}
+
+}  // namespace nsk

@@ -1,0 +1,401 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (stated per test): integer draws bit-exact; SA within 1e-12 relative
+Frobenius of the oracle; trailing subspaces within a principal-angle bound
+(complement projection, kernels.cpp:121-128); ||AW||_F within
+1e-10 * max(||AW_ref||_F, 1e3 u ||A||_F).
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SA_TOL = 1e-12
+U = 2.220446049250313e-16
+
+
+@pytest.fixture(scope="module")
+def nsk():
+    import torch
+    from paper_2206_00975_b200 import build
+    build.build()
+    import paper_2206_00975_b200 as nsk
+    torch.cuda.init()
+    return nsk
+
+
+def dev(x):
+    import torch
+    return torch.from_numpy(np.asfortranarray(x)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def gpu_apply(nsk, kind, s, m, seed, A):
+    S = nsk.SketchOperator.draw(kind, s, m, seed)
+    return host(nsk.apply(S, dev(A)).data), S
+
+
+# ----------------------------------------------------------------------------- apply parity
+
+@pytest.mark.parametrize("s,m,n,seed", [(80, 2000, 20, 9000001), (400, 20000, 100, 9000001), (7, 333, 5, 3),
+                                        (64, 4096, 300, 17), (1, 50, 3, 2), (33, 1000, 129, 4)])
+def test_gaussian_apply_parity(nsk, oracle, s, m, n, seed):
+    A = oracle.random_real(m, n, seed + 1)
+    got, S = gpu_apply(nsk, "gaussian", s, m, seed, A)
+    ref = oracle.apply(oracle.draw("gaussian", s, m, seed), A)
+    assert rel(got, ref) <= SA_TOL
+
+
+def test_gaussian_complex_apply_parity(nsk, oracle):
+    A = oracle.random_complex(999, 13, 5)
+    got, _ = gpu_apply(nsk, "gaussian", 50, 999, 77, A)
+    ref = oracle.apply(oracle.draw("gaussian", 50, 999, 77), A)
+    assert got.dtype == np.complex128
+    assert rel(got, ref) <= SA_TOL
+
+
+def test_gaussian_identity_known_answer(nsk, golden):
+    # test_sketch.cpp:103-114: apply(S, I_4) == G/2 (1e-15 there; CUDA libm log/sincospi are
+    # within 2 ulp of glibc, so the bound here is 4 ulp of the largest entry).
+    G = golden["draws"]["G_4_4_42"]
+    got, _ = gpu_apply(nsk, "gaussian", 4, 4, 42, np.eye(4))
+    assert np.max(np.abs(got - G / 2.0)) <= 4 * U * np.max(np.abs(G))
+
+
+@pytest.mark.parametrize("kind,s,m,n", [("srdct", 40, 2000, 20), ("srdct", 60, 60, 11), ("srdct", 17, 1000, 3),
+                                        ("srdct", 256, 1 << 14, 64), ("srft", 64, 1000, 7), ("srft", 60, 60, 11),
+                                        ("srft", 128, 1 << 13, 33)])
+def test_srtt_apply_parity(nsk, oracle, kind, s, m, n):
+    A = oracle.random_real(m, n, 11)
+    got, _ = gpu_apply(nsk, kind, s, m, 21, A)
+    ref = oracle.apply(oracle.draw(kind, s, m, 21), A)
+    assert rel(got, ref) <= SA_TOL
+
+
+def test_srft_complex_parity(nsk, oracle, golden):
+    sa = golden["sa"]
+    A = sa["A_srft"]
+    got, _ = gpu_apply(nsk, "srft", 24, 300, 9000004, A)
+    assert rel(got, sa["SA_srft"]) <= SA_TOL
+
+
+@pytest.mark.parametrize("s,m,n", [(40, 2048, 20), (1024, 1 << 14, 8), (100, 1 << 12, 33), (16, 256, 5),
+                                   (1000, 1 << 16, 3), (2048, 1 << 13, 4)])
+def test_srht_apply_parity(nsk, oracle, s, m, n):
+    A = oracle.random_real(m, n, 5)
+    got, _ = gpu_apply(nsk, "srht", s, m, 9000002, A)
+    ref = oracle.apply(oracle.draw("srht", s, m, 9000002), A)
+    assert rel(got, ref) <= SA_TOL
+
+
+@pytest.mark.parametrize("s,m,n", [(400, 2000, 20), (4096, 100000, 8), (1024, 50000, 3), (64, 1000, 17),
+                                   (30000, 70000, 2)])
+def test_countsketch_apply_parity(nsk, oracle, s, m, n):
+    A = oracle.random_real(m, n, 6)
+    got, _ = gpu_apply(nsk, "countsketch", s, m, 9000003, A)
+    ref = oracle.apply(oracle.draw("countsketch", s, m, 9000003), A)
+    assert rel(got, ref) <= SA_TOL
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "srdct", "srht", "countsketch"])
+def test_golden_fixture_sa(nsk, golden, kind):
+    sa = golden["sa"]
+    m = 2048 if kind == "srht" else 2000
+    s = {"gaussian": 80, "srdct": 40, "srht": 40, "countsketch": 400}[kind]
+    got, _ = gpu_apply(nsk, kind, s, m, 9000001, sa[f"A_{m}_20"])
+    assert rel(got, sa[f"SA_{kind}"]) <= SA_TOL
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "srft", "srdct", "srht", "countsketch"])
+def test_apply_bit_identical_reruns(nsk, oracle, kind):
+    m = 4096
+    A = dev(oracle.random_real(m, 40, 9))
+    S = nsk.SketchOperator.draw(kind, 128, m, 5)
+    a = host(nsk.apply(S, A).data)
+    b = host(nsk.apply(S, A).data)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "srft", "srdct", "srht", "countsketch"])
+def test_apply_is_linear(nsk, oracle, kind):
+    # test_sketch.cpp:140-163: 1e-13 relative
+    m = 2048
+    a = oracle.random_real(m, 6, 13)
+    b = oracle.random_real(m, 6, 14)
+    S = nsk.SketchOperator.draw(kind, 64, m, 21)
+    lhs = host(nsk.apply(S, dev(2 * a - 3 * b)).data)
+    rhs = 2 * host(nsk.apply(S, dev(a)).data) - 3 * host(nsk.apply(S, dev(b)).data)
+    assert np.max(np.abs(lhs - rhs)) < 1e-13 * np.linalg.norm(lhs)
+
+
+@pytest.mark.parametrize("kind", ["srft", "srdct"])
+def test_full_sampling_is_unitary(nsk, oracle, kind):
+    # test_sketch.cpp:116-131: s = m preserves singular values to 1e-12 sigma_1
+    m, n = 60, 11
+    A = oracle.random_real(m, n, 5)
+    got, _ = gpu_apply(nsk, kind, m, m, 7, A)
+    sv, ref = np.linalg.svd(got, compute_uv=False), np.linalg.svd(A, compute_uv=False)
+    assert np.max(np.abs(sv - ref)) < 1e-12 * ref[0]
+
+
+def test_srht_full_sampling_is_unitary(nsk, oracle):
+    m, n = 1 << 12, 9
+    A = oracle.random_real(m, n, 5)
+    got, _ = gpu_apply(nsk, "srht", m, m, 7, A)
+    sv, ref = np.linalg.svd(got, compute_uv=False), np.linalg.svd(A, compute_uv=False)
+    assert np.max(np.abs(sv - ref)) < 1e-12 * ref[0]
+
+
+def test_zero_input_gives_zero(nsk):
+    import torch
+    S = nsk.SketchOperator.draw("srft", 8, 32, 3)
+    Z = torch.zeros(32, 5, dtype=torch.complex128, device="cuda")
+    assert torch.linalg.norm(nsk.apply(S, Z).data).item() == 0.0
+
+
+def test_apply_validation(nsk, oracle):
+    import torch
+    S = nsk.SketchOperator.draw("srft", 8, 32, 3)
+    with pytest.raises(ValueError):
+        nsk.apply(S, torch.zeros(31, 5, dtype=torch.complex128, device="cuda"))
+    D = nsk.SketchOperator.draw("srdct", 8, 32, 3)
+    with pytest.raises(ValueError):
+        nsk.apply(D, torch.zeros(32, 5, dtype=torch.complex128, device="cuda"))
+    H = nsk.SketchOperator.draw("srht", 8, 32, 3)
+    with pytest.raises(ValueError):
+        nsk.apply(H, torch.zeros(32, 5, dtype=torch.complex128, device="cuda"))
+
+
+def test_non_colmajor_and_ld_inputs(nsk, oracle):
+    import torch
+    m, n = 3000, 12
+    A = oracle.random_real(m, n, 3)
+    S = nsk.SketchOperator.draw("gaussian", 50, m, 4)
+    ref = host(nsk.apply(S, dev(A)).data)
+    rowmajor = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    assert np.array_equal(host(nsk.apply(S, rowmajor).data), ref)
+    big = torch.zeros((n, m + 5), dtype=torch.float64, device="cuda")
+    big[:, :m] = torch.from_numpy(A.T.copy()).cuda()
+    view = big.t()[:m]  # column-major with lda = m + 5
+    assert view.stride() == (1, m + 5)
+    assert rel(host(nsk.apply(S, view).data), ref) <= 1e-15
+
+
+def test_host_entry_point_matches_device(nsk, oracle):
+    m, n = 2000, 10
+    A = oracle.random_real(m, n, 8)
+    for kind in ("gaussian", "srdct", "srht", "countsketch", "srft"):
+        mm = 2048 if kind == "srht" else m
+        Ak = oracle.random_real(mm, n, 8)
+        S = nsk.SketchOperator.draw(kind, 40, mm, 4)
+        assert np.array_equal(nsk.apply(S, Ak).data, host(nsk.apply(S, dev(Ak)).data))
+
+
+# ----------------------------------------------------------------------------- shards
+
+@pytest.mark.parametrize("kind,m,splits", [("gaussian", 4000, [0, 1000, 2500, 4000]),
+                                           ("srht", 1 << 14, [0, 4096, 8192, 16384]),
+                                           ("countsketch", 1 << 14, [0, 2048, 10240, 16384])])
+def test_row_shards_sum_to_apply(nsk, oracle, kind, m, splits):
+    import torch
+    A = oracle.random_real(m, 9, 3)
+    S = nsk.SketchOperator.draw(kind, 100, m, 31)
+    full = host(nsk.apply(S, dev(A)).data)
+    acc = torch.zeros(100, 9, dtype=torch.float64, device="cuda")
+    for a, b in zip(splits[:-1], splits[1:]):
+        acc += nsk.apply_shard(S, dev(A[a:b]), a)
+    assert rel(host(acc), full) <= 1e-13
+
+
+@pytest.mark.parametrize("kind", ["srdct", "srft"])
+def test_cyclic_shards_sum_to_apply(nsk, oracle, kind):
+    import torch
+    m, P = 3000, 4
+    A = oracle.random_real(m, 7, 3)
+    S = nsk.SketchOperator.draw(kind, 64, m, 31)
+    full = host(nsk.apply(S, dev(A)).data)
+    acc = None
+    for g in range(P):
+        part = nsk.apply_shard(S, dev(A[g::P]), g, P)
+        acc = part if acc is None else acc + part
+    assert rel(host(acc), full) <= 1e-13
+
+
+# ----------------------------------------------------------------------------- solve
+
+def _angle(W, Wref):
+    from oracle import sketch_oracle as O
+    return O.sin_theta(W, Wref)
+
+
+def test_cfg1_solve_k_parity(nsk, oracle):
+    """BASELINE configs[0]: m=20000, n=100, gaussian s=4n, sigma_n = 1e-10, k=1."""
+    m, n = 20000, 100
+    spec = np.concatenate([np.logspace(0, -3, n - 1), [1e-10]])
+    A = oracle.make_test_matrix(m, n, spec, seed=1)
+    S = nsk.SketchOperator.draw("gaussian", 4 * n, m, 9000001)
+    res = nsk.solve_k(dev(A), 1, S)
+    W, sig = host(res.W), host(res.sketched_singular_values)
+    Wref, sref = oracle.solve_k(A, 1, oracle.draw("gaussian", 4 * n, m, 9000001))
+    assert _angle(W, Wref) <= 1e-10
+    # LAPACK/BDCSVD sigmas are accurate to O(u sigma_1) absolutely (the 8.8e-11 trailing value
+    # differs by ~2e-17 between the two backends), so the sigma bound is absolute.
+    assert np.max(np.abs(sig - sref)) <= 100 * U * sref[0]
+    r, rref = np.linalg.norm(A @ W), np.linalg.norm(A @ Wref)
+    assert abs(r - rref) <= 1e-10 * max(rref, 1e3 * U * np.linalg.norm(A))
+    assert abs(nsk.residual_certificate(dev(A), res.W) - r) <= 1e-12 * max(r, 1e-300) + 1e-20
+    # the sketched solution is near-optimal (Theorem 3): ||AW|| within factor 4 of sigma_n
+    assert r < 4 * spec[-1]
+
+
+@pytest.mark.parametrize("kind,s", [("srdct", 40), ("srht", 40), ("countsketch", 400), ("gaussian", 80)])
+def test_solve_k_golden(nsk, golden, kind, s):
+    sa = golden["sa"]
+    m = 2048 if kind == "srht" else 2000
+    A = sa[f"A_{m}_20"]
+    S = nsk.SketchOperator.draw(kind, s, m, 9000001)
+    res = nsk.solve_k(A, 1, S)  # host entry point
+    assert _angle(res.W, sa[f"W_{kind}"]) <= 1e-10
+    sref = sa[f"sigma_{kind}"]
+    assert np.max(np.abs(res.sketched_singular_values - sref)) <= 1e-12 * sref[0]
+
+
+def test_svd_trailing_contract(nsk, oracle):
+    for (s, n, k) in [(40, 20, 3), (300, 150, 1), (1024, 256, 4), (64, 64, 5), (9, 1, 0)]:
+        X = oracle.random_real(s, n, s + n)
+        W, sig = nsk.svd_trailing(dev(X), k)
+        W, sig = host(W), host(sig)
+        _, sref, vh = np.linalg.svd(X, full_matrices=False)
+        assert np.max(np.abs(sig - sref)) <= 1e-12 * sref[0]
+        assert np.all(np.diff(sig) <= 0)
+        if k:
+            assert np.max(np.abs(W.T @ W - np.eye(k))) < 1e-12
+            assert _angle(W, vh.T[:, n - k:]) < 1e-10
+
+
+def test_svd_trailing_complex(nsk, oracle):
+    X = oracle.random_complex(300, 150, 2)
+    W, sig = nsk.svd_trailing(dev(X), 2)
+    W, sig = host(W), host(sig)
+    _, sref, vh = np.linalg.svd(X, full_matrices=False)
+    assert np.max(np.abs(sig - sref)) <= 1e-12 * sref[0]
+    assert _angle(W, vh.conj().T[:, -2:]) < 1e-10
+
+
+def test_exact_null_space_preserved(nsk, oracle):
+    # test_nullspace.cpp:21-32
+    m, n, k = 200, 20, 2
+    spec = np.ones(n)
+    spec[-k:] = 0.0
+    A = oracle.make_test_matrix(m, n, spec, seed=1)
+    S = nsk.SketchOperator.draw("srft", 2 * n, m, 2)
+    res = nsk.solve_k(dev(A), k, S)
+    assert nsk.residual_certificate(dev(A), res.W) < 1e-10
+    exact = np.linalg.svd(A)[2].T[:, n - k:]
+    assert _angle(host(res.W), exact) < 1e-10
+
+
+def test_unitary_sketch_reproduces_exact_subspace(nsk, oracle):
+    # test_nullspace.cpp:34-45
+    m, n, k = 120, 12, 3
+    spec = np.array([1.0 if i < n - k else 1e-2 * 10.0 ** (-(i - (n - k))) for i in range(n)])
+    A = oracle.make_test_matrix(m, n, spec, seed=3)
+    S = nsk.SketchOperator.draw("srft", m, m, 4)
+    res = nsk.solve_k(dev(A), k, S)
+    exact = np.linalg.svd(A)[2].T[:, n - k:]
+    assert _angle(host(res.W), exact) < 1e-10
+    ref = np.linalg.svd(A, compute_uv=False)
+    assert np.max(np.abs(host(res.sketched_singular_values) - ref)) < 1e-12 * ref[0]
+
+
+def test_trailing_residual_identity(nsk, oracle):
+    # test_nullspace.cpp:47-57
+    m, n, k = 150, 14, 4
+    A = oracle.make_test_matrix(m, n, 10.0 ** (-0.5 * np.arange(n)), seed=5)
+    S = nsk.SketchOperator.draw("srdct", 2 * n, m, 6)
+    res = nsk.solve_k(dev(A), k, S)
+    SA = host(nsk.apply(S, dev(A)).data)
+    lhs = np.linalg.norm(SA @ host(res.W))
+    rhs = math.sqrt(np.sum(host(res.sketched_singular_values)[-k:] ** 2))
+    assert abs(lhs - rhs) <= 1e-10 * rhs
+
+
+def test_solve_tol(nsk, oracle):
+    # test_nullspace.cpp:95-135
+    m, n = 90, 10
+    A = oracle.make_test_matrix(m, n, 10.0 ** (-np.arange(n, dtype=float)), seed=7)
+    S = nsk.SketchOperator.draw("srft", m, m, 8)
+    assert nsk.solve_tol(dev(A), 3e-9, S).k == 1
+    r0 = nsk.solve_tol(dev(A), 1e-12, S)
+    assert r0.k == 0 and r0.W.shape == (n, 0)
+    spec = np.ones(n)
+    spec[-2:] = 0
+    B = oracle.make_test_matrix(m, n, spec, seed=9)
+    assert nsk.solve_tol(dev(B), 1e-14, S).k == 2
+    with pytest.raises(ValueError):
+        nsk.solve_tol(dev(A), 2.0, S)
+    prev = 0
+    for eps in (1e-11, 1e-7, 1e-4, 0.5):
+        k = nsk.solve_tol(dev(A), eps, S).k
+        assert k >= prev
+        prev = k
+    with pytest.raises(ValueError):
+        nsk.solve_tol(dev(A), -1.0, S)
+    kh = nsk.solve_tol(A, 3e-9, S)  # host entry point
+    assert kh.k == 1
+
+
+def test_solve_validation(nsk, oracle):
+    # test_nullspace.cpp:160-170
+    m, n = 64, 8
+    A = dev(oracle.random_real(m, n, 10))
+    S = nsk.SketchOperator.draw("srdct", 2 * n, m, 11)
+    with pytest.raises(ValueError):
+        nsk.solve_k(A, n, S)
+    with pytest.raises(ValueError):
+        nsk.solve_k(A, -1, S)
+    with pytest.raises(ValueError):
+        nsk.solve_k(A, 1, nsk.SketchOperator.draw("srdct", 2 * n, m + 1, 12))
+    with pytest.raises(ValueError):
+        nsk.solve_k(A, 1, nsk.SketchOperator.draw("srdct", n - 2, m, 13))
+
+
+def test_residual_certificate_known_answer(nsk):
+    a = np.zeros((3, 2))
+    a[0, 0] = 3.0
+    a[1, 1] = 1.0
+    w = np.array([[1.0], [0.0]])
+    assert abs(nsk.residual_certificate(dev(a), dev(w)) - 3.0) < 1e-15
+    with pytest.raises(ValueError):
+        nsk.residual_certificate(dev(a), dev(np.eye(3)[:, :1]))
+
+
+# ----------------------------------------------------------------------------- full size
+
+def test_cfg2_srht_full_size_properties(nsk, oracle):
+    """BASELINE configs[1] at full size (m = 2^20, n = 256, s = 1024): linearity,
+    bit-identical re-run and a column-sampled oracle check."""
+    import torch
+    m, n, s = 1 << 20, 256, 1024
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(n, m, dtype=torch.float64, device="cuda", generator=g).t()
+    B = torch.randn(n, m, dtype=torch.float64, device="cuda", generator=g).t()
+    S = nsk.SketchOperator.draw("srht", s, m, 9000002)
+    sa = nsk.apply(S, A).data
+    sb = nsk.apply(S, B).data
+    sab = nsk.apply(S, (2 * A - 3 * B).t().contiguous().t()).data
+    assert (torch.linalg.norm(sab - (2 * sa - 3 * sb)) / torch.linalg.norm(sab)).item() < 1e-13
+    assert torch.equal(sa, nsk.apply(S, A).data)
+    cols = [0, 77, 255]
+    Ah = A[:, cols].cpu().numpy()
+    ref = oracle.apply(oracle.draw("srht", s, m, 9000002), Ah)
+    assert rel(sa[:, cols].cpu().numpy(), ref) <= SA_TOL
