@@ -160,6 +160,9 @@ int nsk_solve_tol_host(const nsk_operator* op, int scalar, int64_t m, int64_t n,
                        int64_t lda, double eps, int64_t* k_out, void* W, int64_t ldw,
                        double* sigma);
 
+int nsk_residual_fro_host(int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k,
+                          const void* W, int64_t ldw, double* out);
+
 /* ---- instrumentation (bench.py; no effect on results) ------------------- */
 
 /* Number of CUDA kernels this library has launched in this process. */

@@ -1,0 +1,254 @@
+// nullsketch_b200.hpp -- C++ host API over the C ABI, mirroring the reference.
+//
+// Same names, argument meaning and error behaviour as the reference's
+// /root/reference/proj/include/nullsketch/{sketch,nullspace}.hpp, so a caller
+// of the reference can switch by changing the include and the namespace:
+//
+//   reference (Eigen-backed, host)              this header (B200 device)
+//   ------------------------------------------  ------------------------------------------
+//   SketchOperator::draw(kind, s, m, seed)      SketchOperator::draw(kind, s, m, seed)
+//   SketchOperator::descriptor()/from_...()     same
+//   apply(S, A) -> SketchedMatrix               apply(S, A) -> SketchedMatrix
+//   solve_k(A, k, S) -> NullspaceResult         solve_k(A, k, S) -> NullspaceResult
+//   solve_tol(A, eps, S)                        solve_tol(A, eps, S)
+//   residual_certificate(A, W)                  residual_certificate(A, W)
+//   std::invalid_argument / std::out_of_range   same (from NSK_EINVAL / NSK_ERANGE)
+//   SvdConvergenceError                         SvdConvergenceError (NSK_ENOCONV)
+//
+// Matrix is a dense column-major host matrix (real or interleaved complex),
+// the reference's value-semantics carrier (matrix.hpp:32-105).  The device
+// entry points (nsk_apply, nsk_solve_k on device pointers and a stream) are
+// available to callers that keep A resident in HBM.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "nullsketch_b200.h"
+
+namespace nullsketch_b200 {
+
+using Index = int64_t;
+using Complex = std::complex<double>;
+
+enum class SketchKind { gaussian = NSK_GAUSSIAN, srft = NSK_SRFT, srdct = NSK_SRDCT, srht = NSK_SRHT,
+                        countsketch = NSK_COUNTSKETCH };
+enum class ScalarKind { real = NSK_REAL, complex = NSK_COMPLEX };
+
+struct SvdConvergenceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == NSK_OK) return;
+  const char* msg = nsk_last_error();
+  std::string m = msg ? msg : "";
+  switch (rc) {
+    case NSK_EINVAL: throw std::invalid_argument(m);
+    case NSK_ERANGE: throw std::out_of_range(m);
+    case NSK_ENOCONV: throw SvdConvergenceError(m);
+    case NSK_ENOMEM: throw std::bad_alloc();
+    default: throw std::runtime_error("nullsketch CUDA failure: " + m);
+  }
+}
+
+inline std::string to_string(SketchKind k) {
+  switch (k) {
+    case SketchKind::gaussian: return "gaussian";
+    case SketchKind::srft: return "srft";
+    case SketchKind::srdct: return "srdct";
+    case SketchKind::srht: return "srht";
+    case SketchKind::countsketch: return "countsketch";
+  }
+  throw std::logic_error("unknown sketch kind");
+}
+
+inline SketchKind sketch_kind_from_string(const std::string& name) {
+  for (SketchKind k : {SketchKind::gaussian, SketchKind::srft, SketchKind::srdct, SketchKind::srht,
+                       SketchKind::countsketch})
+    if (to_string(k) == name) return k;
+  throw std::invalid_argument("unknown sketch kind: " + name);
+}
+
+// sketch.cpp:99-101 (2n transforms, 4n gaussian); n^2 for countsketch.
+inline Index default_sketch_size(SketchKind kind, Index n) {
+  if (kind == SketchKind::gaussian) return 4 * n;
+  if (kind == SketchKind::countsketch) return n * n;
+  return 2 * n;
+}
+
+// Dense column-major host matrix; complex entries interleaved (re, im).
+class Matrix {
+ public:
+  Matrix() = default;
+  Matrix(Index rows, Index cols, ScalarKind kind = ScalarKind::real)
+      : rows_(rows), cols_(cols), kind_(kind), data_(static_cast<size_t>(rows * cols * ncomp()), 0.0) {}
+  static Matrix zeros(Index rows, Index cols, ScalarKind kind) { return Matrix(rows, cols, kind); }
+
+  Index rows() const { return rows_; }
+  Index cols() const { return cols_; }
+  ScalarKind kind() const { return kind_; }
+  bool is_real() const { return kind_ == ScalarKind::real; }
+  int ncomp() const { return kind_ == ScalarKind::real ? 1 : 2; }
+  double* data() { return data_.data(); }
+  const double* data() const { return data_.data(); }
+
+  double& operator()(Index i, Index j) {  // real entry
+    return data_[static_cast<size_t>(i + j * rows_)];
+  }
+  double operator()(Index i, Index j) const { return data_[static_cast<size_t>(i + j * rows_)]; }
+  Complex at(Index i, Index j) const {
+    if (is_real()) return Complex(data_[static_cast<size_t>(i + j * rows_)], 0.0);
+    const size_t p = static_cast<size_t>(2 * (i + j * rows_));
+    return Complex(data_[p], data_[p + 1]);
+  }
+  void set(Index i, Index j, Complex v) {
+    if (is_real()) {
+      data_[static_cast<size_t>(i + j * rows_)] = v.real();
+    } else {
+      const size_t p = static_cast<size_t>(2 * (i + j * rows_));
+      data_[p] = v.real();
+      data_[p + 1] = v.imag();
+    }
+  }
+
+ private:
+  Index rows_ = 0, cols_ = 0;
+  ScalarKind kind_ = ScalarKind::real;
+  std::vector<double> data_;
+};
+
+class SketchOperator {
+ public:
+  static SketchOperator draw(SketchKind kind, Index s, Index m, uint64_t seed) {
+    nsk_operator* h = nullptr;
+    check(nsk_op_draw(static_cast<int>(kind), s, m, seed, &h));
+    return SketchOperator(h);
+  }
+  static SketchOperator from_descriptor(const std::string& json_text) {
+    nsk_operator* h = nullptr;
+    check(nsk_op_from_descriptor(json_text.c_str(), &h));
+    return SketchOperator(h);
+  }
+  std::string descriptor() const {
+    char buf[512];
+    size_t len = 0;
+    check(nsk_op_descriptor(h_, buf, sizeof buf, &len));
+    return std::string(buf, len);
+  }
+
+  SketchOperator(SketchOperator&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  SketchOperator& operator=(SketchOperator&& o) noexcept {
+    if (this != &o) {
+      nsk_op_destroy(h_);
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+  SketchOperator(const SketchOperator&) = delete;
+  SketchOperator& operator=(const SketchOperator&) = delete;
+  ~SketchOperator() { nsk_op_destroy(h_); }
+
+  SketchKind kind() const { return static_cast<SketchKind>(info().kind); }
+  Index s() const { return info().s; }
+  Index m() const { return info().m; }
+  Index m_effective() const { return m(); }
+  uint64_t seed() const { return info().seed; }
+  uint64_t id() const { return info().id; }
+  std::vector<int64_t> sample_indices() const {
+    std::vector<int64_t> idx(static_cast<size_t>(s()));
+    check(nsk_op_sample_indices(h_, idx.data()));
+    return idx;
+  }
+  const nsk_operator* handle() const { return h_; }
+
+ private:
+  explicit SketchOperator(nsk_operator* h) : h_(h) {}
+  struct Info {
+    int kind;
+    int64_t s, m;
+    uint64_t seed, id;
+  };
+  Info info() const {
+    Info i{};
+    check(nsk_op_info(h_, &i.kind, &i.s, &i.m, &i.seed, &i.id));
+    return i;
+  }
+  nsk_operator* h_ = nullptr;
+};
+
+struct SketchedMatrix {
+  Matrix data;
+  uint64_t operator_id = 0;
+};
+
+struct NullspaceResult {
+  Matrix W;                                   // n x k, orthonormal columns
+  std::vector<double> sketched_singular_values;  // all n, non-increasing
+  bool has_residual = false;
+  double residual_fro = 0.0;
+  Index k = 0;
+};
+
+inline ScalarKind out_kind(const SketchOperator& S, const Matrix& A) {
+  return (S.kind() == SketchKind::srft || !A.is_real()) ? ScalarKind::complex : ScalarKind::real;
+}
+
+// sketch.hpp:89
+inline SketchedMatrix apply(const SketchOperator& S, const Matrix& A) {
+  Matrix out(S.s(), A.cols(), out_kind(S, A));
+  check(nsk_apply_host(S.handle(), static_cast<int>(A.kind()), A.rows(), A.cols(), A.data(),
+                       A.rows() > 0 ? A.rows() : 1, out.data(), S.s()));
+  return {std::move(out), S.id()};
+}
+
+// nullspace.hpp:24
+inline NullspaceResult solve_k(const Matrix& A, Index k, const SketchOperator& S) {
+  NullspaceResult r;
+  if (k < 0 || k >= A.cols())
+    throw std::invalid_argument("nullspace: k must satisfy 0 <= k < n, got k = " + std::to_string(k) +
+                                ", n = " + std::to_string(A.cols()));
+  r.W = Matrix(A.cols(), k, out_kind(S, A));
+  r.sketched_singular_values.resize(static_cast<size_t>(A.cols()));
+  check(nsk_solve_k_host(S.handle(), static_cast<int>(A.kind()), A.rows(), A.cols(), A.data(),
+                         A.rows() > 0 ? A.rows() : 1, k, r.W.data(), A.cols(),
+                         r.sketched_singular_values.data()));
+  r.k = k;
+  return r;
+}
+
+// nullspace.hpp:30
+inline NullspaceResult solve_tol(const Matrix& A, double eps, const SketchOperator& S) {
+  NullspaceResult r;
+  const Index n = A.cols();
+  Matrix Wfull(n, n > 1 ? n - 1 : 1, out_kind(S, A));
+  r.sketched_singular_values.resize(static_cast<size_t>(n));
+  int64_t k = 0;
+  check(nsk_solve_tol_host(S.handle(), static_cast<int>(A.kind()), A.rows(), n, A.data(),
+                           A.rows() > 0 ? A.rows() : 1, eps, &k, Wfull.data(), n,
+                           r.sketched_singular_values.data()));
+  r.W = Matrix(n, k, Wfull.kind());
+  for (Index j = 0; j < k; ++j)
+    for (Index i = 0; i < n; ++i) r.W.set(i, j, Wfull.at(i, j));
+  r.k = k;
+  return r;
+}
+
+// nullspace.hpp:33 -- ||A W||_F, one pass over A on the device.
+inline double residual_certificate(const Matrix& A, const Matrix& W) {
+  if (A.cols() != W.rows())
+    throw std::invalid_argument("residual_certificate: basis lives in dimension " + std::to_string(W.rows()) +
+                                ", matrix has " + std::to_string(A.cols()) + " columns");
+  if (A.kind() != W.kind())
+    throw std::invalid_argument("residual_certificate: A and W must have the same scalar kind");
+  double out = 0.0;
+  check(nsk_residual_fro_host(static_cast<int>(A.kind()), A.rows(), A.cols(), A.data(),
+                              A.rows() > 0 ? A.rows() : 1, W.cols(), W.data(), W.rows() > 0 ? W.rows() : 1, &out));
+  return out;
+}
+
+}  // namespace nullsketch_b200

@@ -24,7 +24,7 @@ EXPORTS = (
     "nsk_last_error", "nsk_version", "nsk_op_draw", "nsk_op_destroy", "nsk_op_info",
     "nsk_op_sample_indices", "nsk_op_descriptor", "nsk_op_from_descriptor", "nsk_apply",
     "nsk_apply_shard", "nsk_svd_trailing", "nsk_solve_k", "nsk_solve_tol", "nsk_residual_fro",
-    "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_kernel_launches",
+    "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_residual_fro_host", "nsk_kernel_launches",
     "nsk_timing_enable", "nsk_timing_collect",
 )
 
@@ -66,6 +66,7 @@ def load():
     L.nsk_apply_host.argtypes = [vp, c_int, i64, i64, vp, i64, vp, i64]
     L.nsk_solve_k_host.argtypes = [vp, c_int, i64, i64, vp, i64, i64, vp, i64, vp]
     L.nsk_solve_tol_host.argtypes = [vp, c_int, i64, i64, vp, i64, ctypes.c_double, i64p, vp, i64, vp]
+    L.nsk_residual_fro_host.argtypes = [c_int, i64, i64, vp, i64, i64, vp, i64, dp]
     L.nsk_kernel_launches.restype = i64
     L.nsk_timing_enable.argtypes = [c_int]
     L.nsk_timing_enable.restype = None

@@ -402,4 +402,18 @@ int nsk_solve_tol_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, 
   return nsk::OK;
 }
 
+int nsk_residual_fro_host(int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k, const void* W,
+                          int64_t ldw, double* out) {
+  if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "unknown scalar kind");
+  if (m < 0 || n < 0 || k < 0 || lda < m || (k > 0 && ldw < n))
+    return nsk::fail(nsk::EINVAL_, "residual_certificate: bad dimensions");
+  cudaStream_t st = host_stream();
+  const int nc = scalar == NSK_COMPLEX ? 2 : 1;
+  nsk::Scratch a, w;
+  double *dA = nullptr, *dW = nullptr;
+  if (int rc = copy_in(A, m, n, lda, nc, &dA, a, st)) return rc;
+  if (int rc = copy_in(W, n, k, ldw, nc, &dW, w, st)) return rc;
+  return nsk::residual_fro(nc, m, n, dA, m > 0 ? m : 1, k, dW, n > 0 ? n : 1, out, st);
+}
+
 }  // extern "C"

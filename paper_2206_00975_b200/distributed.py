@@ -1,0 +1,98 @@
+"""Row-sharded multi-GPU sketching: one process per GPU, NCCL over NVLink.
+
+SA = sum_g S[:, rows_g] A_g, so each rank sketches the rows it holds with
+nsk_apply_shard (the operator regenerates S for the *global* row indices;
+nothing is communicated before the reduce) and one all-reduce (sum) of the
+s x n partials -- 2 MiB at BASELINE configs[1] -- produces SA on every rank.
+The SVD of the small SA then runs on the root rank (or every rank).
+
+Row maps:
+  gaussian, countsketch, srht   contiguous shards (srht: multiples of 1024
+                                rows so the Hadamard split stays block-aligned;
+                                countsketch: multiples of 256 rows)
+  srft, srdct                   cyclic shards: rank g holds rows g, g+P, ...
+                                (decimation in time keeps every local
+                                transform a plain strided DFT)
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, List, Optional
+
+
+@dataclasses.dataclass(frozen=True)
+class RowShard:
+    row0: int
+    rstep: int
+    mloc: int
+
+    def global_rows(self):
+        return range(self.row0, self.row0 + self.rstep * self.mloc, self.rstep) if self.mloc else range(0)
+
+
+def _align_for(kind: str) -> int:
+    return {"srht": 1024, "countsketch": 256}.get(kind, 1)
+
+
+def row_partition(m: int, world: int, kind: str) -> List[RowShard]:
+    """Per-rank row shards covering 0..m-1 exactly once."""
+    if world < 1:
+        raise ValueError("world size must be positive")
+    if kind in ("srft", "srdct"):
+        return [RowShard(g, world, (m - g + world - 1) // world if g < m else 0) for g in range(world)]
+    align = _align_for(kind)
+    if m < align * world:
+        align = 1
+    units = (m + align - 1) // align
+    shards = []
+    for g in range(world):
+        u0 = units * g // world
+        u1 = units * (g + 1) // world
+        r0 = min(m, u0 * align)
+        r1 = min(m, u1 * align)
+        shards.append(RowShard(r0, 1, r1 - r0))
+    return shards
+
+
+def local_rows(A_full, shard: RowShard):
+    """The rows of a full matrix a rank would hold (tests and examples)."""
+    return A_full[shard.row0: shard.row0 + shard.rstep * shard.mloc: shard.rstep]
+
+
+def sharded_apply(S, A_local, shard: RowShard, group=None,
+                  partial_fn: Optional[Callable] = None):
+    """SA on every rank: local partial sketch + all-reduce(sum).
+
+    partial_fn(S, A_local, row0, rstep) defaults to the CUDA path
+    (paper_2206_00975_b200.apply_shard); tests inject a CPU oracle."""
+    import torch.distributed as dist
+    if partial_fn is None:
+        from .sketch import apply_shard
+        partial_fn = apply_shard
+    part = partial_fn(S, A_local, shard.row0, shard.rstep)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+    return part
+
+
+def sharded_solve_k(S, A_local, k: int, shard: RowShard, group=None, root: int = 0,
+                    partial_fn: Optional[Callable] = None, svd_fn: Optional[Callable] = None):
+    """solve_k over row shards: (W, sigma) on every rank (broadcast from root)."""
+    import torch
+    import torch.distributed as dist
+    SA = sharded_apply(S, A_local, shard, group, partial_fn)
+    if svd_fn is None:
+        from .sketch import svd_trailing
+        svd_fn = svd_trailing
+    n = SA.shape[1]
+    multi = dist.is_initialized() and dist.get_world_size(group) > 1
+    if not multi or dist.get_rank(group) == root:
+        W, sig = svd_fn(SA, k)
+        W = W.contiguous()
+    else:
+        W = torch.empty((n, k), dtype=SA.dtype, device=SA.device)
+        sig = torch.empty(n, dtype=torch.float64, device=SA.device)
+    if multi:
+        dist.broadcast(W, src=root, group=group)
+        dist.broadcast(sig, src=root, group=group)
+    return W, sig
