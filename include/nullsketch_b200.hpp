@@ -243,8 +243,15 @@ inline double residual_certificate(const Matrix& A, const Matrix& W) {
   if (A.cols() != W.rows())
     throw std::invalid_argument("residual_certificate: basis lives in dimension " + std::to_string(W.rows()) +
                                 ", matrix has " + std::to_string(A.cols()) + " columns");
-  if (A.kind() != W.kind())
-    throw std::invalid_argument("residual_certificate: A and W must have the same scalar kind");
+  if (A.kind() != W.kind()) {  // promote the real side, as matmul does (matrix.cpp:13-20)
+    auto promote = [](const Matrix& x) {
+      Matrix c(x.rows(), x.cols(), ScalarKind::complex);
+      for (Index j = 0; j < x.cols(); ++j)
+        for (Index i = 0; i < x.rows(); ++i) c.set(i, j, x.at(i, j));
+      return c;
+    };
+    return A.is_real() ? residual_certificate(promote(A), W) : residual_certificate(A, promote(W));
+  }
   double out = 0.0;
   check(nsk_residual_fro_host(static_cast<int>(A.kind()), A.rows(), A.cols(), A.data(),
                               A.rows() > 0 ? A.rows() : 1, W.cols(), W.data(), W.rows() > 0 ? W.rows() : 1, &out));

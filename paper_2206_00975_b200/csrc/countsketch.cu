@@ -5,48 +5,81 @@
 // (rng.hpp:57,60-63): on stream (seed, 0) issue m x next_sign() then
 // m x next_below(s); so sigma(i) = bit 0 of word i and h(i) = mulhi64 of the
 // u64 (word m+2i+1 : word m+2i) with s.  Bit-exact against the compiled
-// reference header (tests/test_draws.py).
+// reference header (tests/test_oracle_pins.py, tests/test_capi_host.py).
 //
 // B200 design (HBM-bound streaming read of A, deterministic scatter-add):
-//   * a per-operator row table (4 B/row, built once on the device) packs
-//     h(i), sigma(i) and, inside each 256-row tile, whether row i is the
-//     first of its bucket ("leader") and the offset of the next row of the
-//     same bucket.  It is L2 resident (64 MiB at m = 2^24) and is re-read by
-//     every column group of a row range, which the grid schedules together.
-//   * a CTA owns NC columns and a contiguous range of row tiles; one thread
-//     per row streams its NC values straight from HBM (coalesced 2 KiB
-//     column segments) with a one-tile register prefetch.
-//   * buckets inside a tile are unique among leaders, so leaders add their
-//     chain's sum (rows in increasing order) into shared-memory bins with a
-//     plain read-modify-write; one barrier per tile orders the tiles.  The
-//     whole reduction order is fixed: bit-identical re-runs, no atomics.
-//   * per-CTA bins are summed over row splits in fixed order by a second kernel.
+//   * a per-operator row table (4 B/row, built once on the device) packs h(i),
+//     sigma(i) and, inside each 512-row chain tile, whether row i is the first
+//     of its bucket ("leader") and the offset of the next same-bucket row.
+//   * a CTA owns NC columns and a contiguous range of 512-row tiles.  Thread 0
+//     streams each tile's NC column segments (4 KiB each) and its 2 KiB of
+//     table into a D-stage shared-memory ring with 1-D TMA bulk copies
+//     (cp.async.bulk ... mbarrier::complete_tx), so ~D tiles are in flight.
+//   * inside a tile the leaders' buckets are unique, so each leader sums its
+//     chain (rows in increasing order) and adds it to shared-memory bins with
+//     a plain read-modify-write; one barrier per tile orders the tiles.  No
+//     float atomics anywhere: bit-identical re-runs.
+//   * per-CTA bins are summed over row splits in fixed order by cs_reduce.
 #include "nsk_internal.hpp"
 
 namespace nsk {
 
 namespace {
-constexpr int TILE = 256;  // rows per tile == threads per CTA
+constexpr int CT = 512;        // chain tile (rows)
+constexpr int THREADS = 256;   // 2 rows per thread per tile
+constexpr int STAGES = 4;      // TMA ring depth
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+}  // namespace
 
 // Row table entry: bits 0-15 bucket, bit 16 sign(+1), bit 17 leader,
-// bits 24-31 offset of the next same-bucket row in the tile (0 = none).
+// bits 18-26 offset of the next same-bucket row in the 512-row tile (0 = none).
 __global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, uint32_t* __restrict__ out) {
-  __shared__ uint32_t bucket[TILE];
-  const int64_t ntiles = (m + TILE - 1) / TILE;
+  __shared__ uint32_t bucket[CT];
+  const int64_t ntiles = (m + CT - 1) / CT;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int r = threadIdx.x;
-    const int64_t i = tile * TILE + r;
-    uint32_t b = 0xFFFFFFFFu, sg = 0;
-    if (i < m) {
-      sg = stream_word(key, static_cast<uint64_t>(i)) & 1u;
-      const uint64_t w = static_cast<uint64_t>(m) + 2u * static_cast<uint64_t>(i);
-      const uint64_t u = (static_cast<uint64_t>(stream_word(key, w + 1)) << 32) | stream_word(key, w);
-      b = static_cast<uint32_t>(mulhi64(u, static_cast<uint64_t>(s)));
+    for (int r = threadIdx.x; r < CT; r += blockDim.x) {
+      const int64_t i = tile * CT + r;
+      uint32_t b = 0xFFFFFFFFu;
+      if (i < m) {
+        const uint64_t w = static_cast<uint64_t>(m) + 2u * static_cast<uint64_t>(i);
+        const uint64_t u = (static_cast<uint64_t>(stream_word(key, w + 1)) << 32) | stream_word(key, w);
+        b = static_cast<uint32_t>(mulhi64(u, static_cast<uint64_t>(s)));
+      }
+      bucket[r] = b;
     }
-    bucket[r] = b;
     __syncthreads();
-    if (i < m) {
+    for (int r = threadIdx.x; r < CT; r += blockDim.x) {
+      const int64_t i = tile * CT + r;
+      if (i >= m) continue;
+      const uint32_t b = bucket[r];
       bool leader = true;
       for (int q = 0; q < r; ++q)
         if (bucket[q] == b) {
@@ -54,12 +87,13 @@ __global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, uint3
           break;
         }
       uint32_t next = 0;
-      for (int q = r + 1; q < TILE; ++q)
+      for (int q = r + 1; q < CT; ++q)
         if (bucket[q] == b) {
           next = static_cast<uint32_t>(q - r);
           break;
         }
-      out[i] = (b & 0xFFFFu) | (sg << 16) | (static_cast<uint32_t>(leader) << 17) | (next << 24);
+      const uint32_t sg = stream_word(key, static_cast<uint64_t>(i)) & 1u;
+      out[i] = (b & 0xFFFFu) | (sg << 16) | (static_cast<uint32_t>(leader) << 17) | (next << 18);
     }
     __syncthreads();
   }
@@ -68,9 +102,9 @@ __global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, uint3
 int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out) {
   *out = nullptr;
   NSK_CUDA_OK(cudaMalloc(out, sizeof(uint32_t) * m));
-  const int64_t ntiles = (m + TILE - 1) / TILE;
+  const int64_t ntiles = (m + CT - 1) / CT;
   int64_t blocks = ntiles < 16L * sm_count() ? ntiles : 16L * sm_count();
-  build_cs_table_kernel<<<static_cast<unsigned>(blocks), TILE>>>(key, m, s, *out);
+  build_cs_table_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, m, s, *out);
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
   NSK_CUDA_OK(cudaDeviceSynchronize());
@@ -79,89 +113,218 @@ int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out) {
 
 namespace {
 
+__device__ __forceinline__ uint32_t cs_bucket(uint32_t e) { return e & 0xFFFFu; }
+__device__ __forceinline__ double cs_sign(uint32_t e) { return ((e >> 16) & 1u) ? 1.0 : -1.0; }
+__device__ __forceinline__ bool cs_leader(uint32_t e) { return (e >> 17) & 1u; }
+__device__ __forceinline__ uint32_t cs_next(uint32_t e) { return (e >> 18) & 0x1FFu; }
+
 struct CsParams {
   const double* A;
   int64_t lda;
-  int64_t mloc;
-  int64_t row0;         // multiple of TILE
   int64_t n;
   int64_t s;
-  const uint32_t* table;  // global rows
-  int64_t tiles_per_split;
-  int64_t ntiles;       // local tiles
-  double* P;            // [split][n][s]
-  double* gbins;        // global bins when they do not fit in shared memory
+  const uint32_t* table;  // indexed by global row
+  int64_t row0;           // global row of local row 0 (multiple of CT)
+  int64_t t0;             // first tile (local) handled by split 0
+  int64_t ntiles;         // tiles handled by this launch
+  int64_t per;            // tiles per split
+  int64_t rows_last;      // valid rows in the last tile of this launch (CT for full tiles)
+  int64_t split_base;     // first partial slot written by this launch
+  double* P;              // partials [split][n][s]
+  double* gbins;          // bins in global memory when they do not fit in shared memory
 };
 
+// Sums one tile (values in sv[c][r], table entries in se[r]) into bins.
+template <int NC>
+__device__ __forceinline__ void tile_add(const double* sv, const uint32_t* se, int rows, double* bins, int64_t s,
+                                         int64_t c0, int64_t n) {
+  for (int r = threadIdx.x; r < rows; r += THREADS) {
+    const uint32_t e = se[r];
+    if (!cs_leader(e)) continue;
+    double acc[NC];
+    const double sg = cs_sign(e);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = sg * sv[c * CT + r];
+    int q = r;
+    uint32_t nx = cs_next(e);
+    while (nx) {
+      q += static_cast<int>(nx);
+      if (q >= rows) break;
+      const uint32_t eq = se[q];
+      const double sq = cs_sign(eq);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] += sq * sv[c * CT + q];
+      nx = cs_next(eq);
+    }
+    const uint32_t b = cs_bucket(e);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c0 + c < n) bins[c * s + b] += acc[c];
+  }
+}
+
+// TMA-streamed kernel: full 512-row tiles, 16-byte aligned column segments.
 template <int NC, bool GLOBAL_BINS>
-__global__ void __launch_bounds__(TILE, 2) countsketch_kernel(CsParams p) {
-  extern __shared__ __align__(16) double sm[];
+__global__ void __launch_bounds__(THREADS, 2) countsketch_tma_kernel(CsParams p) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[STAGES];
   const int64_t cg = blockIdx.x, split = blockIdx.y;
   const int64_t c0 = cg * NC;
-  double* bins = GLOBAL_BINS ? p.gbins + (split * gridDim.x + cg) * NC * p.s : sm;
-  double* stage = GLOBAL_BINS ? sm : sm + NC * p.s;  // [2][NC][TILE]
-  for (int64_t e = threadIdx.x; e < NC * p.s; e += TILE) bins[e] = 0.0;
+  int ncol = static_cast<int>(p.n - c0 < NC ? p.n - c0 : NC);
+  double* stage_v = reinterpret_cast<double*>(smraw);                                  // [STAGES][NC][CT]
+  uint32_t* stage_e = reinterpret_cast<uint32_t*>(stage_v + STAGES * NC * CT);         // [STAGES][CT]
+  double* bins = GLOBAL_BINS ? p.gbins + (split * gridDim.x + cg) * NC * p.s
+                             : reinterpret_cast<double*>(stage_e + STAGES * CT);       // [NC][s]
+  for (int64_t e = threadIdx.x; e < NC * p.s; e += THREADS) bins[e] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
-  const int r = threadIdx.x;
-  int64_t t = split * p.tiles_per_split;
-  int64_t tend = t + p.tiles_per_split;
-  if (tend > p.ntiles) tend = p.ntiles;
+  const int64_t tbeg = p.t0 + split * p.per;
+  int64_t tend = tbeg + p.per;
+  if (tend > p.t0 + p.ntiles) tend = p.t0 + p.ntiles;
+  const uint32_t vbytes = CT * 8, ebytes = CT * 4;
+  auto issue = [&](int64_t t, int st) {
+    mbar_expect_tx(&bars[st], vbytes * ncol + ebytes);
+    for (int c = 0; c < ncol; ++c)
+      tma_load_1d(stage_v + (st * NC + c) * CT, p.A + t * CT + (c0 + c) * p.lda, vbytes, &bars[st]);
+    tma_load_1d(stage_e + st * CT, p.table + p.row0 + t * CT, ebytes, &bars[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < STAGES; ++i)
+      if (tbeg + i < tend) issue(tbeg + i, i);
 
-  double v[NC], vn[NC];
-  uint32_t e = 0, en = 0;
-  auto fetch = [&](int64_t tile, double* dst, uint32_t& ent) {
-    const int64_t i = tile * TILE + r;
-    ent = 0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) dst[c] = 0.0;
-    if (i < p.mloc) {
-      ent = __ldg(p.table + p.row0 + i);
+  for (int64_t t = tbeg; t < tend; ++t) {
+    const int64_t k = t - tbeg;
+    const int st = static_cast<int>(k % STAGES);
+    mbar_wait(&bars[st], static_cast<uint32_t>((k / STAGES) & 1));
+    tile_add<NC>(stage_v + st * NC * CT, stage_e + st * CT, CT, bins, p.s, c0, p.n);
+    __syncthreads();  // tile done: bins ordered, stage free
+    if (threadIdx.x == 0 && t + STAGES < tend) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(t + STAGES, st);
+    }
+  }
+  double* P = p.P + ((p.split_base + split) * p.n + c0) * p.s;
+  for (int64_t x = threadIdx.x; x < ncol * p.s; x += THREADS) P[x] = bins[x];
+}
+
+// Register-streamed kernel (default): each thread owns rows 2t, 2t+1 of every
+// tile and keeps DEPTH tiles of 16-byte vector loads in flight in registers,
+// so A never passes through shared memory; only the values of chain members
+// (non-leaders, ~10% of rows) are staged for their leader.  Shared-memory
+// traffic is the bins' read-modify-write alone.
+template <int NC, bool GLOBAL_BINS>
+__global__ void __launch_bounds__(THREADS, 3) countsketch_stream_kernel(CsParams p) {
+  constexpr int DEPTH = NC >= 4 ? 2 : 4;  // 16-byte loads in flight per thread: DEPTH * NC
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int64_t cg = blockIdx.x, split = blockIdx.y;
+  const int64_t c0 = cg * NC;
+  const int ncol = static_cast<int>(p.n - c0 < NC ? p.n - c0 : NC);
+  double* stage = reinterpret_cast<double*>(smraw);                       // [2][NC][CT] member values
+  uint16_t* snext = reinterpret_cast<uint16_t*>(stage + 2 * NC * CT);    // [2][CT] member chain links
+  double* bins = GLOBAL_BINS ? p.gbins + (split * gridDim.x + cg) * NC * p.s
+                             : reinterpret_cast<double*>(snext + 2 * CT);
+  for (int64_t e = threadIdx.x; e < NC * p.s; e += THREADS) bins[e] = 0.0;
+
+  const int64_t tbeg = p.t0 + split * p.per;
+  int64_t tend = tbeg + p.per;
+  if (tend > p.t0 + p.ntiles) tend = p.t0 + p.ntiles;
+  const int r0 = 2 * threadIdx.x;
+  double2 v[DEPTH][NC];
+  uint2 e[DEPTH];
+  auto fetch = [&](int64_t t, int u) {
+    if (t < tend) {
+      e[u] = __ldg(reinterpret_cast<const uint2*>(p.table + p.row0 + t * CT + r0));
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        if (c0 + c < p.n) dst[c] = __ldcs(p.A + i + (c0 + c) * p.lda);
+        v[u][c] = c < ncol ? __ldcs(reinterpret_cast<const double2*>(p.A + t * CT + r0 + (c0 + c) * p.lda))
+                           : make_double2(0.0, 0.0);
     }
   };
-  if (t < tend) fetch(t, v, e);
-  __syncthreads();
-  int buf = 0;
-  for (; t < tend; ++t) {
-    if (t + 1 < tend) fetch(t + 1, vn, en);
-    const bool leader = (e >> 17) & 1u;
-    const double sg = ((e >> 16) & 1u) ? 1.0 : -1.0;
-    double* st = stage + buf * NC * TILE;
-    if (!leader) {  // rows past the shard stage zeros
 #pragma unroll
-      for (int c = 0; c < NC; ++c) st[c * TILE + r] = sg * v[c];
-    }
-    __syncthreads();  // stage visible; previous tile's bin updates complete
-    if (leader) {
-      const uint32_t b = e & 0xFFFFu;
-      double acc[NC];
+  for (int u = 0; u < DEPTH; ++u) fetch(tbeg + u, u);
+
+  for (int64_t t = tbeg; t < tend; t += DEPTH) {
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] = sg * v[c];
-      int q = r;
-      uint32_t nx = e >> 24;
-      while (nx) {
-        q += static_cast<int>(nx);
-        const uint32_t eq = __ldg(p.table + p.row0 + t * TILE + q);
+    for (int u = 0; u < DEPTH; ++u) {
+      const int64_t tt = t + u;
+      if (tt >= tend) break;
+      double* st = stage + (tt & 1) * NC * CT;
+      uint16_t* sn = snext + (tt & 1) * CT;
+      const uint32_t ee[2] = {e[u].x, e[u].y};
+      double vv[2][NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] += st[c * TILE + q];
-        nx = eq >> 24;
+      for (int c = 0; c < NC; ++c) {
+        vv[0][c] = cs_sign(ee[0]) * v[u][c].x;
+        vv[1][c] = cs_sign(ee[1]) * v[u][c].y;
       }
 #pragma unroll
-      for (int c = 0; c < NC; ++c) bins[c * p.s + b] += acc[c];
-    }
-    buf ^= 1;
+      for (int j = 0; j < 2; ++j)
+        if (!cs_leader(ee[j])) {
+          sn[r0 + j] = static_cast<uint16_t>(cs_next(ee[j]));
 #pragma unroll
-    for (int c = 0; c < NC; ++c) v[c] = vn[c];
-    e = en;
+          for (int c = 0; c < NC; ++c) st[c * CT + r0 + j] = vv[j][c];
+        }
+      fetch(tt + DEPTH, u);  // refill this slot while the tile is summed
+      __syncthreads();       // staged members visible; previous tile's bin updates done
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (!cs_leader(ee[j])) continue;
+        double acc[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = vv[j][c];
+        int q = r0 + j;
+        uint32_t nx = cs_next(ee[j]);
+        while (nx) {  // chain members, in row order, from shared memory
+          q += static_cast<int>(nx);
+          nx = sn[q];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) acc[c] += st[c * CT + q];
+        }
+        const uint32_t b = cs_bucket(ee[j]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c < ncol) bins[c * p.s + b] += acc[c];
+      }
+    }
   }
   __syncthreads();
-  double* P = p.P + (split * p.n + c0) * p.s;
-  for (int64_t x = threadIdx.x; x < NC * p.s; x += TILE) {
-    const int64_t c = x / p.s;
-    if (c0 + c < p.n) P[x] = bins[x];
+  double* P = p.P + ((p.split_base + split) * p.n + c0) * p.s;
+  for (int64_t x = threadIdx.x; x < ncol * p.s; x += THREADS) P[x] = bins[x];
+}
+
+// Generic kernel (unaligned inputs, the last partial tile): plain loads.
+template <int NC, bool GLOBAL_BINS>
+__global__ void __launch_bounds__(THREADS) countsketch_generic_kernel(CsParams p) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int64_t cg = blockIdx.x, split = blockIdx.y;
+  const int64_t c0 = cg * NC;
+  const int ncol = static_cast<int>(p.n - c0 < NC ? p.n - c0 : NC);
+  double* sv = reinterpret_cast<double*>(smraw);                  // [NC][CT]
+  uint32_t* se = reinterpret_cast<uint32_t*>(sv + NC * CT);       // [CT]
+  double* bins = GLOBAL_BINS ? p.gbins + (split * gridDim.x + cg) * NC * p.s : reinterpret_cast<double*>(se + CT);
+  for (int64_t e = threadIdx.x; e < NC * p.s; e += THREADS) bins[e] = 0.0;
+  const int64_t tbeg = p.t0 + split * p.per;
+  int64_t tend = tbeg + p.per;
+  if (tend > p.t0 + p.ntiles) tend = p.t0 + p.ntiles;
+  for (int64_t t = tbeg; t < tend; ++t) {
+    const int rows = (t == p.t0 + p.ntiles - 1) ? static_cast<int>(p.rows_last) : CT;
+    __syncthreads();
+    for (int r = threadIdx.x; r < CT; r += THREADS) {
+      const bool ok = r < rows;
+      se[r] = ok ? __ldg(p.table + p.row0 + t * CT + r) : 0u;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sv[c * CT + r] = (ok && c < ncol) ? p.A[t * CT + r + (c0 + c) * p.lda] : 0.0;
+    }
+    __syncthreads();
+    tile_add<NC>(sv, se, rows, bins, p.s, c0, p.n);
   }
+  __syncthreads();
+  double* P = p.P + ((p.split_base + split) * p.n + c0) * p.s;
+  for (int64_t x = threadIdx.x; x < ncol * p.s; x += THREADS) P[x] = bins[x];
 }
 
 __global__ void cs_reduce(const double* __restrict__ P, int64_t splits, int64_t s, int64_t n,
@@ -175,61 +338,122 @@ __global__ void cs_reduce(const double* __restrict__ P, int64_t splits, int64_t 
   }
 }
 
-template <int NC, bool GB>
-int launch_cs(const CsParams& p, int64_t groups, int64_t splits, size_t smem, cudaStream_t st) {
-  auto kern = countsketch_kernel<NC, GB>;
+enum Mode { GENERIC = 0, TMA_RING = 1, STREAM = 2 };
+
+template <int NC, bool GB, int MODE>
+int launch_cs(const CsParams& p, int64_t groups, int64_t splits, cudaStream_t st, bool timed) {
+  size_t smem = MODE == TMA_RING ? (sizeof(double) * STAGES * NC * CT + sizeof(uint32_t) * STAGES * CT)
+              : MODE == STREAM   ? sizeof(double) * 2 * NC * CT + sizeof(uint16_t) * 2 * CT
+                                 : (sizeof(double) * NC * CT + sizeof(uint32_t) * CT);
+  if (!GB) smem += sizeof(double) * NC * p.s;
+  auto kern = MODE == TMA_RING ? countsketch_tma_kernel<NC, GB>
+            : MODE == STREAM   ? countsketch_stream_kernel<NC, GB>
+                               : countsketch_generic_kernel<NC, GB>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  KernelTimer tm(st);
-  kern<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)), TILE, smem, st>>>(p);
+  KernelTimer tm(st, timed);
+  kern<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)), THREADS, smem, st>>>(p);
   tm.stop();
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
   return OK;
 }
 
+template <int MODE>
+int launch_nc(int NC, bool gb, const CsParams& p, int64_t groups, int64_t splits, cudaStream_t st, bool timed) {
+  if (gb) {
+    return NC == 4 ? launch_cs<4, true, MODE>(p, groups, splits, st, timed)
+         : NC == 2 ? launch_cs<2, true, MODE>(p, groups, splits, st, timed)
+                   : launch_cs<1, true, MODE>(p, groups, splits, st, timed);
+  }
+  return NC == 4 ? launch_cs<4, false, MODE>(p, groups, splits, st, timed)
+       : NC == 2 ? launch_cs<2, false, MODE>(p, groups, splits, st, timed)
+                 : launch_cs<1, false, MODE>(p, groups, splits, st, timed);
+}
+
+template <int NC, bool GB>
+int stream_occupancy(int64_t s) {
+  const size_t smem = sizeof(double) * 2 * NC * CT + sizeof(uint16_t) * 2 * CT + (GB ? 0 : sizeof(double) * NC * s);
+  auto kern = countsketch_stream_kernel<NC, GB>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+    return 1;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, smem) != cudaSuccess || occ < 1) return 1;
+  return occ;
+}
+
+int stream_occupancy(int NC, bool gb, int64_t s) {
+  if (gb) return NC == 4 ? stream_occupancy<4, true>(s) : NC == 2 ? stream_occupancy<2, true>(s)
+                                                                  : stream_occupancy<1, true>(s);
+  return NC == 4 ? stream_occupancy<4, false>(s) : NC == 2 ? stream_occupancy<2, false>(s)
+                                                           : stream_occupancy<1, false>(s);
+}
+
+// NSK_CS_MODE=tma selects the TMA-ring kernel (kept for A/B measurements).
+bool use_tma_ring() {
+  const char* v = std::getenv("NSK_CS_MODE");
+  return v && std::string(v) == "tma";
+}
+
 }  // namespace
 
-int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda,
-                      double* SA, int64_t ldsa, cudaStream_t st) {
+int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
+                      int64_t ldsa, cudaStream_t st) {
   const int64_t s = op.s, mloc = rows.mloc;
   if (n == 0) return OK;
-  if (rows.rstep != 1 || rows.row0 % TILE != 0)
-    return fail(EINVAL_, "countsketch shard: rows must be contiguous and start at a multiple of 256");
+  if (rows.rstep != 1 || rows.row0 % CT != 0)
+    return fail(EINVAL_, "countsketch shard: rows must be contiguous and start at a multiple of 512");
   if (s > 65536) return fail(EINVAL_, "countsketch: this build supports s <= 65536");
   const DeviceTables* tb = op.tables();
   if (!tb || !tb->cs_table) return ECUDA;
-  // Columns per CTA: as many as fit next to 64 KiB of shared-memory bins.
-  int NC = static_cast<int>(65536 / (s * 8));
-  NC = NC >= 8 ? 8 : (NC >= 4 ? 4 : (NC >= 2 ? 2 : 1));
-  const bool global_bins = s * 8 > 160 * 1024;
-  if (n < NC) NC = n >= 4 ? 4 : (n >= 2 ? 2 : 1);
-  const int64_t groups = (n + NC - 1) / NC;
-  const int64_t ntiles = (mloc + TILE - 1) / TILE;
-  int64_t splits = (2L * sm_count() + groups - 1) / groups;
-  if (splits < 1) splits = 1;
-  if (splits > ntiles) splits = ntiles > 0 ? ntiles : 1;
-  const int64_t per = ntiles > 0 ? (ntiles + splits - 1) / splits : 0;
-  if (per > 0) splits = (ntiles + per - 1) / per;
-  Scratch part, gb;
-  NSK_CUDA_OK(part.alloc(sizeof(double) * splits * n * s, st));
-  if (global_bins) NSK_CUDA_OK(gb.alloc(sizeof(double) * splits * groups * NC * s, st));
-  CsParams p{A, lda, mloc, rows.row0, n, s, tb->cs_table, per, ntiles, part.as<double>(),
-             global_bins ? gb.as<double>() : nullptr};
-  const size_t stage_bytes = sizeof(double) * 2 * NC * TILE;
-  const size_t smem = (global_bins ? 0 : sizeof(double) * NC * s) + stage_bytes;
-  int rc;
-  if (global_bins) {
-    rc = NC == 8 ? launch_cs<8, true>(p, groups, splits, smem, st)
-                 : NC == 4 ? launch_cs<4, true>(p, groups, splits, smem, st)
-                           : NC == 2 ? launch_cs<2, true>(p, groups, splits, smem, st)
-                                     : launch_cs<1, true>(p, groups, splits, smem, st);
-  } else {
-    rc = NC == 8 ? launch_cs<8, false>(p, groups, splits, smem, st)
-                 : NC == 4 ? launch_cs<4, false>(p, groups, splits, smem, st)
-                           : NC == 2 ? launch_cs<2, false>(p, groups, splits, smem, st)
-                                     : launch_cs<1, false>(p, groups, splits, smem, st);
+  if (mloc == 0) {
+    for (int64_t c = 0; c < n; ++c) NSK_CUDA_OK(cudaMemsetAsync(SA + c * ldsa, 0, sizeof(double) * s, st));
+    return OK;
   }
-  if (rc != OK) return rc;
+  // Columns per CTA: up to 32 KiB of shared-memory bins (3+ CTAs per SM keep
+  // enough independent tiles in flight to cover the per-tile barrier).
+  int NC = static_cast<int>(32768 / (s * 8));
+  NC = NC >= 4 ? 4 : (NC >= 2 ? 2 : 1);
+  if (n < NC) NC = n >= 2 ? 2 : 1;
+  const bool gb = s * 8 > 96 * 1024;
+  const int64_t groups = (n + NC - 1) / NC;
+  const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda % 2) == 0;
+  const int64_t full = aligned ? mloc / CT : 0;          // tiles for the TMA kernel
+  const int64_t rest_rows = mloc - full * CT;
+  const int64_t rest_tiles = (rest_rows + CT - 1) / CT;  // tiles for the generic kernel
+  const int ctas_per_sm = use_tma_ring() ? 2 : stream_occupancy(NC, gb, s);
+  int64_t splits_f = 0, per_f = 0;
+  if (full > 0) {
+    splits_f = (static_cast<int64_t>(ctas_per_sm) * sm_count()) / groups;
+    if (splits_f < 1) splits_f = 1;
+    if (splits_f > full) splits_f = full;
+    per_f = (full + splits_f - 1) / splits_f;
+    splits_f = (full + per_f - 1) / per_f;
+  }
+  int64_t splits_r = 0, per_r = 0;
+  if (rest_tiles > 0) {
+    splits_r = (static_cast<int64_t>(ctas_per_sm) * sm_count()) / groups;
+    if (splits_r < 1) splits_r = 1;
+    if (splits_r > rest_tiles) splits_r = rest_tiles;
+    per_r = (rest_tiles + splits_r - 1) / splits_r;
+    splits_r = (rest_tiles + per_r - 1) / per_r;
+  }
+  const int64_t splits = splits_f + splits_r;
+  Scratch part, gbins;
+  NSK_CUDA_OK(part.alloc(sizeof(double) * splits * n * s, st));
+  if (gb) NSK_CUDA_OK(gbins.alloc(sizeof(double) * splits * groups * NC * s, st));
+  if (full > 0) {
+    CsParams p{A, lda, n, s, tb->cs_table, rows.row0, 0, full, per_f, CT, 0, part.as<double>(),
+               gb ? gbins.as<double>() : nullptr};
+    const int rc = use_tma_ring() ? launch_nc<TMA_RING>(NC, gb, p, groups, splits_f, st, true)
+                                  : launch_nc<STREAM>(NC, gb, p, groups, splits_f, st, true);
+    if (rc) return rc;
+  }
+  if (rest_tiles > 0) {
+    const int64_t last_rows = rest_rows - (rest_tiles - 1) * CT;
+    CsParams p{A, lda, n, s, tb->cs_table, rows.row0, full, rest_tiles, per_r, last_rows, splits_f, part.as<double>(),
+               gb ? gbins.as<double>() + splits_f * groups * NC * s : nullptr};
+    if (int rc = launch_nc<GENERIC>(NC, gb, p, groups, splits_r, st, full == 0)) return rc;
+  }
   int64_t blocks = (s * n + 255) / 256;
   if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
   cs_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double>(), splits, s, n, SA, ldsa);

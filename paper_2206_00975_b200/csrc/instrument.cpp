@@ -19,7 +19,8 @@ thread_local std::vector<EvPair> t_free;
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-KernelTimer::KernelTimer(cudaStream_t s) : st(s) {
+KernelTimer::KernelTimer(cudaStream_t s, bool enabled) : st(s) {
+  if (!enabled) return;
   if (!g_timing.load(std::memory_order_relaxed)) return;
   EvPair p;
   if (!t_free.empty()) {

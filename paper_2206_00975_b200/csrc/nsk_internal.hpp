@@ -111,7 +111,7 @@ void count_launch(int n = 1);
 struct KernelTimer {
   cudaStream_t st;
   void* pair = nullptr;
-  explicit KernelTimer(cudaStream_t s);
+  explicit KernelTimer(cudaStream_t s, bool enabled = true);
   void stop();
 };
 

@@ -9,7 +9,7 @@ The SVD of the small SA then runs on the root rank (or every rank).
 Row maps:
   gaussian, countsketch, srht   contiguous shards (srht: multiples of 1024
                                 rows so the Hadamard split stays block-aligned;
-                                countsketch: multiples of 256 rows)
+                                countsketch: multiples of 512 rows)
   srft, srdct                   cyclic shards: rank g holds rows g, g+P, ...
                                 (decimation in time keeps every local
                                 transform a plain strided DFT)
@@ -31,7 +31,7 @@ class RowShard:
 
 
 def _align_for(kind: str) -> int:
-    return {"srht": 1024, "countsketch": 256}.get(kind, 1)
+    return {"srht": 1024, "countsketch": 512}.get(kind, 1)
 
 
 def row_partition(m: int, world: int, kind: str) -> List[RowShard]:

@@ -251,8 +251,10 @@ def test_cfg1_solve_k_parity(nsk, oracle):
     # differs by ~2e-17 between the two backends), so the sigma bound is absolute.
     assert np.max(np.abs(sig - sref)) <= 100 * U * sref[0]
     r, rref = np.linalg.norm(A @ W), np.linalg.norm(A @ Wref)
-    assert abs(r - rref) <= 1e-10 * max(rref, 1e3 * U * np.linalg.norm(A))
-    assert abs(nsk.residual_certificate(dev(A), res.W) - r) <= 1e-12 * max(r, 1e-300) + 1e-20
+    # 1e-10 relative, floored at the rounding level of evaluating ||A W||_F itself
+    # (100 u ||A||_F): at configs[0] the reorder-only gap is ~3e-18.
+    assert abs(r - rref) <= max(1e-10 * rref, 100 * U * np.linalg.norm(A))
+    assert abs(nsk.residual_certificate(dev(A), res.W) - r) <= max(1e-12 * r, 100 * U * np.linalg.norm(A))
     # the sketched solution is near-optimal (Theorem 3): ||AW|| within factor 4 of sigma_n
     assert r < 4 * spec[-1]
 
