@@ -29,11 +29,13 @@ struct DeviceTables {
   int32_t* srht_row = nullptr;      // output row of each slot
   uint32_t* sign_mask = nullptr;    // SRHT: m-bit Rademacher mask, lane-transposed per 1024 rows
   uint32_t* cs_table = nullptr;     // CountSketch: per-row bucket | sign | tile chain (4 B/row)
+  uint32_t* sign_bits = nullptr;    // srft/srdct: bit j of word j/32 = Rademacher bit of row j
 };
 
 // Device-side table builders (run once per operator and device).
 int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out);
 int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out);
+int build_sign_bits(PhiloxKey key, int64_t m, uint32_t** out);
 
 // The operator is its descriptor (sketch.cpp:303-313): nothing else is stored.
 struct Operator {

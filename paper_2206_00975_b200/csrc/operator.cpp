@@ -175,6 +175,7 @@ const DeviceTables* Operator::tables() const {
   }
   if (kind == SRHT && m >= 1024 && build_sign_mask(key0, m, &t.sign_mask) != OK) return nullptr;
   if (kind == COUNTSKETCH && s <= 65536 && build_cs_table(key0, m, s, &t.cs_table) != OK) return nullptr;
+  if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return nullptr;
   dev.push_back(t);
   return &dev.back();
 }
@@ -189,6 +190,7 @@ Operator::~Operator() {
     if (t.srht_row) cudaFree(t.srht_row);
     if (t.sign_mask) cudaFree(t.sign_mask);
     if (t.cs_table) cudaFree(t.cs_table);
+    if (t.sign_bits) cudaFree(t.sign_bits);
   }
   cudaSetDevice(cur);
 }

@@ -81,6 +81,16 @@ def test_srtt_apply_parity(nsk, oracle, kind, s, m, n):
     assert rel(got, ref) <= SA_TOL
 
 
+@pytest.mark.parametrize("kind,s,m,n,cplx", [("srdct", 1024, 1 << 16, 8, False), ("srft", 1000, 1 << 15, 5, True),
+                                             ("srft", 512, 3 << 12, 6, False), ("srdct", 300, 5 << 12, 4, False)])
+def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
+    """Blocked FFT path (m % 4096 == 0): sampled DFT / Makhoul DCT-III against scipy/numpy."""
+    A = oracle.random_complex(m, n, 3) if cplx else oracle.random_real(m, n, 3)
+    got, _ = gpu_apply(nsk, kind, s, m, 77, A)
+    ref = oracle.apply(oracle.draw(kind, s, m, 77), A)
+    assert rel(got, ref) <= SA_TOL
+
+
 def test_srft_complex_parity(nsk, oracle, golden):
     sa = golden["sa"]
     A = sa["A_srft"]
@@ -400,4 +410,19 @@ def test_cfg2_srht_full_size_properties(nsk, oracle):
     cols = [0, 77, 255]
     Ah = A[:, cols].cpu().numpy()
     ref = oracle.apply(oracle.draw("srht", s, m, 9000002), Ah)
+    assert rel(sa[:, cols].cpu().numpy(), ref) <= SA_TOL
+
+
+@pytest.mark.parametrize("kind", ["srdct", "srft"])
+def test_cfg2_srtt_full_size_properties(nsk, oracle, kind):
+    """configs[1] shape through the transform sketches: column sample vs scipy/numpy, re-run identity."""
+    import torch
+    m, n, s = 1 << 20, 64, 1024
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = torch.randn(n, m, dtype=torch.float64, device="cuda", generator=g).t()
+    S = nsk.SketchOperator.draw(kind, s, m, 9000005)
+    sa = nsk.apply(S, A).data
+    assert torch.equal(sa, nsk.apply(S, A).data)
+    cols = [0, 63]
+    ref = oracle.apply(oracle.draw(kind, s, m, 9000005), A[:, cols].cpu().numpy())
     assert rel(sa[:, cols].cpu().numpy(), ref) <= SA_TOL

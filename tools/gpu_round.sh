@@ -1,7 +1,11 @@
 #!/bin/bash
-# usage: tools/gpu_round.sh "<kinds>" [pytest-args]   -- run inside gpurun
+# usage: tools/gpu_round.sh "<kinds>" [pytest -k expression]   -- run inside gpurun
 cd "$(dirname "$0")/.."
-timeout 900 python -m pytest tests -m gpu -q --timeout 300 -x $2 > gpurun_out/pytest_gpu.log 2>&1
+if [ -n "$2" ]; then
+  timeout 900 python -m pytest tests -m gpu -q --timeout 300 -k "$2" > gpurun_out/pytest_gpu.log 2>&1
+else
+  timeout 900 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1
+fi
 tail -3 gpurun_out/pytest_gpu.log
 for k in $1; do
   timeout 400 python bench.py --kind $k --steps 20 --warmup 3 --e2e-steps 2 > gpurun_out/bench_$k.log 2>&1
