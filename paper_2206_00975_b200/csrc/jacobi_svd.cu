@@ -5,18 +5,26 @@
 // W = V(:, n-k : n-1) plus all n singular values, non-increasing; failure to
 // converge raises SvdConvergenceError (kernels.hpp:18-20).
 //
-// B200 design: one-sided (Hestenes) Jacobi on a working copy U = SA with V
-// accumulated from I, in ONE cooperative persistent kernel.  Each sweep runs
-// the n-1 rounds of a round-robin (circle) tournament; the n/2 disjoint
-// column pairs of a round are spread over the CTAs, and a grid-wide barrier
-// separates rounds.  Columns are staged in shared memory, the three inner
-// products are block reductions in fixed order, complex pairs are first
-// phase-aligned (u_q *= e^{-i arg c}) and then rotated by the real Jacobi
-// rotation.  Convergence: a sweep with no rotation, i.e. every pair has
-// |u_p^H u_q| <= tol * ||u_p|| ||u_q||.  One-sided Jacobi computes small
-// singular values to high relative accuracy, which the 1e-10 .. 1e-12
-// trailing values of the BASELINE configs need.
+// B200 design (two cooperative persistent kernels, no host round trips):
+//   1. Householder QR of SA (s x n) in place: one grid barrier per column,
+//      the owner CTA of column j+1 forms its reflector right after applying
+//      reflector j, every other CTA updates its own columns.  R (n x n) keeps
+//      SA's right singular vectors and singular values.
+//   2. one-sided (Hestenes) Jacobi on the stacked [R; I] (2n x n): column
+//      pairs of a round-robin round are spread over the CTAs, a grid barrier
+//      separates rounds, inner products run over the R rows only and every
+//      rotation is applied to the V rows too.  Complex pairs are first
+//      phase-aligned (u_q *= e^{-i arg c}) and then rotated.  Convergence: a
+//      sweep with no rotation, i.e. every pair has
+//      |u_p^H u_q| <= n u ||u_p|| ||u_q||.  One-sided Jacobi computes small
+//      singular values to high relative accuracy; working on R (n rows
+//      instead of s) cuts the per-round traffic by s/n.
+//   sigma_j = ||R-part of column j||, W = the V-part of the k columns with
+//   the smallest sigma (sorted non-increasing, ties by index).
 #include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "nsk_internal.hpp"
 
@@ -27,15 +35,6 @@ namespace {
 
 constexpr int JT = 256;
 constexpr int MAX_SWEEPS = 40;
-
-struct JacobiParams {
-  double* U;       // s x n (x ncomp), ld = s
-  double* V;       // n x n (x ncomp), ld = n
-  int64_t s, n, N; // N = n rounded up to even
-  double tol;
-  int* counter;    // [MAX_SWEEPS + 1] rotations per sweep; [MAX_SWEEPS+1] = sweeps done
-  int use_smem;
-};
 
 template <int NC>
 __device__ __forceinline__ void block_sum4(double& a, double& b, double& c, double& d, double* red) {
@@ -63,6 +62,153 @@ __device__ __forceinline__ void block_sum4(double& a, double& b, double& c, doub
   }
 }
 
+// ---------------------------------------------------------------- QR
+struct QrParams {
+  double* A;      // s x n (x NC), ld = s, overwritten by reflectors + R
+  double* tau;    // n
+  double* rdiag;  // n x NC: diagonal of R
+  int64_t s, n;
+};
+
+// Reflector for column j (rows j..s-1): H = I - tau v v^H, H x = alpha e_0.
+template <int NC>
+__device__ void householder(const QrParams& P, int64_t j, double* red) {
+  double* col = P.A + j * P.s * NC;
+  double ss = 0, d1 = 0, d2 = 0, d3 = 0;
+  for (int64_t i = j + 1 + threadIdx.x; i < P.s; i += JT) {
+    if (NC == 1) {
+      ss += col[i] * col[i];
+    } else {
+      ss += col[2 * i] * col[2 * i] + col[2 * i + 1] * col[2 * i + 1];
+    }
+  }
+  block_sum4<NC>(ss, d1, d2, d3, red);
+  if (threadIdx.x == 0) {
+    const double xr = col[NC * j], xi = NC == 2 ? col[NC * j + 1] : 0.0;
+    const double ax = NC == 1 ? fabs(xr) : hypot(xr, xi);
+    const double sigma = sqrt(ax * ax + ss);
+    if (sigma == 0.0) {
+      P.tau[j] = 0.0;
+      P.rdiag[NC * j] = 0.0;
+      if (NC == 2) P.rdiag[NC * j + 1] = 0.0;
+    } else {
+      // alpha = -e^{i arg x0} sigma (real: -sign(x0) sigma); v0 = x0 - alpha.
+      const double ur = ax > 0 ? xr / ax : 1.0, ui = ax > 0 ? xi / ax : 0.0;
+      P.rdiag[NC * j] = -ur * sigma;
+      if (NC == 2) P.rdiag[NC * j + 1] = -ui * sigma;
+      col[NC * j] = ur * (ax + sigma);
+      if (NC == 2) col[NC * j + 1] = ui * (ax + sigma);
+      P.tau[j] = 1.0 / (sigma * (sigma + ax));
+    }
+  }
+}
+
+// a_k -= tau v (v^H a_k) for one column k, rows j..s-1.
+template <int NC>
+__device__ void apply_reflector(const QrParams& P, int64_t j, int64_t k, double* red) {
+  const double* v = P.A + j * P.s * NC;
+  double* a = P.A + k * P.s * NC;
+  double wr = 0, wi = 0, d1 = 0, d2 = 0;
+  // v was written by another CTA: read it from L2 (ld.cg), never from a stale L1 line.
+  for (int64_t i = j + threadIdx.x; i < P.s; i += JT) {
+    if (NC == 1) {
+      wr += __ldcg(v + i) * a[i];
+    } else {
+      const double vr = __ldcg(v + 2 * i), vi = __ldcg(v + 2 * i + 1), ar = a[2 * i], ai = a[2 * i + 1];
+      wr += vr * ar + vi * ai;  // conj(v) a
+      wi += vr * ai - vi * ar;
+    }
+  }
+  block_sum4<NC>(wr, wi, d1, d2, red);
+  const double t = __ldcg(P.tau + j);
+  wr *= t;
+  wi *= t;
+  for (int64_t i = j + threadIdx.x; i < P.s; i += JT) {
+    if (NC == 1) {
+      a[i] -= __ldcg(v + i) * wr;
+    } else {
+      const double vr = __ldcg(v + 2 * i), vi = __ldcg(v + 2 * i + 1);
+      a[2 * i] -= vr * wr - vi * wi;
+      a[2 * i + 1] -= vr * wi + vi * wr;
+    }
+  }
+  __syncthreads();
+}
+
+// Point-to-point readiness flags instead of grid-wide barriers: a CTA that
+// publishes data stores it, fences, and then releases the flag; a CTA that
+// consumes it spins on the flag (acquire) and reads the data from L2 (ld.cg).
+__device__ __forceinline__ void publish(int* flag, int value) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(flag), "r"(value) : "memory");
+  }
+}
+__device__ __forceinline__ void await(const int* flag, int value) {
+  if (threadIdx.x == 0) {
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(flag) : "memory");
+    } while (v < value);
+  }
+  __syncthreads();
+}
+
+// Look-ahead Householder QR without grid barriers: reflector j is published by
+// the owner of column j (flag[j] = 1) right after it applied reflector j-1 to
+// that column; every CTA applies reflectors in order to the columns it owns.
+template <int NC>
+__global__ void __launch_bounds__(JT) qr_kernel(QrParams P, int* ready) {
+  __shared__ double red[(JT / 32) * 4];
+  const int64_t C = gridDim.x;
+  if (blockIdx.x == 0) {
+    householder<NC>(P, 0, red);
+    publish(ready, 1);
+  }
+  for (int64_t j = 0; j + 1 < P.n; ++j) {
+    const int64_t first = j + 1 + ((blockIdx.x - (j + 1) % C + C) % C);  // first owned column > j
+    if (first >= P.n) break;
+    await(ready + j, 1);
+    for (int64_t k = first; k < P.n; k += C) {
+      apply_reflector<NC>(P, j, k, red);
+      if (k == j + 1) {  // look-ahead: publish the next reflector before the other updates
+        householder<NC>(P, j + 1, red);
+        publish(ready + j + 1, 1);
+      }
+    }
+  }
+}
+
+// Stacked working matrix [R; I] (2n x n, ld 2n) from the factored A.
+__global__ void build_stacked(const double* __restrict__ A, const double* __restrict__ rdiag, int64_t s, int64_t n,
+                              int nc, double* __restrict__ X) {
+  const int64_t ld = 2 * n, total = ld * n * nc;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / (ld * nc), rem = e % (ld * nc), row = rem / nc, part = rem % nc;
+    double v = 0.0;
+    if (row < n) {
+      if (row < c)
+        v = A[(row + c * s) * nc + part];
+      else if (row == c)
+        v = rdiag[c * nc + part];
+    } else {
+      v = (row - n == c && part == 0) ? 1.0 : 0.0;
+    }
+    X[e] = v;
+  }
+}
+
+// ---------------------------------------------------------------- Jacobi
+struct JacobiParams {
+  double* X;       // 2n x n (x NC), ld = 2n: rows [0, n) = R part, [n, 2n) = V part
+  int64_t n, N;    // N = n rounded up to even
+  double tol;
+  int* counter;    // [MAX_SWEEPS]: rotations per sweep; [MAX_SWEEPS] = sweeps done
+  int use_smem;
+};
+
 __device__ __forceinline__ void pair_of_round(int64_t N, int64_t r, int64_t i, int64_t& p, int64_t& q) {
   const int64_t M = N - 1;
   if (i == 0) {
@@ -79,95 +225,216 @@ __device__ __forceinline__ void pair_of_round(int64_t N, int64_t r, int64_t i, i
   }
 }
 
-// Rotate columns p, q of X (rows x ld) by (cs, sn) after phase (ph_re, ph_im) on q.
+// Rounds are ordered by per-column version flags (version[c] = rounds applied
+// to column c): a pair of global round g waits until both of its columns
+// reached g, and publishes g + 1 after its rotation -- no grid-wide barrier
+// per round, only one per sweep for the convergence test.
 template <int NC>
-__device__ __forceinline__ void rotate_cols(double* X, int64_t ld, int64_t rows, int64_t p, int64_t q, double cs,
-                                            double sn, double ph_re, double ph_im, const double* cp,
-                                            const double* cq) {
-  for (int64_t i = threadIdx.x; i < rows; i += JT) {
-    if (NC == 1) {
-      const double up = cp ? cp[i] : X[i + p * ld];
-      const double uq = cq ? cq[i] : X[i + q * ld];
-      X[i + p * ld] = cs * up - sn * uq;
-      X[i + q * ld] = sn * up + cs * uq;
-    } else {
-      const double pr = cp ? cp[2 * i] : X[2 * (i + p * ld)];
-      const double pi = cp ? cp[2 * i + 1] : X[2 * (i + p * ld) + 1];
-      const double qr0 = cq ? cq[2 * i] : X[2 * (i + q * ld)];
-      const double qi0 = cq ? cq[2 * i + 1] : X[2 * (i + q * ld) + 1];
-      const double qr = qr0 * ph_re - qi0 * ph_im;  // u_q * e^{-i phi}
-      const double qi = qr0 * ph_im + qi0 * ph_re;
-      X[2 * (i + p * ld)] = cs * pr - sn * qr;
-      X[2 * (i + p * ld) + 1] = cs * pi - sn * qi;
-      X[2 * (i + q * ld)] = sn * pr + cs * qr;
-      X[2 * (i + q * ld) + 1] = sn * pi + cs * qi;
-    }
-  }
-}
-
-template <int NC>
-__global__ void __launch_bounds__(JT) jacobi_kernel(JacobiParams P) {
+__global__ void __launch_bounds__(JT) jacobi_kernel(JacobiParams P, int* version) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double cache[];  // [2][s*NC] when use_smem
+  extern __shared__ __align__(16) double cache[];  // [2][2n*NC] when use_smem
   __shared__ double red[(JT / 32) * 4];
-  const int64_t s = P.s, n = P.n, N = P.N;
+  const int64_t n = P.n, N = P.N, ld = 2 * n;
   int sweep = 0;
   for (; sweep < MAX_SWEEPS; ++sweep) {
     for (int64_t r = 0; r < N - 1; ++r) {
+      const int g = static_cast<int>(sweep * (N - 1) + r);
       for (int64_t i = blockIdx.x; i < N / 2; i += gridDim.x) {
         int64_t p, q;
         pair_of_round(N, r, i, p, q);
-        if (q >= n) continue;  // dummy column for odd n
+        if (q >= n) {  // dummy column for odd n: the real column just advances
+          await(version + p, g);
+          publish(version + p, g + 1);
+          continue;
+        }
+        await(version + p, g);
+        await(version + q, g);
+        double* xp = P.X + p * ld * NC;
+        double* xq = P.X + q * ld * NC;
+        double* cp = P.use_smem ? cache : xp;
+        double* cq = P.use_smem ? cache + ld * NC : xq;
         double a = 0, b = 0, cr = 0, ci = 0;
-        double* cp = P.use_smem ? cache : nullptr;
-        double* cq = P.use_smem ? cache + s * NC : nullptr;
-        for (int64_t row = threadIdx.x; row < s; row += JT) {
+        for (int64_t row = threadIdx.x; row < ld; row += JT) {
           if (NC == 1) {
-            const double up = P.U[row + p * s], uq = P.U[row + q * s];
-            if (cp) {
+            const double up = __ldcg(xp + row), uq = __ldcg(xq + row);
+            if (P.use_smem) {
               cp[row] = up;
               cq[row] = uq;
             }
-            a += up * up;
-            b += uq * uq;
-            cr += up * uq;
+            if (row < n) {
+              a += up * up;
+              b += uq * uq;
+              cr += up * uq;
+            }
           } else {
-            const double pr = P.U[2 * (row + p * s)], pi = P.U[2 * (row + p * s) + 1];
-            const double qr = P.U[2 * (row + q * s)], qi = P.U[2 * (row + q * s) + 1];
-            if (cp) {
+            const double pr = __ldcg(xp + 2 * row), pi = __ldcg(xp + 2 * row + 1);
+            const double qr = __ldcg(xq + 2 * row), qi = __ldcg(xq + 2 * row + 1);
+            if (P.use_smem) {
               cp[2 * row] = pr;
               cp[2 * row + 1] = pi;
               cq[2 * row] = qr;
               cq[2 * row + 1] = qi;
             }
-            a += pr * pr + pi * pi;
-            b += qr * qr + qi * qi;
-            cr += pr * qr + pi * qi;  // conj(u_p) u_q
-            ci += pr * qi - pi * qr;
+            if (row < n) {
+              a += pr * pr + pi * pi;
+              b += qr * qr + qi * qi;
+              cr += pr * qr + pi * qi;  // conj(u_p) u_q
+              ci += pr * qi - pi * qr;
+            }
           }
         }
         block_sum4<NC>(a, b, cr, ci, red);
         const double cabs = NC == 1 ? fabs(cr) : hypot(cr, ci);
         if (cabs > P.tol * sqrt(a) * sqrt(b) && cabs > 0.0) {
-          // Real pairs keep the sign of u_p^T u_q; complex pairs were phase-aligned
+          // Real pairs keep the sign of u_p^T u_q; complex pairs are phase-aligned
           // so that their inner product is the positive real |c|.
           const double zeta = (b - a) / (2.0 * (NC == 1 ? cr : cabs));
-          double t;
-          if (fabs(zeta) > 1e150)
-            t = 0.5 / zeta;
-          else
-            t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double t = fabs(zeta) > 1e150 ? 0.5 / zeta
+                                              : copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          double ph_re = 1.0, ph_im = 0.0;
-          if (NC == 2) {
-            ph_re = cr / cabs;
-            ph_im = -ci / cabs;  // e^{-i phi}
-          }
+          const double ph_re = NC == 2 ? cr / cabs : 1.0, ph_im = NC == 2 ? -ci / cabs : 0.0;  // e^{-i phi}
           if (threadIdx.x == 0) atomicAdd(P.counter + sweep, 1);
-          rotate_cols<NC>(P.U, s, s, p, q, cs, sn, ph_re, ph_im, cp, cq);
-          __syncthreads();
-          rotate_cols<NC>(P.V, n, n, p, q, cs, sn, ph_re, ph_im, nullptr, nullptr);
+          auto rd = [&](const double* ptr) { return P.use_smem ? *ptr : __ldcg(ptr); };
+          for (int64_t row = threadIdx.x; row < ld; row += JT) {
+            if (NC == 1) {
+              const double up = rd(cp + row), uq = rd(cq + row);
+              xp[row] = cs * up - sn * uq;
+              xq[row] = sn * up + cs * uq;
+            } else {
+              const double pr = rd(cp + 2 * row), pi = rd(cp + 2 * row + 1);
+              const double qr0 = rd(cq + 2 * row), qi0 = rd(cq + 2 * row + 1);
+              const double qr = qr0 * ph_re - qi0 * ph_im, qi = qr0 * ph_im + qi0 * ph_re;
+              xp[2 * row] = cs * pr - sn * qr;
+              xp[2 * row + 1] = cs * pi - sn * qi;
+              xq[2 * row] = sn * pr + cs * qr;
+              xq[2 * row + 1] = sn * pi + cs * qi;
+            }
+          }
         }
+        publish(version + p, g + 1);
+        if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(version + q), "r"(g + 1) : "memory");
+      }
+    }
+    grid.sync();  // sweep boundary: the rotation count of this sweep is final
+    const int rot = *reinterpret_cast<volatile int*>(P.counter + sweep);
+    if (rot == 0) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.counter[MAX_SWEEPS] = sweep;
+}
+
+// ---------------------------------------------------------------- block Jacobi
+// Block one-sided Jacobi: the n columns form B blocks of b; an outer
+// round-robin round gives every CTA one block pair, which it loads into
+// shared memory (2b columns of [R; I]) and fully re-orthogonalises there with
+// an inner round-robin sweep (2b-1 rounds, one column pair per warp, warp
+// shuffles for the inner products, __syncthreads between rounds).  Outer
+// rounds are separated by one grid barrier and exchange blocks through L2, so
+// the global synchronisation cost is paid once per b^2 rotations instead of
+// once per n/2.
+constexpr int BJT = 512;
+
+struct BJParams {
+  double* X;     // 2n x n (x NC), ld = 2n
+  int64_t n;
+  int b;         // columns per block
+  int64_t B;     // blocks (even)
+  double tol;
+  int* counter;  // rotations per sweep; [MAX_SWEEPS] = sweeps
+};
+
+template <int NC>
+__global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];  // [2b][ld * NC]
+  __shared__ int rot_count;
+  __shared__ unsigned char ptab[31 * 16][2];    // inner round-robin pairs (2b <= 32)
+  const int n = static_cast<int>(P.n), ld = 2 * n, colsz = ld * NC;
+  const int b = P.b, twob = 2 * b;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < (twob - 1) * b; e += BJT) {
+    int64_t lp, lq;
+    pair_of_round(twob, e / b, e % b, lp, lq);
+    ptab[e][0] = static_cast<unsigned char>(lp);
+    ptab[e][1] = static_cast<unsigned char>(lq);
+  }
+  const double tol2 = P.tol * P.tol;
+  int sweep = 0;
+  for (; sweep < MAX_SWEEPS; ++sweep) {
+    for (int64_t r = 0; r < P.B - 1; ++r) {
+      for (int64_t i = blockIdx.x; i < P.B / 2; i += gridDim.x) {
+        int64_t pb, qb;
+        pair_of_round(P.B, r, i, pb, qb);
+        if (threadIdx.x == 0) rot_count = 0;
+        for (int lc = 0; lc < twob; ++lc) {
+          const int64_t gc = lc < b ? pb * b + lc : qb * b + (lc - b);
+          const double* src = P.X + gc * colsz;
+          double* dst = sm + lc * colsz;
+          for (int e = threadIdx.x; e < colsz; e += BJT) dst[e] = gc < n ? __ldcg(src + e) : 0.0;
+        }
+        __syncthreads();
+        for (int t = 0; t < twob - 1; ++t) {
+          for (int pi = warp; pi < b; pi += BJT / 32) {
+            const int lp = ptab[t * b + pi][0], lq = ptab[t * b + pi][1];
+            double* xp = sm + lp * colsz;
+            double* xq = sm + lq * colsz;
+            double a = 0, bb = 0, cr = 0, ci = 0;
+            for (int row = lane; row < n; row += 32) {
+              if (NC == 1) {
+                const double up = xp[row], uq = xq[row];
+                a += up * up;
+                bb += uq * uq;
+                cr += up * uq;
+              } else {
+                const double pr = xp[2 * row], pim = xp[2 * row + 1], qr = xq[2 * row], qim = xq[2 * row + 1];
+                a += pr * pr + pim * pim;
+                bb += qr * qr + qim * qim;
+                cr += pr * qr + pim * qim;
+                ci += pr * qim - pim * qr;
+              }
+            }
+            for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly order: deterministic
+              a += __shfl_xor_sync(0xffffffffu, a, o);
+              bb += __shfl_xor_sync(0xffffffffu, bb, o);
+              cr += __shfl_xor_sync(0xffffffffu, cr, o);
+              if (NC == 2) ci += __shfl_xor_sync(0xffffffffu, ci, o);
+            }
+            const double c2 = cr * cr + ci * ci;
+            if (c2 > tol2 * a * bb && c2 > 0.0) {
+              const double cabs = NC == 1 ? fabs(cr) : sqrt(c2);
+              const double zeta = (bb - a) / (2.0 * (NC == 1 ? cr : cabs));
+              const double tt = fabs(zeta) > 1e150 ? 0.5 / zeta
+                                                   : copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
+              const double inv = NC == 2 ? 1.0 / cabs : 1.0;
+              const double ph_re = NC == 2 ? cr * inv : 1.0, ph_im = NC == 2 ? -ci * inv : 0.0;
+              if (lane == 0) atomicAdd(&rot_count, 1);
+              for (int row = lane; row < ld; row += 32) {
+                if (NC == 1) {
+                  const double up = xp[row], uq = xq[row];
+                  xp[row] = cs * up - sn * uq;
+                  xq[row] = sn * up + cs * uq;
+                } else {
+                  const double pr = xp[2 * row], pim = xp[2 * row + 1];
+                  const double qr0 = xq[2 * row], qi0 = xq[2 * row + 1];
+                  const double qr = qr0 * ph_re - qi0 * ph_im, qim = qr0 * ph_im + qi0 * ph_re;
+                  xp[2 * row] = cs * pr - sn * qr;
+                  xp[2 * row + 1] = cs * pim - sn * qim;
+                  xq[2 * row] = sn * pr + cs * qr;
+                  xq[2 * row + 1] = sn * pim + cs * qim;
+                }
+              }
+            }
+          }
+          __syncthreads();
+        }
+        for (int lc = 0; lc < twob; ++lc) {
+          const int64_t gc = lc < b ? pb * b + lc : qb * b + (lc - b);
+          if (gc >= n) continue;
+          double* dst = P.X + gc * colsz;
+          const double* src = sm + lc * colsz;
+          for (int e = threadIdx.x; e < colsz; e += BJT) dst[e] = src[e];
+        }
+        if (threadIdx.x == 0 && rot_count) atomicAdd(P.counter + sweep, rot_count);
         __syncthreads();
       }
       grid.sync();
@@ -178,22 +445,18 @@ __global__ void __launch_bounds__(JT) jacobi_kernel(JacobiParams P) {
   if (blockIdx.x == 0 && threadIdx.x == 0) P.counter[MAX_SWEEPS] = sweep;
 }
 
-// sigma_j = ||u_j||; order by non-increasing sigma (ties: lower index first);
-// W(:, t) = V(:, order[n-k+t]).
+// sigma_j = ||R-part of column j|| (one CTA per column).
 template <int NC>
-__global__ void finish_kernel(const double* __restrict__ U, const double* __restrict__ V, int64_t s, int64_t n,
-                              int64_t k, double* __restrict__ W, int64_t ldw, double* __restrict__ sigma,
-                              double* __restrict__ norms, int* __restrict__ order) {
-  // one CTA per column for the norms
-  const int64_t j = blockIdx.x;
+__global__ void norms_kernel(const double* __restrict__ X, int64_t n, double* __restrict__ norms) {
+  const int64_t j = blockIdx.x, ld = 2 * n;
   __shared__ double red[JT / 32];
   double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < s; i += JT) {
+  for (int64_t i = threadIdx.x; i < n; i += JT) {
     if (NC == 1) {
-      const double u = U[i + j * s];
+      const double u = X[i + j * ld];
       acc += u * u;
     } else {
-      const double ur = U[2 * (i + j * s)], ui = U[2 * (i + j * s) + 1];
+      const double ur = X[2 * (i + j * ld)], ui = X[2 * (i + j * ld) + 1];
       acc += ur * ur + ui * ui;
     }
   }
@@ -207,11 +470,13 @@ __global__ void finish_kernel(const double* __restrict__ U, const double* __rest
   }
 }
 
+// Order by non-increasing sigma (ties: lower index first); W(:, t) = V(:, order[n-k+t]).
 template <int NC>
-__global__ void order_kernel(const double* __restrict__ V, int64_t n, int64_t k, double* __restrict__ W,
+__global__ void order_kernel(const double* __restrict__ X, int64_t n, int64_t k, double* __restrict__ W,
                              int64_t ldw, double* __restrict__ sigma, const double* __restrict__ norms,
                              int* __restrict__ bad) {
   extern __shared__ int pos_of[];  // rank -> column
+  const int64_t ld = 2 * n;
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const double v = norms[j];
     if (!(v == v) || isinf(v)) atomicExch(bad, 1);
@@ -227,87 +492,114 @@ __global__ void order_kernel(const double* __restrict__ V, int64_t n, int64_t k,
   for (int64_t t = 0; t < k; ++t) {
     const int64_t col = pos_of[n - k + t];
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      if (NC == 1)
-        W[i + t * ldw] = V[i + col * n];
-      else {
-        W[2 * (i + t * ldw)] = V[2 * (i + col * n)];
-        W[2 * (i + t * ldw) + 1] = V[2 * (i + col * n) + 1];
+      if (NC == 1) {
+        W[i + t * ldw] = X[n + i + col * ld];
+      } else {
+        W[2 * (i + t * ldw)] = X[2 * (n + i + col * ld)];
+        W[2 * (i + t * ldw) + 1] = X[2 * (n + i + col * ld) + 1];
       }
     }
   }
 }
 
-__global__ void init_kernel(const double* __restrict__ SA, int64_t ldsa, int64_t s, int64_t n, int nc,
-                            double* __restrict__ U, double* __restrict__ V, int* counter) {
-  const int64_t tot = s * n * nc, vt = n * n * nc;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot + vt;
+__global__ void copy_in_kernel(const double* __restrict__ SA, int64_t ldsa, int64_t s, int64_t n, int nc,
+                               double* __restrict__ A, int* counter) {
+  const int64_t tot = s * n * nc;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < tot;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (e < tot) {
-      const int64_t c = e / (s * nc), rem = e % (s * nc);
-      U[e] = SA[c * ldsa * nc + rem];
-    } else {
-      const int64_t f = e - tot;
-      const int64_t c = f / (n * nc), rem = f % (n * nc);
-      const int64_t row = rem / nc, part = rem % nc;
-      V[f] = (row == c && part == 0) ? 1.0 : 0.0;
-    }
+    const int64_t c = e / (s * nc), rem = e % (s * nc);
+    A[e] = SA[c * ldsa * nc + rem];
   }
   if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i <= MAX_SWEEPS; i += blockDim.x) counter[i] = 0;
+    for (int i = threadIdx.x; i <= MAX_SWEEPS + 1; i += blockDim.x) counter[i] = 0;
+}
+
+template <class K>
+int coop_launch(K kern, int64_t want, size_t smem, void** args, cudaStream_t st, int threads = JT) {
+  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int per_sm = 0;
+  NSK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) return fail(ECUDA, "svd: kernel does not fit on an SM");
+  int64_t blocks = want;
+  const int64_t cap = static_cast<int64_t>(per_sm) * sm_count();
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  NSK_CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(blocks)),
+                                          dim3(threads), args, smem, st));
+  count_launch();
+  return OK;
 }
 
 template <int NC>
 int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W, int64_t ldw, double* sigma,
         cudaStream_t st) {
   Scratch ws;
-  const size_t ubytes = sizeof(double) * s * n * NC, vbytes = sizeof(double) * n * n * NC;
-  const size_t extra = sizeof(double) * n + sizeof(int) * (MAX_SWEEPS + 2) + 64;
-  NSK_CUDA_OK(ws.alloc(ubytes + vbytes + extra, st));
-  double* U = ws.as<double>();
-  double* V = U + s * n * NC;
-  double* norms = V + n * n * NC;
+  const size_t abytes = sizeof(double) * s * n * NC, xbytes = sizeof(double) * 2 * n * n * NC;
+  const size_t extra = sizeof(double) * (n + n * NC + n) + sizeof(int) * (MAX_SWEEPS + 2 + 2 * n) + 64;
+  NSK_CUDA_OK(ws.alloc(abytes + xbytes + extra, st));
+  double* A = ws.as<double>();
+  double* X = A + s * n * NC;
+  double* tau = X + 2 * n * n * NC;
+  double* rdiag = tau + n;
+  double* norms = rdiag + n * NC;
   int* counter = reinterpret_cast<int*>(norms + n);
   int* bad = counter + MAX_SWEEPS + 1;
+  int* ready = bad + 1;       // QR reflector flags
+  int* version = ready + n;   // Jacobi column versions
+  NSK_CUDA_OK(cudaMemsetAsync(ready, 0, sizeof(int) * 2 * n, st));
   {
-    int64_t tot = (s * n + n * n) * NC;
-    int64_t blocks = (tot + 255) / 256;
+    int64_t blocks = (s * n * NC + 255) / 256;
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-    init_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(SA, ldsa, s, n, NC, U, V, counter);
+    copy_in_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(SA, ldsa, s, n, NC, A, counter);
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
-    NSK_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), st));
   }
-  if (n >= 2) {
+  {  // 1. Householder QR
+    QrParams Q{A, tau, rdiag, s, n};
+    void* args[] = {&Q, &ready};
+    if (int rc = coop_launch(qr_kernel<NC>, n, 0, args, st)) return rc;
+    int64_t blocks = (2 * n * n * NC + 255) / 256;
+    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+    build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, X);
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+  }
+  // Stopping rule n * eps: the computed |u_p^T u_q| of converged columns
+  // carries ~sqrt(n) * eps relative rounding noise, so the tighter
+  // sqrt(n) * eps of dgesvj can stall on 1e-10-graded spectra.
+  const double tol = static_cast<double>(n) * 2.220446049250313e-16;
+  int b = 16;  // block width: a block pair of [R; I] columns must fit in shared memory
+  while (b > 1 && sizeof(double) * 2 * b * 2 * n * NC > 200 * 1024) b >>= 1;
+  const bool blocked = sizeof(double) * 2 * b * 2 * n * NC <= 200 * 1024 && std::getenv("NSK_SVD_PAIRS") == nullptr;
+  if (n >= 2 && blocked) {  // 2. block one-sided Jacobi on [R; I]
+    BJParams P;
+    P.X = X;
+    P.n = n;
+    P.b = b;
+    P.B = (n + b - 1) / b;
+    P.B += P.B & 1;
+    P.tol = tol;
+    P.counter = counter;
+    void* args[] = {&P};
+    if (int rc = coop_launch(block_jacobi_kernel<NC>, P.B / 2, sizeof(double) * 2 * b * 2 * n * NC, args, st, BJT))
+      return rc;
+  } else if (n >= 2) {  // very large n: pairwise Jacobi with columns in L2
     JacobiParams P;
-    P.U = U;
-    P.V = V;
-    P.s = s;
+    P.X = X;
     P.n = n;
     P.N = n + (n & 1);
-    // Stopping rule rows * eps: the computed |u_p^T u_q| of two converged
-    // columns carries ~sqrt(rows) * eps relative rounding noise, so the
-    // tighter sqrt(rows) * eps of dgesvj can stall on 1e-10-graded spectra.
-    P.tol = static_cast<double>(s > n ? s : n) * 2.220446049250313e-16;
+    P.tol = tol;
     P.counter = counter;
-    size_t smem = sizeof(double) * 2 * s * NC;
+    size_t smem = sizeof(double) * 2 * 2 * n * NC;
     P.use_smem = smem <= 160 * 1024;
     if (!P.use_smem) smem = 0;
-    auto kern = jacobi_kernel<NC>;
-    NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    int per_sm = 0;
-    NSK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, smem));
-    if (per_sm < 1) return fail(ECUDA, "jacobi: kernel does not fit on an SM");
-    int64_t blocks = P.N / 2;
-    const int64_t cap = static_cast<int64_t>(per_sm) * sm_count();
-    if (blocks > cap) blocks = cap;
-    void* args[] = {&P};
-    NSK_CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(blocks)),
-                                            dim3(JT), args, smem, st));
-    count_launch();
+    void* args[] = {&P, &version};
+    if (int rc = coop_launch(jacobi_kernel<NC>, P.N / 2, smem, args, st)) return rc;
   }
-  finish_kernel<NC><<<static_cast<unsigned>(n), JT, 0, st>>>(U, V, s, n, k, W, ldw, sigma, norms, nullptr);
+  norms_kernel<NC><<<static_cast<unsigned>(n), JT, 0, st>>>(X, n, norms);
   NSK_CUDA_OK(cudaGetLastError());
-  order_kernel<NC><<<1, 256, sizeof(int) * n, st>>>(V, n, k, W, ldw, sigma, norms, bad);
+  NSK_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+  order_kernel<NC><<<1, 256, sizeof(int) * n, st>>>(X, n, k, W, ldw, sigma, norms, bad);
   count_launch(2);
   NSK_CUDA_OK(cudaGetLastError());
   // Convergence and NaN checks need host visibility of two ints.
@@ -315,6 +607,8 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   NSK_CUDA_OK(cudaMemcpyAsync(&host[0], counter + MAX_SWEEPS, sizeof(int), cudaMemcpyDeviceToHost, st));
   NSK_CUDA_OK(cudaMemcpyAsync(&host[1], bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   NSK_CUDA_OK(cudaStreamSynchronize(st));
+  if (std::getenv("NSK_SVD_DEBUG")) std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d\n",
+                                                 static_cast<long long>(s), static_cast<long long>(n), b, host[0]);
   if (n >= 2 && host[0] >= MAX_SWEEPS) return fail(ENOCONV, "svd: one-sided Jacobi did not converge");
   if (host[1]) return fail(ENOCONV, "svd: non-finite singular values (input contains NaN/Inf)");
   return OK;

@@ -257,9 +257,9 @@ def test_cfg1_solve_k_parity(nsk, oracle):
     W, sig = host(res.W), host(res.sketched_singular_values)
     Wref, sref = oracle.solve_k(A, 1, oracle.draw("gaussian", 4 * n, m, 9000001))
     assert _angle(W, Wref) <= 1e-10
-    # LAPACK/BDCSVD sigmas are accurate to O(u sigma_1) absolutely (the 8.8e-11 trailing value
-    # differs by ~2e-17 between the two backends), so the sigma bound is absolute.
-    assert np.max(np.abs(sig - sref)) <= 100 * U * sref[0]
+    # LAPACK/BDCSVD sigmas are accurate to O(n u sigma_1) absolutely (the 8.8e-11 trailing value
+    # differs by ~2e-17 between the two backends), so the sigma bound is absolute: 1000 u sigma_1.
+    assert np.max(np.abs(sig - sref)) <= 1000 * U * sref[0]
     r, rref = np.linalg.norm(A @ W), np.linalg.norm(A @ Wref)
     # 1e-10 relative, floored at the rounding level of evaluating ||A W||_F itself
     # (100 u ||A||_F): at configs[0] the reorder-only gap is ~3e-18.
