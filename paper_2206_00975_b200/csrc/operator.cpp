@@ -137,6 +137,38 @@ int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out)
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
       return (op->idx[a] & mask) < (op->idx[b] & mask);
     });
+    // Bank-balanced slot order for the kernel's shared-memory gather: slot t is
+    // read by lane t % 32, and the value of row r_lo sits at double offset
+    // r_lo + r_lo / 32, i.e. in 8-byte bank pair (r_lo + r_lo / 32) % 16.  Fill
+    // each half-warp (16 consecutive slots) with distinct bank pairs where the
+    // sample allows it, taking rows in increasing r_lo within each class.
+    if (lb == 10) {
+      std::vector<std::vector<int32_t>> cls(16);
+      for (int32_t r : order) {
+        const int64_t lo = op->idx[static_cast<size_t>(r)] & mask;
+        cls[static_cast<size_t>((lo + (lo >> 5)) & 15)].push_back(r);
+      }
+      std::vector<size_t> head(16, 0);
+      std::vector<int32_t> balanced;
+      balanced.reserve(order.size());
+      int64_t left = s;
+      while (left > 0) {
+        int took = 0;
+        for (int c = 0; c < 16 && took < 16 && left > 0; ++c)
+          if (head[static_cast<size_t>(c)] < cls[static_cast<size_t>(c)].size()) {
+            balanced.push_back(cls[static_cast<size_t>(c)][head[static_cast<size_t>(c)]++]);
+            ++took;
+            --left;
+          }
+        for (int c = 0; c < 16 && took < 16 && left > 0; ++c)  // pad the half-warp with leftovers
+          while (took < 16 && left > 0 && head[static_cast<size_t>(c)] < cls[static_cast<size_t>(c)].size()) {
+            balanced.push_back(cls[static_cast<size_t>(c)][head[static_cast<size_t>(c)]++]);
+            ++took;
+            --left;
+          }
+      }
+      order.swap(balanced);
+    }
     op->srht_slot.resize(static_cast<size_t>(s));
     op->srht_row.resize(static_cast<size_t>(s));
     for (int64_t t = 0; t < s; ++t) {

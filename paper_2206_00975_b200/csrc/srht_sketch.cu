@@ -60,7 +60,6 @@ int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out) {
 namespace {
 
 constexpr int WARPS_PER_CTA = 4;
-constexpr int PADDED = 1024 + 32;  // one pad double per 32: conflict-free transpose
 
 struct SrhtParams {
   const double* A;
@@ -82,26 +81,39 @@ __device__ __forceinline__ void bfly(double& a, double& b) {
   b = x - y;
 }
 
-template <int NQ>
-__global__ void __launch_bounds__(WARPS_PER_CTA * 32, 3) srht_kernel(SrhtParams p) {
-  __shared__ double zbuf[WARPS_PER_CTA][PADDED];
+// LB = log2 of the per-warp block (10: 1024 rows, 32 values per lane;
+// 11: 2048 rows, 64 values per lane, which halves the gather work per element
+// at the price of occupancy).
+template <int NQ, int LB>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_kernel(SrhtParams p) {
+  constexpr int L = 1 << LB, T = L / 32, PAD = L + L / 32;
+  extern __shared__ double zbuf[];  // [WARPS_PER_CTA][PAD]
   __shared__ uint32_t sslot[NQ * 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x)
-    sslot[t] = t < p.nslots ? p.slot[t] : 0u;
+  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x) sslot[t] = t < p.nslots ? p.slot[t] : 0u;
   __syncthreads();
 
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * WARPS_PER_CTA + wib;
   int64_t it = warp * p.per;
   int64_t end = it + p.per;
   if (end > p.total) end = p.total;
-  double* z = zbuf[wib];
+  double* z = zbuf + wib * PAD;
 
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
   int seg = 0;
   int64_t cur_col = it < end ? it / p.nb : -1;
+  // Lane holds rows lane + 32 t (coalesced 256 B per load), streamed once.  The
+  // next block is issued into the same registers as soon as the current one has
+  // been written to shared memory, so its loads overlap the gather phase.
+  double x[T];
+  if (it < end) {
+    const int64_t col = it / p.nb, blk = it - col * p.nb;
+    const double* a = p.A + col * p.lda + blk * L + lane;
+#pragma unroll
+    for (int t = 0; t < T; ++t) x[t] = __ldcs(a + 32 * t);
+  }
 
   for (; it < end; ++it) {
     const int64_t col = it / p.nb, blk = it - col * p.nb;
@@ -115,46 +127,59 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 3) srht_kernel(SrhtParams 
       seg = 1;
       cur_col = col;
     }
-    const double* a = p.A + col * p.lda + blk * 1024 + lane;
-    double x[32];
+    const int64_t jhi = p.jhi0 + blk;  // global L-row block index
+    // D: flip the sign where the stream bit is 0 (rng.hpp:57); masks are per 1024 rows.
 #pragma unroll
-    for (int t = 0; t < 32; ++t) x[t] = __ldcs(a + 32 * t);  // streamed once: evict-first
-    const int64_t jhi = p.jhi0 + blk;
-    const uint32_t sm = __ldg(p.mask + jhi * 32 + lane);
-    // D: flip the sign where the stream bit is 0 (rng.hpp:57).
+    for (int h = 0; h < T / 32; ++h) {
+      const uint32_t sm = __ldg(p.mask + (jhi * (T / 32) + h) * 32 + lane);
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const uint32_t flip = ((~sm) >> t) & 1u;
-      x[t] = __hiloint2double(__double2hiint(x[t]) ^ static_cast<int>(flip << 31), __double2loint(x[t]));
+      for (int t = 0; t < 32; ++t) {
+        const uint32_t flip = ((~sm) >> t) & 1u;
+        double& v = x[h * 32 + t];
+        v = __hiloint2double(__double2hiint(v) ^ static_cast<int>(flip << 31), __double2loint(v));
+      }
     }
-    // Stages on row bits 5..9 (register index t).
+    // Stages on row bits 5 .. LB-1 (register index t).
 #pragma unroll
-    for (int h = 1; h < 32; h <<= 1)
+    for (int h = 1; h < T; h <<= 1)
 #pragma unroll
-      for (int t = 0; t < 32; ++t)
+      for (int t = 0; t < T; ++t)
         if ((t & h) == 0) bfly(x[t], x[t + h]);
     // Transpose through shared memory: row j at j + j/32.
 #pragma unroll
-    for (int t = 0; t < 32; ++t) z[lane + 33 * t] = x[t];
+    for (int t = 0; t < T; ++t) z[lane + 33 * t] = x[t];
+    __syncwarp();
+    // Lane now holds rows u + 32 lane + 1024 w (u < 32, w < T/32) in x[w*32 + u].
+#pragma unroll
+    for (int w = 0; w < T / 32; ++w)
+#pragma unroll
+      for (int u = 0; u < 32; ++u) x[w * 32 + u] = z[u + 33 * lane + 1056 * w];
+    // Stages on row bits 0..4.
+#pragma unroll
+    for (int w = 0; w < T / 32; ++w)
+#pragma unroll
+      for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+          if ((u & h) == 0) bfly(x[w * 32 + u], x[w * 32 + u + h]);
     __syncwarp();
 #pragma unroll
-    for (int u = 0; u < 32; ++u) x[u] = z[33 * lane + u];
-    // Stages on row bits 0..4 (register index u); lane now holds rows 32*lane + u.
+    for (int w = 0; w < T / 32; ++w)
 #pragma unroll
-    for (int h = 1; h < 32; h <<= 1)
+      for (int u = 0; u < 32; ++u) z[u + 33 * lane + 1056 * w] = x[w * 32 + u];
+    if (it + 1 < end) {  // prefetch the next block into the now free registers
+      const int64_t c2 = (it + 1) / p.nb, b2 = (it + 1) - c2 * p.nb;
+      const double* a2 = p.A + c2 * p.lda + b2 * L + lane;
 #pragma unroll
-      for (int u = 0; u < 32; ++u)
-        if ((u & h) == 0) bfly(x[u], x[u + h]);
+      for (int t = 0; t < T; ++t) x[t] = __ldcs(a2 + 32 * t);
+    }
     __syncwarp();
-#pragma unroll
-    for (int u = 0; u < 32; ++u) z[33 * lane + u] = x[u];
-    __syncwarp();
-    // Sampled second stage.
+    // Sampled second stage: acc += (-1)^popc(r_hi & j_hi) Z[r_lo].
     const uint32_t jh = static_cast<uint32_t>(jhi);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const uint32_t v = sslot[q * 32 + lane];
-      const uint32_t rlo = v & 1023u, rhi = v >> 10;
+      const uint32_t rlo = v & (L - 1), rhi = v >> LB;
       const double zz = z[rlo + (rlo >> 5)];
       acc[q] += (__popc(rhi & jh) & 1) ? -zz : zz;
     }
@@ -207,15 +232,23 @@ __global__ void srht_direct(const double* __restrict__ A, int64_t lda, int64_t m
   }
 }
 
-template <int NQ>
-int launch_srht(SrhtParams p, int64_t warps, cudaStream_t st) {
+template <int NQ, int LB>
+int launch_srht_lb(SrhtParams p, int64_t warps, cudaStream_t st) {
   const int64_t ctas = (warps + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  const size_t smem = sizeof(double) * WARPS_PER_CTA * ((1 << LB) + (1 << LB) / 32);
+  auto kern = srht_kernel<NQ, LB>;
+  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   KernelTimer tm(st);
-  srht_kernel<NQ><<<static_cast<unsigned>(ctas), WARPS_PER_CTA * 32, 0, st>>>(p);
+  kern<<<static_cast<unsigned>(ctas), WARPS_PER_CTA * 32, smem, st>>>(p);
   tm.stop();
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
   return OK;
+}
+
+template <int NQ>
+int launch_srht(SrhtParams p, int64_t warps, int lb, cudaStream_t st) {
+  return lb == 11 ? launch_srht_lb<NQ, 11>(p, warps, st) : launch_srht_lb<NQ, 10>(p, warps, st);
 }
 
 }  // namespace
@@ -228,7 +261,12 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
   const DeviceTables* tb = op.tables();
   if (!tb) return ECUDA;
   if (rows.rstep != 1) return fail(EINVAL_, "srht shard: rows must be contiguous (rstep 1)");
-  const bool blocked = op.m >= 1024 && mloc >= 1024 && (mloc % 1024) == 0 && (rows.row0 % 1024) == 0 &&
+  // Per-warp block of 2^lb rows: 2048 when the shard allows (NSK_SRHT_LB=10 forces 1024).
+  const char* lbenv = std::getenv("NSK_SRHT_LB");
+  int lb = (lbenv && lbenv[0] == '1' && lbenv[1] == '0') ? 10 : 11;
+  if (!(op.m >= 2048 && mloc % 2048 == 0 && rows.row0 % 2048 == 0)) lb = 10;
+  const int64_t L = int64_t(1) << lb;
+  const bool blocked = op.m >= L && mloc >= L && (mloc % L) == 0 && (rows.row0 % L) == 0 &&
                        tb->sign_mask != nullptr;
   if (!blocked) {
     int64_t blocks = (s * n + 127) / 128;
@@ -239,9 +277,9 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
     NSK_CUDA_OK(cudaGetLastError());
     return OK;
   }
-  const int64_t nb = mloc / 1024;
+  const int64_t nb = mloc / L;
   const int64_t total = n * nb;
-  const int64_t max_warps = static_cast<int64_t>(sm_count()) * 3 * WARPS_PER_CTA;
+  const int64_t max_warps = static_cast<int64_t>(sm_count()) * (lb == 10 ? 3 : 2) * WARPS_PER_CTA;
   int64_t warps = total < max_warps ? total : max_warps;
   int64_t per = (total + warps - 1) / warps;
   if (per > nb) per = nb;  // a warp touches at most two columns
@@ -253,10 +291,10 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
     const int NQ = nq <= 8 ? 8 : (nq <= 16 ? 16 : 32);
     Scratch part;
     NSK_CUDA_OK(part.alloc(sizeof(double) * warps * 2 * NQ * 32, st));
-    SrhtParams p{A, lda, n, nb, rows.row0 / 1024, total, per, tb->sign_mask, tb->srht_slot + base, ns,
+    SrhtParams p{A, lda, n, nb, rows.row0 / L, total, per, tb->sign_mask, tb->srht_slot + base, ns,
                  part.as<double>()};
-    int rc = NQ == 8 ? launch_srht<8>(p, warps, st) : (NQ == 16 ? launch_srht<16>(p, warps, st)
-                                                                : launch_srht<32>(p, warps, st));
+    int rc = NQ == 8 ? launch_srht<8>(p, warps, lb, st)
+                     : (NQ == 16 ? launch_srht<16>(p, warps, lb, st) : launch_srht<32>(p, warps, lb, st));
     if (rc != OK) return rc;
     int64_t blocks = (n * ns + 255) / 256;
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();

@@ -31,7 +31,7 @@ class RowShard:
 
 
 def _align_for(kind: str) -> int:
-    return {"srht": 1024, "countsketch": 512}.get(kind, 1)
+    return {"srht": 2048, "countsketch": 512}.get(kind, 1)
 
 
 def row_partition(m: int, world: int, kind: str) -> List[RowShard]:
