@@ -29,15 +29,20 @@ constexpr int CONSUMERS = 256;  // 8 MMA warps
 constexpr int PRODUCERS = 128;  // 4 generator / loader warps
 constexpr int THREADS = CONSUMERS + PRODUCERS;
 
+// Shared-memory tiles use a "k4-interleaved" layout: element (row x, k) of a
+// tile with X rows sits at (k / 4) * (4 X) + 4 x + (k % 4).  An m8n8k4
+// fragment load (x = lane / 4, k = lane % 4) then covers 32 consecutive
+// doubles -- conflict-free without padding -- and a 16-byte cp.async of two
+// consecutive A rows of one column stays contiguous.
 template <int BN>
 struct Tile {
   static constexpr int BM = 16384 / BN;                                // 128, 64, 32
-  static constexpr int BK = BN == 512 ? 8 : (BN == 256 ? 16 : 32);     // A rows per stage
-  static constexpr int LD = BK + 4;  // LD mod 16 in {4, 12}: conflict-free fragment loads
-  static constexpr int WGM = BM / 32, WGN = BN / 64;                   // consumer warp grid
-  static constexpr int STAGE = (BM + BN) * LD;                         // doubles per stage
-  static constexpr int STAGES = BN == 128 ? 3 : 4;                     // ring depth (<= 216 KiB)
+  static constexpr int BK = BN == 128 ? 32 : 16;                       // A rows per stage
+  static constexpr int STAGE = (BM + BN) * BK;                         // doubles per stage
+  static constexpr int STAGES = BN == 512 ? 3 : (BN == 256 ? 4 : 3);   // ring depth (<= 216 KiB)
+  static constexpr int WGM = BM / 32;                                  // consumer warp grid rows
 };
+__device__ __forceinline__ int k4(int x, int k, int X) { return (k >> 2) * (4 * X) + 4 * x + (k & 3); }
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -94,7 +99,7 @@ __device__ __forceinline__ void load_a_tile(const GaussParams& p, double* sb, in
         bytes = (row + 1 < p.mloc) ? 16 : 8;
         src = p.A + row + q * p.lda;
       }
-      cp_async16(sb + col * T::LD + r2, src, bytes);
+      cp_async16(sb + k4(col, r2, BN), src, bytes);
     }
   } else {
     constexpr int ELEMS = BN * T::BK;
@@ -108,7 +113,7 @@ __device__ __forceinline__ void load_a_tile(const GaussParams& p, double* sb, in
         bytes = 8;
         src = NCOMP == 1 ? p.A + row + q * p.lda : p.A + 2 * (row + (q >> 1) * p.lda) + (q & 1);
       }
-      cp_async8(sb + col * T::LD + r, src, bytes);
+      cp_async8(sb + k4(col, r, BN), src, bytes);
     }
   }
 }
@@ -134,8 +139,8 @@ __device__ __forceinline__ void gen_g_tile(const GaussParams& p, double* sa, int
         if (i + 1 < p.s) g1 = gaussian_at(p.key, L + 1);
       }
     }
-    sa[ii * T::LD + k] = g0;
-    sa[(ii + 1) * T::LD + k] = g1;
+    sa[k4(ii, k, T::BM)] = g0;
+    sa[k4(ii + 1, k, T::BM)] = g1;
   }
 }
 
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         const int st = static_cast<int>(c % T::STAGES);
         if (c >= T::STAGES) named_sync(1 + T::STAGES + st, THREADS);  // consumers released stage
         double* sa = smem + st * T::STAGE;
-        double* sb = sa + T::BM * T::LD;
+        double* sb = sa + T::BM * T::BK;
         const int64_t k0 = kbeg + c * T::BK;
         load_a_tile<BN, NCOMP, VEC16>(p, sb, k0, q0, pt);
         cp_async_commit();
@@ -194,18 +199,19 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
   for (int64_t c = 0; c < nchunks; ++c) {
     const int st = static_cast<int>(c % T::STAGES);
     named_sync(1 + st, THREADS);  // wait: stage full
-    const double* A_ = smem + st * T::STAGE + (wm * 32 + (lane >> 2)) * T::LD + (lane & 3);
-    const double* B_ = smem + st * T::STAGE + T::BM * T::LD + (wn * 64 + (lane >> 2)) * T::LD + (lane & 3);
+    // k4 layout: fragment (x = lane/4, k = lane%4) of k-step kk at (kk/4)*4X + 4x + k.
+    const double* A_ = smem + st * T::STAGE + 4 * (wm * 32) + lane;
+    const double* B_ = smem + st * T::STAGE + T::BM * T::BK + 4 * (wn * 64) + lane;
 #pragma unroll
     for (int kk = 0; kk < T::BK; kk += 4) {
       double af[TM];
 #pragma unroll
-      for (int a = 0; a < TM; ++a) af[a] = A_[a * 8 * T::LD + kk];
+      for (int a = 0; a < TM; ++a) af[a] = A_[kk * T::BM + a * 32];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         double bf[TN / 2];
 #pragma unroll
-        for (int b = 0; b < TN / 2; ++b) bf[b] = B_[(h * (TN / 2) + b) * 8 * T::LD + kk];
+        for (int b = 0; b < TN / 2; ++b) bf[b] = B_[kk * BN + (h * (TN / 2) + b) * 32];
 #pragma unroll
         for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -284,7 +290,11 @@ int gaussian_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n,
     return OK;
   }
   // Widest n-tile that the problem fills (each G entry is regenerated once per n-tile).
-  const int BN = nq <= 128 ? 128 : (nq <= 256 ? 256 : 512);
+  int BN = nq <= 128 ? 128 : (nq <= 256 ? 256 : 512);
+  if (const char* e = std::getenv("NSK_GAUSS_BN")) {  // A/B override: 128, 256 or 512
+    const int v = std::atoi(e);
+    if (v == 128 || v == 256 || v == 512) BN = v;
+  }
   const int BM = 16384 / BN, BK = BN == 512 ? 8 : (BN == 256 ? 16 : 32);
   const int64_t q_tiles = (nq + BN - 1) / BN;
   const int64_t s_tiles = (s + BM - 1) / BM;
