@@ -75,7 +75,9 @@ enum nsk_status {
   NSK_ERANGE = 2,
   NSK_ENOCONV = 3,
   NSK_ECUDA = 4,
-  NSK_ENOMEM = 5
+  NSK_ENOMEM = 5,
+  NSK_ETLS_EXISTENCE = 6, /* TlsExistenceError (tls.hpp:37-48) */
+  NSK_ETLS_CONDITION = 7  /* TlsConditionError (tls.hpp:50-57) */
 };
 
 /* Thread-local message describing the last non-OK status. */
@@ -162,6 +164,49 @@ int nsk_solve_tol_host(const nsk_operator* op, int scalar, int64_t m, int64_t n,
 
 int nsk_residual_fro_host(int scalar, int64_t m, int64_t n, const void* A, int64_t lda, int64_t k,
                           const void* W, int64_t ldw, double* out);
+
+/* ---- incremental maintenance (sketch.hpp:90-109, sketch.cpp:234-301) ---- */
+
+/* Operator state: m_effective = m + appended rows, the sorted zeroed rows
+ * (up to cap of them into zeroed_rows when non-null). */
+int nsk_op_state(const nsk_operator* op, int64_t* m_eff, int64_t* appended, int64_t* nzeroed,
+                 int64_t* zeroed_rows, int64_t cap);
+
+/* update_row: append row a_row (1 x n, device) to the underlying matrix.  Draws
+ * the next Gaussian column g of stream (seed, 1) and adds g a_row / sqrt(s) to
+ * SA (s x n, device) in place; m_effective grows by one.  srdct rejects a
+ * complex row; a complex row needs a complex SA (promote it first). */
+int nsk_update_row(nsk_operator* op, int scalar_sa, int64_t n, int scalar_row, const void* a_row, void* SA,
+                   int64_t ldsa, void* stream);
+
+/* downdate_row: remove row j whose current content is a_row (1 x n, device):
+ * SA -= (S e_j) a_row, then row j is recorded as zeroed.  NSK_ERANGE for j
+ * outside [0, m_effective), NSK_EINVAL if j was already removed; warns on
+ * stderr when fewer than 2s live rows remain (sketch.cpp:296-299). */
+int nsk_downdate_row(nsk_operator* op, int64_t j, int scalar_sa, int64_t n, int scalar_row, const void* a_row,
+                     void* SA, int64_t ldsa, void* stream);
+
+/* update_column: out (s x 1, device) = S a_col with a_col's entries at zeroed
+ * rows forced to zero (sketch.cpp:244-252); the caller splices it into SA
+ * (downdate_column is a pure splice and needs no call). */
+int nsk_update_column(const nsk_operator* op, int scalar, int64_t m, const void* a_col, void* out,
+                      void* stream);
+
+/* ---- sketched total least squares (tls.hpp:59-65, tls.cpp:97-113) ------- */
+
+/* X (n x k) = -V_k1 V_k2^{-1} from the trailing k right singular vectors Vk
+ * ((n+k) x k) of S [A | B]; sigma receives the n+k sketched singular values;
+ * info[4] = {tls_residual, cond(V_k2), sigma_n(S A), sigma_{n+1}(S [A|B])}.
+ * NSK_ETLS_EXISTENCE when sigma_n(S A) <= sigma_{n+1} and !allow_marginal,
+ * NSK_ETLS_CONDITION when cond(V_k2) > cond_limit.  Device pointers. */
+int nsk_tls_solve_sketched(const nsk_operator* op, int scalar, int64_t m, int64_t n, int64_t k,
+                           const void* A, int64_t lda, const void* B, int64_t ldb, double cond_limit,
+                           int allow_marginal, void* X, int64_t ldx, void* Vk, int64_t ldv, double* sigma,
+                           double* info, void* stream);
+int nsk_tls_solve_sketched_host(const nsk_operator* op, int scalar, int64_t m, int64_t n, int64_t k,
+                                const void* A, int64_t lda, const void* B, int64_t ldb, double cond_limit,
+                                int allow_marginal, void* X, int64_t ldx, void* Vk, int64_t ldv,
+                                double* sigma, double* info);
 
 /* ---- instrumentation (bench.py; no effect on results) ------------------- */
 

@@ -354,3 +354,131 @@ def random_complex(m, n, seed):
     """Test fixture of the reference (tests/test_support.hpp:26-33): stream 78, (re, im) pairs."""
     g = gaussians(seed, 78, 0, 2 * m * n).reshape(n, m, 2)
     return np.asfortranarray((g[..., 0] + 1j * g[..., 1]).T)
+
+
+# ----------------------------------------------------------------------------- incremental state
+# sketch.cpp:130-160 (sketch_vector), 174-182 (zero_row), 234-301 (updates).  The
+# oracle operator grows the same state the device operator keeps: appended
+# Gaussian columns (stream (seed, 1)) and the sorted zeroed rows.
+
+def _m_eff(op):
+    return op.m + getattr(op, "appended", 0)
+
+
+def _zeroed(op):
+    if not hasattr(op, "zeroed"):
+        op.zeroed = []
+    return op.zeroed
+
+
+def sketch_vector(op, j):
+    """Column j of S, scaling included (sketch.cpp:130-160); zeroed gaussian/appended columns are 0."""
+    s, m = op.s, op.m
+    inv = 1.0 / math.sqrt(s)
+    if j >= m:
+        if j in _zeroed(op):
+            return np.zeros(s)
+        return inv * gaussians(op.seed, 1, (j - m) * s, s)
+    if op.kind == "gaussian":
+        if j in _zeroed(op):
+            return np.zeros(s)
+        return inv * gaussian_block(op.seed, s, j, j + 1, nthreads=1)[:, 0]
+    if op.kind == "countsketch":
+        e = np.zeros(s)
+        e[op.bucket[j]] = op.signs[j]
+        return e
+    d = op.signs[j]
+    a = op.idx.astype(object)
+    if op.kind == "srft":  # transforms.cpp:66-72, argument reduced mod m
+        r = np.array([(int(x) * j) % m for x in a], dtype=np.float64)
+        return inv * d * np.exp(2j * np.pi * r / m)
+    if op.kind == "srdct":  # transforms.cpp:74-80 with exact reduction of j (2a+1) mod 4m
+        r = np.array([(j * (2 * int(x) + 1)) % (4 * m) for x in a], dtype=np.float64)
+        cj = math.sqrt(1.0 / m) if j == 0 else math.sqrt(2.0 / m)
+        return math.sqrt(m / s) * d * cj * np.cos(np.pi * r / (2 * m))
+    par = np.array([bin(int(x) & j).count("1") & 1 for x in a])
+    return inv * d * np.where(par == 1, -1.0, 1.0)  # srht
+
+
+def dense_state(op):
+    """s x m_effective matrix currently applied (SketchOperator::dense, sketch.cpp:162-172)."""
+    cols = [sketch_vector(op, j) for j in range(_m_eff(op))]
+    return np.stack(cols, axis=1)
+
+
+def apply_state(op, A):
+    """apply() with appended rows and zeroed rows (sketch.cpp:184-232)."""
+    A = np.asarray(A)
+    if A.ndim == 1:
+        A = A[:, None]
+    if A.shape[0] != _m_eff(op):
+        raise ValueError("sketch apply: row count mismatch")
+    top = A[:op.m].copy()
+    if op.kind == "gaussian":  # zeroed columns of G
+        for z in _zeroed(op):
+            if z < op.m:
+                top[z] = 0
+    SA = apply(op, top)
+    p = _m_eff(op) - op.m
+    if p:
+        G = np.stack([gaussians(op.seed, 1, c * op.s, op.s) for c in range(p)], axis=1)
+        for z in _zeroed(op):
+            if z >= op.m:
+                G[:, z - op.m] = 0
+        bottom = (G @ A[op.m:]) / math.sqrt(op.s)
+        SA = SA + bottom
+    return SA
+
+
+def update_row(op, SA, a_row):
+    """SA + g a_row / sqrt(s), g = next Gaussian column of stream (seed, 1) (sketch.cpp:268-280)."""
+    p = _m_eff(op) - op.m
+    g = gaussians(op.seed, 1, p * op.s, op.s)
+    op.appended = getattr(op, "appended", 0) + 1
+    return SA + np.outer(g, np.ravel(a_row)) / math.sqrt(op.s)
+
+
+def downdate_row(op, SA, j, a_row):
+    """SA - (S e_j) a_row, then zero row j (sketch.cpp:283-301)."""
+    if j < 0 or j >= _m_eff(op):
+        raise IndexError("downdate_row: row index out of range")
+    if j in _zeroed(op):
+        raise ValueError("downdate_row: row already removed")
+    e = sketch_vector(op, j)
+    out = SA - np.outer(e, np.ravel(a_row))
+    z = _zeroed(op)
+    z.append(j)
+    z.sort()
+    return out
+
+
+def update_column(op, SA, a_col, position):
+    """Insert the sketch of a_col with zeroed rows forced to 0 (sketch.cpp:234-257)."""
+    col = np.array(a_col, dtype=np.result_type(a_col, np.float64)).reshape(-1, 1)
+    for z in _zeroed(op):
+        col[z] = 0
+    sk = apply_state(op, col)
+    return np.concatenate([SA[:, :position], sk, SA[:, position:]], axis=1)
+
+
+def tls_solve_sketched(A, B, op, cond_limit=1e12, allow_marginal=False):
+    """Sketched TLS (tls.cpp:97-113, extract_x 26-43, assemble 45-60); returns (X, Vk, sigma, residual, cond)."""
+    A = np.asarray(A)
+    B = np.asarray(B).reshape(A.shape[0], -1)
+    m, n = A.shape
+    k = B.shape[1]
+    if k < 1 or n < k or m < n + k:
+        raise ValueError("tls: bad shape")
+    sk = apply_state(op, np.concatenate([A, B], axis=1))
+    _, sv, v = svd(sk)
+    sa = np.linalg.svd(sk[:, :n], compute_uv=False)
+    if not (sa[n - 1] > sv[n]) and not allow_marginal:
+        raise RuntimeError("tls: solution existence check failed")
+    vk = v[:, n:n + k]
+    v1, v2 = vk[:n], vk[n:]
+    s2 = np.linalg.svd(v2, compute_uv=False)
+    cond = np.inf if s2[-1] == 0 else s2[0] / s2[-1]
+    if not (cond <= cond_limit):
+        raise RuntimeError("tls: V_k2 ill conditioned")
+    X = np.linalg.solve(v2.T, -v1.T).T
+    return X, vk, sv, math.sqrt(np.sum(sv[n:] ** 2)), cond

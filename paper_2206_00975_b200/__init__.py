@@ -5,8 +5,12 @@ Public API mirrors the reference's sketch / nullspace modules
 compute runs in libnullsketch_b200.so (hand-written sm_100a CUDA) through the
 C ABI declared in include/nullsketch_b200.h.
 """
-from .sketch import (KINDS, NullspaceResult, SketchedMatrix, SketchOperator, SvdConvergenceError, apply,
-                     apply_shard, default_sketch_size, residual_certificate, solve_k, solve_tol, svd_trailing)
+from .sketch import (KINDS, NullspaceResult, SketchedMatrix, SketchOperator, SvdConvergenceError, TlsConditionError,
+                     TlsExistenceError, TlsSolution, apply, apply_shard, default_sketch_size, downdate_column,
+                     downdate_row, residual_certificate, solve_k, solve_tol, svd_trailing, tls_solve_sketched,
+                     update_column, update_row)
 
-__all__ = ["KINDS", "NullspaceResult", "SketchedMatrix", "SketchOperator", "SvdConvergenceError", "apply",
-           "apply_shard", "default_sketch_size", "residual_certificate", "solve_k", "solve_tol", "svd_trailing"]
+__all__ = ["KINDS", "NullspaceResult", "SketchedMatrix", "SketchOperator", "SvdConvergenceError", "TlsConditionError",
+           "TlsExistenceError", "TlsSolution", "apply", "apply_shard", "default_sketch_size", "downdate_column",
+           "downdate_row", "residual_certificate", "solve_k", "solve_tol", "svd_trailing", "tls_solve_sketched",
+           "update_column", "update_row"]

@@ -14,7 +14,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libnullsketch_b200.so")
 
-NSK_OK, NSK_EINVAL, NSK_ERANGE, NSK_ENOCONV, NSK_ECUDA, NSK_ENOMEM = range(6)
+NSK_OK, NSK_EINVAL, NSK_ERANGE, NSK_ENOCONV, NSK_ECUDA, NSK_ENOMEM, NSK_ETLS_EXISTENCE, NSK_ETLS_CONDITION = range(8)
 NSK_REAL, NSK_COMPLEX = 0, 1
 KIND_CODES = {"gaussian": 0, "srft": 1, "srdct": 2, "srht": 3, "countsketch": 4}
 KIND_NAMES = {v: k for k, v in KIND_CODES.items()}
@@ -25,12 +25,21 @@ EXPORTS = (
     "nsk_op_sample_indices", "nsk_op_descriptor", "nsk_op_from_descriptor", "nsk_apply",
     "nsk_apply_shard", "nsk_svd_trailing", "nsk_solve_k", "nsk_solve_tol", "nsk_residual_fro",
     "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_residual_fro_host", "nsk_kernel_launches",
-    "nsk_timing_enable", "nsk_timing_collect",
+    "nsk_timing_enable", "nsk_timing_collect", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
+    "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host",
 )
 
 
 class SvdConvergenceError(RuntimeError):
     """Raised when the on-device SVD does not converge (kernels.hpp:18-20)."""
+
+
+class TlsExistenceError(RuntimeError):
+    """sigma_n(A) is not above sigma_{n+1}([A|B]) (tls.hpp:37-48)."""
+
+
+class TlsConditionError(RuntimeError):
+    """V_k2 is ill conditioned (tls.hpp:50-57)."""
 
 
 _lib = None
@@ -67,6 +76,14 @@ def load():
     L.nsk_solve_k_host.argtypes = [vp, c_int, i64, i64, vp, i64, i64, vp, i64, vp]
     L.nsk_solve_tol_host.argtypes = [vp, c_int, i64, i64, vp, i64, ctypes.c_double, i64p, vp, i64, vp]
     L.nsk_residual_fro_host.argtypes = [c_int, i64, i64, vp, i64, i64, vp, i64, dp]
+    L.nsk_op_state.argtypes = [vp, i64p, i64p, i64p, i64p, i64]
+    L.nsk_update_row.argtypes = [vp, c_int, i64, c_int, vp, vp, i64, vp]
+    L.nsk_downdate_row.argtypes = [vp, i64, c_int, i64, c_int, vp, vp, i64, vp]
+    L.nsk_update_column.argtypes = [vp, c_int, i64, vp, vp, vp]
+    L.nsk_tls_solve_sketched.argtypes = [vp, c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp, i64,
+                                         vp, i64, vp, dp, vp]
+    L.nsk_tls_solve_sketched_host.argtypes = [vp, c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp,
+                                              i64, vp, i64, vp, dp]
     L.nsk_kernel_launches.restype = i64
     L.nsk_timing_enable.argtypes = [c_int]
     L.nsk_timing_enable.restype = None
@@ -89,4 +106,8 @@ def check(rc):
         raise SvdConvergenceError(msg)
     if rc == NSK_ENOMEM:
         raise MemoryError(msg)
+    if rc == NSK_ETLS_EXISTENCE:
+        raise TlsExistenceError(msg)
+    if rc == NSK_ETLS_CONDITION:
+        raise TlsConditionError(msg)
     raise RuntimeError(f"nullsketch CUDA failure: {msg}")

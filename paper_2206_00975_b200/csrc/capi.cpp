@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/nullsketch_b200.h"
@@ -43,9 +45,9 @@ int out_ncomp(const Operator& op, int in_ncomp) {
 int validate_apply(const Operator& op, int scalar, int64_t m, int64_t n, const void* A, int64_t lda,
                    const void* SA, int64_t ldsa, bool shard) {
   if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "unknown scalar kind");
-  if (!shard && m != op.m)
+  if (!shard && m != op.m_eff())
     return nsk::fail(nsk::EINVAL_, "sketch apply: matrix has " + std::to_string(m) + " rows, operator expects " +
-                                       std::to_string(op.m));
+                                       std::to_string(op.m_eff()));
   if (n < 0 || m < 0) return nsk::fail(nsk::EINVAL_, "sketch apply: negative dimension");
   if (scalar == NSK_COMPLEX && op.kind == nsk::SRDCT)
     return nsk::fail(nsk::EINVAL_, "srdct sketch is defined for real matrices only");
@@ -60,8 +62,8 @@ int validate_apply(const Operator& op, int scalar, int64_t m, int64_t n, const v
   return nsk::OK;
 }
 
-int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
-                   double* SA, int64_t ldsa, cudaStream_t st) {
+int dispatch_main(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
+                  double* SA, int64_t ldsa, cudaStream_t st) {
   switch (op.kind) {
     case nsk::GAUSSIAN: return nsk::gaussian_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
     case nsk::SRFT:
@@ -70,6 +72,28 @@ int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64
     case nsk::COUNTSKETCH: return nsk::countsketch_apply(op, rows, n, A, lda, SA, ldsa, st);
   }
   return nsk::fail(nsk::EINVAL_, "unknown sketch kind");
+}
+
+// Full apply of an operator with p appended rows (sketch.cpp:195-229): the first
+// m rows go through the kind's kernel, the appended rows through the Gaussian
+// kernel on stream (seed, 1) (appended column c = Gaussians #(c*s + i)), added in.
+int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
+                   double* SA, int64_t ldsa, cudaStream_t st) {
+  const bool full = rows.row0 == 0 && rows.rstep == 1 && rows.mloc == op.m_eff();
+  if (op.appended == 0 || !full) {
+    if (op.appended > 0) return nsk::fail(nsk::EINVAL_, "apply_shard: operators with row updates are not sharded");
+    return dispatch_main(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+  }
+  nsk::RowMap top{0, 1, op.m};
+  if (int rc = dispatch_main(op, ncomp, top, n, A, lda, SA, ldsa, st)) return rc;
+  const int nc_out = op.kind == nsk::SRFT ? 2 : ncomp;
+  nsk::Scratch t;
+  NSK_CUDA_OK(t.alloc(sizeof(double) * op.s * (n > 0 ? n : 1) * ncomp, st));
+  nsk::RowMap app{0, 1, op.appended};
+  if (int rc = nsk::gaussian_apply_key(op.key1, op.s, op.zero_mask(), op.m, ncomp, app, n, A + op.m * ncomp, lda,
+                                       t.as<double>(), op.s, st))
+    return rc;
+  return nsk::accumulate(SA, ldsa, nc_out, t.as<double>(), op.s, n, ncomp, st);
 }
 
 // Minimal JSON field readers for the descriptor (flat object, known keys).
@@ -184,18 +208,21 @@ int nsk_op_sample_indices(const nsk_operator* h, int64_t* idx_host) {
 int nsk_op_descriptor(const nsk_operator* h, char* buf, size_t cap, size_t* len) {
   if (int rc = check_op(h)) return rc;
   const Operator& op = *OP(h);
-  char tmp[256];
-  int nw = std::snprintf(tmp, sizeof tmp,
-                         "{\"appended\":0,\"format\":1,\"kind\":\"%s\",\"m\":%" PRId64 ",\"s\":%" PRId64
-                         ",\"seed\":%" PRIu64 ",\"zeroed_rows\":[]}",
-                         nsk::kind_name(op.kind), op.m, op.s, op.seed);
-  if (len) *len = static_cast<size_t>(nw);
-  if (!buf || cap < static_cast<size_t>(nw) + 1)
-    return nsk::fail(nsk::ERANGE_, "descriptor: buffer too small (" + std::to_string(nw + 1) + " bytes needed)");
-  std::memcpy(buf, tmp, static_cast<size_t>(nw) + 1);
+  std::string js = "{\"appended\":" + std::to_string(op.appended) + ",\"format\":1,\"kind\":\"" +
+                   nsk::kind_name(op.kind) + "\",\"m\":" + std::to_string(op.m) + ",\"s\":" + std::to_string(op.s) +
+                   ",\"seed\":" + std::to_string(op.seed) + ",\"zeroed_rows\":[";
+  for (size_t i = 0; i < op.zeroed.size(); ++i) js += (i ? "," : "") + std::to_string(op.zeroed[i]);
+  js += "]}";
+  if (len) *len = js.size();
+  if (!buf || cap < js.size() + 1)
+    return nsk::fail(nsk::ERANGE_, "descriptor: buffer too small (" + std::to_string(js.size() + 1) + " bytes needed)");
+  std::memcpy(buf, js.c_str(), js.size() + 1);
   return nsk::OK;
 }
 
+// SketchOperator::from_descriptor (sketch.cpp:315-337): redraw, replay the
+// appended-column count (their Gaussians are regenerated from stream (seed, 1)
+// on use) and the zeroed rows, validating each like the reference.
 int nsk_op_from_descriptor(const char* json, nsk_operator** out) {
   if (out) *out = nullptr;
   if (!json) return nsk::fail(nsk::EINVAL_, "sketch descriptor: null text");
@@ -216,22 +243,32 @@ int nsk_op_from_descriptor(const char* json, nsk_operator** out) {
   size_t p;
   if (!json_find(js, "zeroed_rows", p) || js[p] != '[')
     return nsk::fail(nsk::EINVAL_, "sketch descriptor: missing zeroed_rows");
-  size_t q = js.find(']', p);
-  std::string inner = js.substr(p + 1, q == std::string::npos ? 0 : q - p - 1);
-  bool has_rows = inner.find_first_not_of(" \t\r\n") != std::string::npos;
-  if (has_rows) {
-    // Validate like from_descriptor (sketch.cpp:330-335) before rejecting:
-    // an out-of-range row is a malformed descriptor either way.
-    long long z = std::atoll(inner.c_str());
-    if (z < 0 || static_cast<uint64_t>(z) >= m + app)
-      return nsk::fail(nsk::EINVAL_, "sketch descriptor: bad zeroed row " + std::to_string(z));
+  const size_t q = js.find(']', p);
+  if (q == std::string::npos) return nsk::fail(nsk::EINVAL_, "sketch descriptor: malformed zeroed_rows");
+  std::vector<int64_t> rows;
+  for (size_t i = p + 1; i < q;) {
+    while (i < q && (js[i] == ' ' || js[i] == ',' || js[i] == '\n' || js[i] == '\t' || js[i] == '\r')) ++i;
+    if (i >= q) break;
+    char* endp = nullptr;
+    const long long z = std::strtoll(js.c_str() + i, &endp, 10);
+    if (endp == js.c_str() + i) return nsk::fail(nsk::EINVAL_, "sketch descriptor: malformed zeroed_rows");
+    rows.push_back(z);
+    i = static_cast<size_t>(endp - js.c_str());
   }
-  if (app != 0 || has_rows)
-    return nsk::fail(nsk::EINVAL_, "sketch descriptor: row updates/downdates are not supported by this build");
   Operator* op = nullptr;
   int rc = nsk::draw_operator(k, static_cast<int64_t>(s), static_cast<int64_t>(m), seed, &op);
+  if (rc) return rc;
+  op->appended = static_cast<int64_t>(app);
+  for (long long z : rows) {
+    if (z < 0 || z >= op->m_eff() || op->is_zeroed(z)) {
+      delete op;
+      return nsk::fail(nsk::EINVAL_, "sketch descriptor: bad zeroed row " + std::to_string(z));
+    }
+    op->zeroed.insert(std::lower_bound(op->zeroed.begin(), op->zeroed.end(), static_cast<int64_t>(z)), z);
+  }
+  ++op->state_version;
   if (out) *out = reinterpret_cast<nsk_operator*>(op);
-  return rc;
+  return nsk::OK;
 }
 
 int nsk_apply(const nsk_operator* h, int scalar, int64_t m, int64_t n, const void* A, int64_t lda, void* SA,
@@ -273,7 +310,7 @@ int nsk_svd_trailing(int scalar, int64_t s, int64_t n, const void* SA, int64_t l
 
 static int solve_common(const Operator& op, int scalar, int64_t m, int64_t n, const void* A, int64_t lda,
                         nsk::Scratch& sa_buf, int& nc_out, cudaStream_t st) {
-  if (m != op.m) return nsk::fail(nsk::EINVAL_, "nullspace: matrix rows do not match the sketch operator");
+  if (m != op.m_eff()) return nsk::fail(nsk::EINVAL_, "nullspace: matrix rows do not match the sketch operator");
   if (op.s < n)
     return nsk::fail(nsk::EINVAL_, "nullspace: sketch size s = " + std::to_string(op.s) + " is smaller than n = " +
                                        std::to_string(n));
@@ -414,6 +451,181 @@ int nsk_residual_fro_host(int scalar, int64_t m, int64_t n, const void* A, int64
   if (int rc = copy_in(A, m, n, lda, nc, &dA, a, st)) return rc;
   if (int rc = copy_in(W, n, k, ldw, nc, &dW, w, st)) return rc;
   return nsk::residual_fro(nc, m, n, dA, m > 0 ? m : 1, k, dW, n > 0 ? n : 1, out, st);
+}
+
+// ---- incremental maintenance (sketch.hpp:90-109) ----------------------------
+
+int nsk_op_state(const nsk_operator* h, int64_t* m_eff, int64_t* appended, int64_t* nzeroed, int64_t* zeroed_rows,
+                 int64_t cap) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (m_eff) *m_eff = op.m_eff();
+  if (appended) *appended = op.appended;
+  if (nzeroed) *nzeroed = static_cast<int64_t>(op.zeroed.size());
+  if (zeroed_rows)
+    for (int64_t i = 0; i < cap && i < static_cast<int64_t>(op.zeroed.size()); ++i)
+      zeroed_rows[i] = op.zeroed[static_cast<size_t>(i)];
+  return nsk::OK;
+}
+
+int nsk_update_row(nsk_operator* h, int scalar_sa, int64_t n, int scalar_row, const void* a_row, void* SA,
+                   int64_t ldsa, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  Operator& op = *OP(h);
+  if (n < 0 || ldsa < op.s || (n > 0 && (!a_row || !SA))) return nsk::fail(nsk::EINVAL_, "update_row: bad arguments");
+  if (op.kind == nsk::SRDCT && scalar_row == NSK_COMPLEX)
+    return nsk::fail(nsk::EINVAL_, "update_row: srdct sketch carries real data only");
+  if (scalar_sa == NSK_REAL && scalar_row == NSK_COMPLEX)
+    return nsk::fail(nsk::EINVAL_, "update_row: a complex row needs a complex sketch (promote SA first)");
+  cudaStream_t st = ST(stream);
+  nsk::Scratch g;
+  NSK_CUDA_OK(g.alloc(sizeof(double) * op.s, st));
+  // (1/sqrt s) g, g = Gaussians #(p*s + i) of stream (seed, 1): column m + p of S.
+  if (int rc = nsk::sketch_column(op, op.m_eff(), g.as<double>(), 1, st)) return rc;
+  if (int rc = nsk::rank1_update(static_cast<double*>(SA), ldsa, scalar_sa == NSK_COMPLEX ? 2 : 1, op.s, n,
+                                 g.as<double>(), 1, static_cast<const double*>(a_row),
+                                 scalar_row == NSK_COMPLEX ? 2 : 1, 1.0, st))
+    return rc;
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  ++op.appended;
+  ++op.state_version;
+  return nsk::OK;
+}
+
+int nsk_downdate_row(nsk_operator* h, int64_t j, int scalar_sa, int64_t n, int scalar_row, const void* a_row,
+                     void* SA, int64_t ldsa, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  Operator& op = *OP(h);
+  if (j < 0 || j >= op.m_eff()) return nsk::fail(nsk::ERANGE_, "downdate_row: row index out of range");
+  if (op.is_zeroed(j))
+    return nsk::fail(nsk::EINVAL_, "downdate_row: row " + std::to_string(j) + " already removed");
+  if (n < 0 || ldsa < op.s || (n > 0 && (!a_row || !SA))) return nsk::fail(nsk::EINVAL_, "downdate_row: bad arguments");
+  const int nc_col = (op.kind == nsk::SRFT && j < op.m) ? 2 : 1;
+  if (scalar_sa == NSK_REAL && (nc_col == 2 || scalar_row == NSK_COMPLEX))
+    return nsk::fail(nsk::EINVAL_, "downdate_row: the update is complex, pass a complex sketch");
+  cudaStream_t st = ST(stream);
+  nsk::Scratch col;
+  NSK_CUDA_OK(col.alloc(sizeof(double) * op.s * nc_col, st));
+  if (int rc = nsk::sketch_column(op, j, col.as<double>(), nc_col, st)) return rc;  // S e_j before zeroing
+  if (int rc = nsk::rank1_update(static_cast<double*>(SA), ldsa, scalar_sa == NSK_COMPLEX ? 2 : 1, op.s, n,
+                                 col.as<double>(), nc_col, static_cast<const double*>(a_row),
+                                 scalar_row == NSK_COMPLEX ? 2 : 1, -1.0, st))
+    return rc;
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  op.zeroed.insert(std::lower_bound(op.zeroed.begin(), op.zeroed.end(), j), j);
+  ++op.state_version;
+  const int64_t live = op.m_eff() - static_cast<int64_t>(op.zeroed.size());
+  if (live < 2 * op.s)  // sketch.cpp:296-299
+    std::fprintf(stderr, "nullsketch: warning: sketch operator down to %lld live rows (s = %lld); quality degrades "
+                         "as rows are removed\n",
+                 static_cast<long long>(live), static_cast<long long>(op.s));
+  return nsk::OK;
+}
+
+int nsk_update_column(const nsk_operator* h, int scalar, int64_t m, const void* a_col, void* out, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (int rc = validate_apply(op, scalar, m, 1, a_col, m, out, op.s, false)) return rc;
+  cudaStream_t st = ST(stream);
+  const int nc = scalar == NSK_COMPLEX ? 2 : 1;
+  nsk::Scratch c;
+  NSK_CUDA_OK(c.alloc(sizeof(double) * (m > 0 ? m : 1) * nc, st));
+  NSK_CUDA_OK(cudaMemcpyAsync(c.p, a_col, sizeof(double) * m * nc, cudaMemcpyDeviceToDevice, st));
+  if (int rc = nsk::mask_zeroed(op, c.as<double>(), nc, st)) return rc;  // sketch.cpp:244-251
+  nsk::RowMap rows{0, 1, m};
+  return dispatch_apply(op, nc, rows, 1, c.as<double>(), m > 0 ? m : 1, static_cast<double*>(out), op.s, st);
+}
+
+// ---- sketched total least squares (tls.cpp:97-113) ------------------------
+
+int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,
+                           int64_t lda, const void* B, int64_t ldb, double cond_limit, int allow_marginal, void* X,
+                           int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info, void* stream) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (k < 1) return nsk::fail(nsk::EINVAL_, "tls: B must have at least one column");
+  if (n < k) return nsk::fail(nsk::EINVAL_, "tls: need n >= k");
+  if (m < n + k) return nsk::fail(nsk::EINVAL_, "tls: need m >= n + k");
+  if (op.m_eff() != m) return nsk::fail(nsk::EINVAL_, "tls: sketch operator row count does not match [A|B]");
+  if (op.s < n + k) return nsk::fail(nsk::EINVAL_, "tls: sketch size below n + k");
+  if (int rc = validate_apply(op, scalar, m, n, A, lda, reinterpret_cast<const void*>(1), op.s, false)) return rc;
+  if (int rc = validate_apply(op, scalar, m, k, B, ldb, reinterpret_cast<const void*>(1), op.s, false)) return rc;
+  if (!X || !Vk || !sigma || !info || ldx < n || ldv < n + k) return nsk::fail(nsk::EINVAL_, "tls: bad outputs");
+  cudaStream_t st = ST(stream);
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_ncomp(op, nc_in);
+  const int64_t nk = n + k;
+  nsk::Scratch sa, siga, v2s, v2w;
+  NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * nk * nc, st));
+  NSK_CUDA_OK(siga.alloc(sizeof(double) * n, st));
+  NSK_CUDA_OK(v2s.alloc(sizeof(double) * k, st));
+  NSK_CUDA_OK(v2w.alloc(sizeof(double) * k * k * nc, st));
+  nsk::RowMap rows{0, 1, m};
+  // S [A | B] without forming [A | B] (tls.cpp:108-109): two applies into adjacent columns.
+  if (int rc = dispatch_apply(op, nc_in, rows, n, static_cast<const double*>(A), lda, sa.as<double>(), op.s, st))
+    return rc;
+  if (int rc = dispatch_apply(op, nc_in, rows, k, static_cast<const double*>(B), ldb, sa.as<double>() + op.s * n * nc,
+                              op.s, st))
+    return rc;
+  // Trailing k right singular vectors of S[A|B] and its full spectrum; sigma_n(S A).
+  if (int rc = nsk::jacobi_trailing(nc, op.s, nk, sa.as<double>(), op.s, k, static_cast<double*>(Vk), ldv, sigma, st))
+    return rc;
+  if (int rc = nsk::jacobi_trailing(nc, op.s, n, sa.as<double>(), op.s, 0, nullptr, 1, siga.as<double>(), st))
+    return rc;
+  std::vector<double> s_aug(static_cast<size_t>(nk)), s_a(static_cast<size_t>(n));
+  NSK_CUDA_OK(cudaMemcpyAsync(s_aug.data(), sigma, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaMemcpyAsync(s_a.data(), siga.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  double tail = 0.0;
+  for (int64_t i = n; i < nk; ++i) tail += s_aug[static_cast<size_t>(i)] * s_aug[static_cast<size_t>(i)];
+  info[0] = std::sqrt(tail);                   // tls_residual
+  info[2] = s_a[static_cast<size_t>(n - 1)];   // sigma_n(S A)
+  info[3] = s_aug[static_cast<size_t>(n)];     // sigma_{n+1}(S [A|B])
+  if (!(info[2] > info[3]) && !allow_marginal)
+    return nsk::fail(NSK_ETLS_EXISTENCE, "tls: solution existence check failed: sigma_n(A) = " +
+                                             std::to_string(info[2]) + " is not above sigma_{n+1}([A|B]) = " +
+                                             std::to_string(info[3]));
+  // Condition estimate of the k x k corner V_k2 (tls.cpp:32-37), then X = -V_k1 V_k2^{-1}.
+  NSK_CUDA_OK(cudaMemcpy2DAsync(v2w.p, sizeof(double) * k * nc, static_cast<double*>(Vk) + n * nc,
+                                sizeof(double) * ldv * nc, sizeof(double) * k * nc, k, cudaMemcpyDeviceToDevice, st));
+  if (int rc = nsk::jacobi_trailing(nc, k, k, v2w.as<double>(), k, 0, nullptr, 1, v2s.as<double>(), st)) return rc;
+  std::vector<double> sv2(static_cast<size_t>(k));
+  NSK_CUDA_OK(cudaMemcpyAsync(sv2.data(), v2s.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  const double smin = sv2[static_cast<size_t>(k - 1)];
+  info[1] = smin == 0.0 ? HUGE_VAL : sv2[0] / smin;
+  if (!(info[1] <= cond_limit))
+    return nsk::fail(NSK_ETLS_CONDITION, "tls: V_k2 is ill conditioned (cond estimate " + std::to_string(info[1]) +
+                                             "); X = -V_k1 V_k2^{-1} is unreliable");
+  return nsk::tls_corner(nc, static_cast<const double*>(Vk), ldv, n, k, static_cast<double*>(X), ldx, st);
+}
+
+int nsk_tls_solve_sketched_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,
+                                int64_t lda, const void* B, int64_t ldb, double cond_limit, int allow_marginal,
+                                void* X, int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (lda < m || ldb < m || k < 1 || n < 1) return nsk::fail(nsk::EINVAL_, "tls: bad dimensions");
+  cudaStream_t st = host_stream();
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_ncomp(op, nc_in);
+  nsk::Scratch a, b, x, v, sg;
+  double *dA = nullptr, *dB = nullptr;
+  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
+  if (int rc = copy_in(B, m, k, ldb, nc_in, &dB, b, st)) return rc;
+  NSK_CUDA_OK(x.alloc(sizeof(double) * n * k * nc, st));
+  NSK_CUDA_OK(v.alloc(sizeof(double) * (n + k) * k * nc, st));
+  NSK_CUDA_OK(sg.alloc(sizeof(double) * (n + k), st));
+  const int rc = nsk_tls_solve_sketched(h, scalar, m, n, k, dA, m, dB, m, cond_limit, allow_marginal, x.p, n, v.p,
+                                        n + k, sg.as<double>(), info, st);
+  if (rc != NSK_OK && rc != NSK_ETLS_CONDITION) return rc;
+  if (rc == NSK_OK && X) {
+    if (int r2 = copy_out(X, ldx, x.as<double>(), n, k, nc, st)) return r2;
+  }
+  if (Vk) {
+    if (int r2 = copy_out(Vk, ldv, v.as<double>(), n + k, k, nc, st)) return r2;
+  }
+  if (sigma) NSK_CUDA_OK(cudaMemcpyAsync(sigma, sg.p, sizeof(double) * (n + k), cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return rc;
 }
 
 }  // extern "C"

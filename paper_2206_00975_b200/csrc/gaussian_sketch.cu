@@ -81,6 +81,8 @@ struct GaussParams {
   double* P;        // partials [split][nq][s]
   int64_t chunks_per_split;
   PhiloxKey key;
+  const uint32_t* zmask;  // zeroed rows (bit zoff + global row), or nullptr
+  int64_t zoff;
 };
 
 // Producer: A rows [k0, k0 + BK) x logical columns [q0, q0 + BN) -> sb[col][row].
@@ -128,7 +130,12 @@ __device__ __forceinline__ void gen_g_tile(const GaussParams& p, double* sa, int
     const int k = t % T::BK, ii = (t / T::BK) * 2;
     const int64_t i = i0 + ii, row = k0 + k;
     double g0 = 0.0, g1 = 0.0;
-    if (row < p.mloc && i < p.s) {
+    bool live = row < p.mloc && i < p.s;
+    if (live && p.zmask) {
+      const uint64_t zb = static_cast<uint64_t>(p.zoff + p.row0 + row);
+      live = ((__ldg(p.zmask + (zb >> 5)) >> (zb & 31)) & 1u) == 0;
+    }
+    if (live) {
       const uint64_t L = static_cast<uint64_t>(p.row0 + row) * static_cast<uint64_t>(p.s) + static_cast<uint64_t>(i);
       if ((L & 1u) == 0) {
         const double2 g = gaussian_pair(p.key, L >> 1);
@@ -280,8 +287,14 @@ int launch_bn(int BN, const GaussParams& p, int64_t q_tiles, int64_t s_tiles, in
 
 int gaussian_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                    double* SA, int64_t ldsa, cudaStream_t st) {
+  return gaussian_apply_key(op.key0, op.s, op.zero_mask(), 0, ncomp, rows, n, A, lda, SA, ldsa, st);
+}
+
+int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t zoff, int ncomp, const RowMap& rows,
+                       int64_t n, const double* A, int64_t lda,
+                   double* SA, int64_t ldsa, cudaStream_t st) {
   if (rows.rstep != 1) return fail(EINVAL_, "gaussian shard: rows must be contiguous (rstep 1)");
-  const int64_t s = op.s, nq = n * ncomp, mloc = rows.mloc;
+  const int64_t nq = n * ncomp, mloc = rows.mloc;
   const double scale = 1.0 / std::sqrt(static_cast<double>(s));
   if (nq == 0) return OK;
   if (mloc == 0) {
@@ -315,7 +328,7 @@ int gaussian_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n,
 
   Scratch part;
   NSK_CUDA_OK(part.alloc(sizeof(double) * splits * nq * s, st));
-  GaussParams p{A, lda, mloc, rows.row0, s, nq, part.as<double>(), per, op.key0};
+  GaussParams p{A, lda, mloc, rows.row0, s, nq, part.as<double>(), per, key, zmask, zoff};
   const bool vec16 = ncomp == 1 && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
   int rc = ncomp == 2 ? launch_bn<2, false>(BN, p, q_tiles, s_tiles, splits, st)
          : vec16     ? launch_bn<1, true>(BN, p, q_tiles, s_tiles, splits, st)

@@ -37,6 +37,11 @@ int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out);
 int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out);
 int build_sign_bits(PhiloxKey key, int64_t m, uint32_t** out);
 
+// A shard view: local row j of A is global row row0 + rstep * j, j < mloc.
+struct RowMap {
+  int64_t row0 = 0, rstep = 1, mloc = 0;
+};
+
 // The operator is its descriptor (sketch.cpp:303-313): nothing else is stored.
 struct Operator {
   int kind = GAUSSIAN;
@@ -50,11 +55,31 @@ struct Operator {
   std::vector<uint32_t> srht_slot;
   std::vector<int32_t> srht_row;
 
+  // Incremental state (sketch.hpp:70-80): row updates append Gaussian columns
+  // drawn from stream (seed, 1) (appended column c = Gaussians #(c*s + i));
+  // row downdates record the removed rows (sorted).  Single writer.
+  int64_t appended = 0;
+  std::vector<int64_t> zeroed;
+  int64_t m_eff() const { return m + appended; }
+  bool is_zeroed(int64_t j) const;
+
   mutable std::mutex mu;
   mutable std::deque<DeviceTables> dev;  // one entry per device used (stable addresses)
   const DeviceTables* tables() const;      // uploads on first use on the current device
+  // Device bitmask of the zeroed rows (m_eff bits) on the current device, or
+  // nullptr when no row is zeroed.  Re-uploaded after every downdate.
+  const uint32_t* zero_mask() const;
+  mutable std::vector<std::pair<int, uint32_t*>> zmask_dev;  // (device, mask)
+  mutable uint64_t zmask_version = 0, state_version = 0;
   ~Operator();
 };
+
+// Gaussian sketch with an explicit stream and zero mask: SA (+)= (1/sqrt s) G A
+// with G(i, j) = Gaussian #((row0 + j) * s + i) of `key`; rows whose bit
+// (zoff + row0 + j) is set in zmask contribute nothing.
+int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t zoff, int ncomp,
+                       const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
+                       int64_t ldsa, cudaStream_t st);
 
 int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out);
 
@@ -62,10 +87,6 @@ int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out)
 std::vector<int64_t> sample_without_replacement(PhiloxKey key, int64_t m, int64_t s);
 
 // ---- kernel launchers (return Status) ------------------------------------
-// A shard view: local row j of A is global row row0 + rstep * j, j < mloc.
-struct RowMap {
-  int64_t row0 = 0, rstep = 1, mloc = 0;
-};
 
 int gaussian_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                    int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
@@ -84,6 +105,23 @@ int jacobi_trailing(int ncomp, int64_t s, int64_t n, const double* SA, int64_t l
 
 int residual_fro(int ncomp, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k,
                  const double* W, int64_t ldw, double* out_host, cudaStream_t st);
+
+// ---- incremental maintenance (sketch.cpp:234-301) --------------------------
+// out (s entries, ncomp_out) = S e_j: column j of the current operator.
+int sketch_column(const Operator& op, int64_t j, double* out, int ncomp_out, cudaStream_t st);
+// SA(:, c) -= col * row(c) (rank one; complex when either side is).
+int rank1_update(double* SA, int64_t ldsa, int ncomp_sa, int64_t s, int64_t n, const double* col, int ncomp_col,
+                 const double* row, int ncomp_row, double alpha, cudaStream_t st);
+// SA += T (T s x n dense, ncomp_t <= ncomp_sa).
+int accumulate(double* SA, int64_t ldsa, int ncomp_sa, const double* T, int64_t s, int64_t n, int ncomp_t,
+               cudaStream_t st);
+// Zero the entries of a device column (m_eff rows) at the operator's zeroed rows.
+int mask_zeroed(const Operator& op, double* col, int ncomp, cudaStream_t st);
+
+// ---- sketched total least squares (tls.cpp:97-113) -------------------------
+// X = -V1 V2^{-1} from the trailing (n+k) x k basis Vk (device, one CTA).
+int tls_corner(int ncomp, const double* Vk, int64_t ldv, int64_t n, int64_t k, double* X, int64_t ldx,
+               cudaStream_t st);
 
 // Stream-ordered scratch allocation (cudaMallocAsync from the device pool).
 struct Scratch {

@@ -212,9 +212,42 @@ const DeviceTables* Operator::tables() const {
   return &dev.back();
 }
 
+bool Operator::is_zeroed(int64_t j) const { return std::binary_search(zeroed.begin(), zeroed.end(), j); }
+
+const uint32_t* Operator::zero_mask() const {
+  if (zeroed.empty()) return nullptr;
+  int devno = 0;
+  if (cudaGetDevice(&devno) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (zmask_version != state_version) {  // operator changed: drop every device copy
+    if (!zmask_dev.empty()) cudaDeviceSynchronize();  // earlier applies may still read them
+    for (auto& d : zmask_dev) {
+      cudaSetDevice(d.first);
+      cudaFree(d.second);
+    }
+    cudaSetDevice(devno);
+    zmask_dev.clear();
+    zmask_version = state_version;
+  }
+  for (auto& d : zmask_dev)
+    if (d.first == devno) return d.second;
+  const int64_t words = (m_eff() + 31) / 32;
+  std::vector<uint32_t> bits(static_cast<size_t>(words), 0u);
+  for (int64_t j : zeroed) bits[static_cast<size_t>(j >> 5)] |= 1u << (j & 31);
+  uint32_t* d = nullptr;
+  if (cudaMalloc(&d, sizeof(uint32_t) * words) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, bits.data(), sizeof(uint32_t) * words, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  zmask_dev.emplace_back(devno, d);
+  return d;
+}
+
 Operator::~Operator() {
   int cur = 0;
   cudaGetDevice(&cur);
+  for (auto& d : zmask_dev) {
+    cudaSetDevice(d.first);
+    cudaFree(d.second);
+  }
   for (auto& t : dev) {
     cudaSetDevice(t.device);
     if (t.idx) cudaFree(t.idx);

@@ -32,11 +32,13 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from ._lib import KIND_CODES, KIND_NAMES, NSK_COMPLEX, NSK_REAL, SvdConvergenceError, check
+from ._lib import (KIND_CODES, KIND_NAMES, NSK_COMPLEX, NSK_REAL, SvdConvergenceError, TlsConditionError,
+                   TlsExistenceError, check)
 
 __all__ = ["SketchOperator", "SketchedMatrix", "NullspaceResult", "apply", "apply_shard", "solve_k",
-           "solve_tol", "residual_certificate", "svd_trailing", "default_sketch_size",
-           "SvdConvergenceError", "KINDS"]
+           "solve_tol", "residual_certificate", "svd_trailing", "default_sketch_size", "update_column",
+           "downdate_column", "update_row", "downdate_row", "tls_solve_sketched", "TlsSolution",
+           "SvdConvergenceError", "TlsExistenceError", "TlsConditionError", "KINDS"]
 
 KINDS = tuple(KIND_CODES)
 
@@ -125,9 +127,10 @@ class SketchOperator:
         return SketchOperator(h.value)
 
     def descriptor(self) -> str:
-        buf = ctypes.create_string_buffer(512)
         n = ctypes.c_size_t()
-        check(_lib.load().nsk_op_descriptor(self._h, buf, 512, ctypes.byref(n)))
+        _lib.load().nsk_op_descriptor(self._h, None, 0, ctypes.byref(n))  # size query
+        buf = ctypes.create_string_buffer(n.value + 1)
+        check(_lib.load().nsk_op_descriptor(self._h, buf, n.value + 1, ctypes.byref(n)))
         return buf.value.decode()
 
     def sample_indices(self) -> np.ndarray:
@@ -140,9 +143,20 @@ class SketchOperator:
     m = property(lambda self: self._m)
     seed = property(lambda self: self._seed)
     id = property(lambda self: self._id)
-    m_effective = property(lambda self: self._m)
-    appended_count = property(lambda self: 0)
-    zeroed_rows = property(lambda self: [])
+
+    def _state(self):
+        me, ap, nz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(_lib.load().nsk_op_state(self._h, ctypes.byref(me), ctypes.byref(ap), ctypes.byref(nz), None, 0))
+        rows = np.empty(nz.value, dtype=np.int64)
+        if nz.value:
+            check(_lib.load().nsk_op_state(self._h, None, None, None,
+                                           rows.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), nz.value))
+        return me.value, ap.value, [int(r) for r in rows]
+
+    m_effective = property(lambda self: self._state()[0])
+    appended_count = property(lambda self: self._state()[1])
+    zeroed_rows = property(lambda self: self._state()[2])
+    live_rows = property(lambda self: self._state()[0] - len(self._state()[2]))
 
     @property
     def handle(self):
@@ -305,3 +319,150 @@ def residual_certificate(A, W) -> float:
     check(L.nsk_residual_fro(scalar, A.shape[0], A.shape[1], ctypes.c_void_p(A.data_ptr()), lda, W.shape[1],
                              ctypes.c_void_p(W.data_ptr()), ldw, ctypes.byref(out), _stream_ptr()))
     return out.value
+
+
+# ----------------------------------------------------------------------------- incremental maintenance
+# sketch.hpp:90-109.  SketchedMatrix.data is a CUDA tensor; host arrays are moved to the device.
+
+def _as_device(x, like=None):
+    torch = _torch()
+    if _is_torch(x):
+        return x
+    dev = like.device if like is not None else torch.device("cuda", torch.cuda.current_device())
+    return torch.from_numpy(np.asfortranarray(x)).to(dev)
+
+
+def _require_same_operator(sa: SketchedMatrix, S: SketchOperator):
+    if sa.operator_id != S.id:  # sketch.cpp:75-79
+        raise ValueError("sketched matrix does not belong to this operator")
+
+
+def _promoted(data, cplx):
+    torch = _torch()
+    if cplx and not data.is_complex():
+        return data.to(torch.complex128).t().contiguous().t()
+    return data.clone() if data.stride(0) == 1 else data.t().contiguous().t()
+
+
+def update_column(sa: SketchedMatrix, S: SketchOperator, a_col, position: int) -> SketchedMatrix:
+    """Insert the sketch of a_col (zeroed rows forced to 0) at `position` (sketch.cpp:234-257)."""
+    torch = _torch()
+    _require_same_operator(sa, S)
+    a_col = _as_device(a_col, sa.data)
+    if a_col.dim() == 1:
+        a_col = a_col.reshape(-1, 1)
+    if a_col.shape != (S.m_effective, 1):
+        raise ValueError(f"update_column: column must be {S.m_effective} x 1")
+    n = sa.data.shape[1]
+    if position < 0 or position > n:
+        raise IndexError("update_column: position out of range")
+    scalar = _scalar_of(a_col)
+    cplx_out = _out_dtype_is_complex(S, scalar)
+    col = _empty_colmajor(S.s, 1, torch.complex128 if cplx_out else torch.float64, a_col.device)
+    a_col = a_col.contiguous()
+    check(_lib.load().nsk_update_column(S.handle, scalar, S.m_effective, ctypes.c_void_p(a_col.data_ptr()),
+                                        ctypes.c_void_p(col.data_ptr()), _stream_ptr()))
+    data = sa.data
+    if col.is_complex() and not data.is_complex():
+        data = data.to(torch.complex128)
+    elif data.is_complex() and not col.is_complex():
+        col = col.to(torch.complex128)
+    out = torch.cat([data[:, :position], col, data[:, position:]], dim=1)
+    return SketchedMatrix(out.t().contiguous().t(), sa.operator_id)
+
+
+def downdate_column(sa: SketchedMatrix, position: int) -> SketchedMatrix:
+    """Remove a column: an exact splice, no arithmetic (sketch.cpp:259-266)."""
+    torch = _torch()
+    n = sa.data.shape[1]
+    if position < 0 or position >= n:
+        raise IndexError("downdate_column: position out of range")
+    out = torch.cat([sa.data[:, :position], sa.data[:, position + 1:]], dim=1)
+    return SketchedMatrix(out.t().contiguous().t(), sa.operator_id)
+
+
+def _row_arg(S, a_row, n, like):
+    a_row = _as_device(a_row, like)
+    if a_row.dim() == 1:
+        a_row = a_row.reshape(1, -1)
+    if a_row.shape != (1, n):
+        raise ValueError(f"expected a 1 x {n} row, got {a_row.shape[0]} x {a_row.shape[1]}")
+    return a_row.contiguous().reshape(-1)
+
+
+def update_row(sa: SketchedMatrix, S: SketchOperator, a_row) -> SketchedMatrix:
+    """Append row a_row: SA + g a_row / sqrt(s), g the next Gaussian column of stream (seed, 1) (sketch.cpp:268-280)."""
+    _require_same_operator(sa, S)
+    n = sa.data.shape[1]
+    row = _row_arg(S, a_row, n, sa.data)
+    rs = _scalar_of(row)
+    if S.kind == "srdct" and rs == NSK_COMPLEX:
+        raise ValueError("update_row: srdct sketch carries real data only")
+    data = _promoted(sa.data, rs == NSK_COMPLEX)
+    check(_lib.load().nsk_update_row(S.handle, _scalar_of(data), n, rs, ctypes.c_void_p(row.data_ptr()),
+                                     ctypes.c_void_p(data.data_ptr()), data.stride(1) if n > 1 else S.s,
+                                     _stream_ptr()))
+    return SketchedMatrix(data, sa.operator_id)
+
+
+def downdate_row(sa: SketchedMatrix, S: SketchOperator, j: int, a_row_j) -> SketchedMatrix:
+    """Remove row j with content a_row_j: SA - (S e_j) a_row_j (sketch.cpp:283-301)."""
+    _require_same_operator(sa, S)
+    n = sa.data.shape[1]
+    row = _row_arg(S, a_row_j, n, sa.data)
+    rs = _scalar_of(row)
+    cplx = rs == NSK_COMPLEX or (S.kind == "srft" and j < S.m)
+    data = _promoted(sa.data, cplx)
+    check(_lib.load().nsk_downdate_row(S.handle, int(j), _scalar_of(data), n, rs, ctypes.c_void_p(row.data_ptr()),
+                                       ctypes.c_void_p(data.data_ptr()), data.stride(1) if n > 1 else S.s,
+                                       _stream_ptr()))
+    return SketchedMatrix(data, sa.operator_id)
+
+
+# ----------------------------------------------------------------------------- sketched TLS
+
+@dataclasses.dataclass
+class TlsSolution:
+    X: object                      # n x k, X = -V_k1 V_k2^{-1}
+    Vk: object                     # (n+k) x k trailing subspace of [A|B]
+    tls_residual: float            # sqrt(sum of the k trailing sigma^2)
+    cond_Vk2: float
+    augmented_singular_values: object
+    residual_certificate: Optional[float] = None
+
+
+def tls_solve_sketched(A, B, S: SketchOperator, cond_limit: float = 1e12, allow_marginal: bool = False,
+                       certificate: bool = False) -> TlsSolution:
+    """Sketched total least squares (tls.cpp:97-113): trailing subspace of S [A|B], X = -V_k1 V_k2^{-1}."""
+    torch = _torch()
+    L = _lib.load()
+    A = _as_device(A)
+    B = _as_device(B, A)
+    if B.dim() == 1:
+        B = B.reshape(-1, 1)
+    if B.shape[0] != A.shape[0]:
+        raise ValueError("tls: A and B row counts differ")
+    scalar = NSK_COMPLEX if (A.is_complex() or B.is_complex()) else NSK_REAL
+    if scalar == NSK_COMPLEX:
+        A, B = A.to(torch.complex128), B.to(torch.complex128)
+    A, lda = _colmajor(A)
+    B, ldb = _colmajor(B)
+    m, n = A.shape
+    k = B.shape[1]
+    cplx_out = _out_dtype_is_complex(S, scalar)
+    dt = torch.complex128 if cplx_out else torch.float64
+    X = _empty_colmajor(n, max(k, 1), dt, A.device)
+    Vk = _empty_colmajor(n + k, max(k, 1), dt, A.device)
+    sig = torch.empty(n + k, dtype=torch.float64, device=A.device)
+    info = np.zeros(4)
+    check(L.nsk_tls_solve_sketched(S.handle, scalar, m, n, k, ctypes.c_void_p(A.data_ptr()), lda,
+                                   ctypes.c_void_p(B.data_ptr()), ldb, float(cond_limit), int(bool(allow_marginal)),
+                                   ctypes.c_void_p(X.data_ptr()), max(n, 1), ctypes.c_void_p(Vk.data_ptr()), n + k,
+                                   ctypes.c_void_p(sig.data_ptr()), info.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                   _stream_ptr()))
+    sol = TlsSolution(X[:, :k], Vk[:, :k], float(info[0]), float(info[1]), sig)
+    if certificate:  # ||[A|B] Vk||_F = ||A V_k1 + B V_k2||_F (tls.cpp:55-58), opt-in check
+        pd = Vk.dtype
+        prod = A.to(pd) @ Vk[:n, :k] + B.to(pd) @ Vk[n:, :k]
+        sol.residual_certificate = float(torch.linalg.norm(prod).item())
+    return sol

@@ -91,7 +91,7 @@ def test_row_partition_covers_rows_once(kind, world):
         shards = row_partition(m, world, kind)
         rows = np.concatenate([np.fromiter(sh.global_rows(), dtype=np.int64, count=sh.mloc) for sh in shards])
         assert np.array_equal(np.sort(rows), np.arange(m))
-        if kind == "srht" and m >= 1024 * world:
-            assert all(sh.row0 % 1024 == 0 and sh.mloc % 1024 == 0 for sh in shards)
+        if kind == "srht" and m >= 2048 * world:
+            assert all(sh.row0 % 2048 == 0 and sh.mloc % 2048 == 0 for sh in shards)
         if kind == "countsketch" and m >= 512 * world:
             assert all(sh.row0 % 512 == 0 for sh in shards)
