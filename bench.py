@@ -346,8 +346,7 @@ def e2e_measure(nsk, S, A, k, kind, args, world, rank, mloc):
     sig = np.empty(n)
     steps = max(1, min(args.steps, args.e2e_steps))
     if world > 1:
-        # each rank sketches its shard from host memory; the solve runs on rank 0's reduced SA
-        return None
+        return e2e_sharded(nsk, S, Ah, k, kind, steps, rank, mloc)
 
     def one():
         rc = L.nsk_solve_k_host(S.handle, 0, mloc, n, ctypes.c_void_p(Ah.data_ptr()), mloc, k,
@@ -364,6 +363,43 @@ def e2e_measure(nsk, S, A, k, kind, args, world, rank, mloc):
     return {"value": mloc / dt, "unit": "rows/s", "ms": round(dt * 1e3, 3), "steps": steps,
             "api": "nsk_solve_k_host (H2D of A from pinned memory, sketch, Jacobi SVD, D2H of W and sigma)",
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
+
+
+def e2e_sharded(nsk, S, Ah, k, kind, steps, rank, mloc):
+    """N > 1: every rank copies its pinned host shard in, sketches it, the partials are
+    all-reduced, rank 0 runs the SVD and W / sigma are broadcast and copied out
+    (paper_2206_00975_b200.distributed.sharded_solve_k); device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2206_00975_b200.distributed import RowShard, sharded_solve_k
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = Ah.shape[1]
+    Ad = torch.empty((n, mloc), dtype=torch.float64, device=dev).t()
+    shard = RowShard(rank * mloc, 1, mloc)
+
+    def one():
+        Ad.copy_(Ah, non_blocking=True)
+        W, sig = sharded_solve_k(S, Ad, k, shard)
+        return W.cpu(), sig.cpu()
+
+    one()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        W, sig = one()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = t.item() / 1e3
+    world = dist.get_world_size()
+    return {"value": world * mloc / dt, "unit": "rows/s", "ms": round(dt * 1e3, 3), "steps": steps,
+            "api": "distributed.sharded_solve_k (pinned H2D of each shard, apply_shard, NCCL all-reduce, "
+                   "Jacobi SVD on rank 0, broadcast, D2H of W and sigma)",
+            "h2d_bytes_per_step": world * mloc * n * 8, "d2h_bytes_per_step": int(W.numel() * W.element_size()
+                                                                                 + sig.numel() * 8)}
 
 
 def traffic_from_profiles(kind):

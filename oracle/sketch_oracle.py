@@ -482,3 +482,24 @@ def tls_solve_sketched(A, B, op, cond_limit=1e12, allow_marginal=False):
         raise RuntimeError("tls: V_k2 ill conditioned")
     X = np.linalg.solve(v2.T, -v1.T).T
     return X, vk, sv, math.sqrt(np.sum(sv[n:] ** 2)), cond
+
+
+def doubles(seed, stream, first, count):
+    """next_double #first.. of a stream (rng.hpp:36-39): (u64 >> 11) * 2^-53, u64 = words (2i+1 : 2i)."""
+    w = words(seed, stream, 2 * first, 2 * count).astype(np.uint64).reshape(count, 2)
+    u = (w[:, 1] << np.uint64(32)) | w[:, 0]
+    return (u >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def loewner_config5(m=100000, n=150, seed=7):
+    """BASELINE configs[4]: z on the unit circle by the reference sampler protocol
+    (theta = 2 pi next_double of stream 11, bench.cpp:390-398), f(z) = 1/(1.1 - z) + e^z,
+    support = floor(j m / n), Loewner (F_i - f_j)/(Z_i - z_j) over the active rows
+    (aaa.cpp:152-177).  Returns the (m - n) x n complex matrix."""
+    theta = 2.0 * math.pi * doubles(seed, 11, 0, m)
+    z = np.cos(theta) + 1j * np.sin(theta)
+    f = 1.0 / (1.1 - z) + np.exp(z)
+    support = (np.arange(n) * m) // n
+    active = np.setdiff1d(np.arange(m), support)
+    L = (f[active, None] - f[None, support]) / (z[active, None] - z[None, support])
+    return np.asfortranarray(L)

@@ -426,3 +426,21 @@ def test_cfg2_srtt_full_size_properties(nsk, oracle, kind):
     cols = [0, 63]
     ref = oracle.apply(oracle.draw(kind, s, m, 9000005), A[:, cols].cpu().numpy())
     assert rel(sa[:, cols].cpu().numpy(), ref) <= SA_TOL
+
+
+def test_cfg5_loewner_complex_gaussian(nsk, oracle):
+    """BASELINE configs[4]: complex128 Loewner matrix (m = 99850 active rows, n = 150),
+    Gaussian sketch s = 2n on complex data, k = 1 trailing vector."""
+    L = oracle.loewner_config5()
+    m, n = L.shape
+    S = nsk.SketchOperator.draw("gaussian", 2 * n, m, 9000005)
+    res = nsk.solve_k(dev(L), 1, S)
+    Wref, sref = oracle.solve_k(L, 1, oracle.draw("gaussian", 2 * n, m, 9000005))
+    # L is numerically rank-deficient (trailing sigmas ~1e-12 ~ u ||L||): the trailing vector is
+    # not unique, so parity is on the residual (rounding level, 100 u ||L||_F) and the sigmas.
+    W = host(res.W)
+    assert abs(np.linalg.norm(W) - 1.0) < 1e-12
+    assert np.linalg.norm(L @ W) <= max(10 * np.linalg.norm(L @ Wref), 100 * U * np.linalg.norm(L))
+    assert np.max(np.abs(host(res.sketched_singular_values) - sref)) <= 1000 * U * sref[0]
+    SA = host(nsk.apply(S, dev(L)).data)
+    assert rel(SA, oracle.apply(oracle.draw("gaussian", 2 * n, m, 9000005), L)) <= SA_TOL
