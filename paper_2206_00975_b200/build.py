@@ -21,7 +21,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-warn-spills"]
 
 SOURCES = ["operator.cpp", "capi.cpp", "gaussian_sketch.cu", "srht_sketch.cu", "countsketch.cu",
-           "srtt_sketch.cu", "srtt_fast.cu", "jacobi_svd.cu", "residual.cu", "instrument.cpp", "updates.cu"]
+           "srtt_sketch.cu", "srtt_fast.cu", "jacobi_svd.cu", "residual.cu", "instrument.cpp", "updates.cu",
+           "cs_schedule.cpp"]
 
 
 def _deps():

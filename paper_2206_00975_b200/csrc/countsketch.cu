@@ -327,6 +327,154 @@ __global__ void __launch_bounds__(THREADS) countsketch_generic_kernel(CsParams p
   for (int64_t x = threadIdx.x; x < ncol * p.s; x += THREADS) P[x] = bins[x];
 }
 
+// Owner kernel (default when the schedule exists, cs_schedule.cpp): one CTA of
+// CS_THREADS threads per pair of columns and row split; thread t owns the
+// bins of the buckets b = t + j * CS_THREADS (j < BPT) of both columns in
+// registers.  Thread 0 streams each tile's two column segments (2 x 32 KiB)
+// and its schedule section into a shared-memory ring with 1-D TMA; each warp
+// then walks its iterations, in which every lane adds at most one staged row
+// (both columns) to one of its own bins, the 16 lanes of a half-warp reading
+// 16 distinct bank pairs.  No bin is shared: no shared-memory read-modify-
+// write, no barrier per tile; a stage is released through an mbarrier that
+// every warp arrives on.  Entry: row | slot << 12 | negative << 14 | valid << 15.
+struct CsOwnerParams {
+  const double* A;
+  int64_t lda;
+  int64_t n;
+  int64_t s;
+  const uint8_t* sec;
+  const uint64_t* off;
+  int64_t g0;          // global tile of local tile 0
+  int64_t ntiles;      // tiles handled by this launch
+  int64_t per;         // tiles per split
+  uint32_t sec_bytes;  // section stride in the stage (>= largest section, 128-byte multiple)
+  int stages;
+  int64_t split_base;
+  double* P;           // partials [split][n][s]
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// One schedule entry: bin j of both columns += sigma * value, as an FMA with a
+// multiplier that is sigma for the entry's slot and 0 for the other slots
+// (ptxas if-converts predicated DADDs into DADD + 2 FSEL; the multiplier costs
+// one SEL per slot for both columns).  x * 0 = +-0 leaves a bin unchanged for
+// every finite x; a non-finite entry of A reaches all bins of its owner thread.
+template <int BPT, int T>
+__device__ __forceinline__ void owner_step(uint32_t e, const unsigned char* base, double (&b0)[BPT],
+                                           double (&b1)[BPT]) {
+  const uint32_t off = (e & 0xFFFu) * 8u;
+  const double v0 = *reinterpret_cast<const double*>(base + off);
+  const double v1 = *reinterpret_cast<const double*>(base + T * 8 + off);
+  const uint32_t one_hi = 0x3FF00000u | ((e & 0x4000u) << 17);  // +-1.0, high word
+  const uint32_t sel = e & 0xB000u;
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    const uint32_t hi = sel == (0x8000u | (static_cast<uint32_t>(j) << 12)) ? one_hi : 0u;
+    const double mj = __hiloint2double(static_cast<int>(hi), 0);
+    b0[j] = fma(v0, mj, b0[j]);
+    b1[j] = fma(v1, mj, b1[j]);
+  }
+}
+
+// Blocking wait with a suspend-time hint: the warp sleeps until the phase
+// flips instead of re-issuing try_wait.
+__device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int BPT, int STG, int T>
+__global__ void __launch_bounds__(CS_THREADS, 1) countsketch_owner_kernel(CsOwnerParams p) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[STG];
+  __shared__ uint32_t done[STG];  // warps finished with the stage's current tile
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = 2 * static_cast<int64_t>(blockIdx.x), split = blockIdx.y;
+  const int ncol = p.n - c0 >= 2 ? 2 : 1;
+  const uint32_t stage_bytes = 2 * T * 8 + p.sec_bytes;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STG; ++i) {
+      mbar_init(&full[i], 1);
+      done[i] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t tbeg = split * p.per;
+  const int ntl = static_cast<int>((tbeg + p.per < p.ntiles ? tbeg + p.per : p.ntiles) - tbeg);
+  const double* Acol = p.A + c0 * p.lda + tbeg * T;
+  const uint64_t* off = p.off + p.g0 + tbeg;
+  auto issue = [&](int k, int st) {  // one thread: tile k into stage st
+    const uint64_t o0 = __ldg(off + k), o1 = __ldg(off + k + 1);
+    const uint32_t sb = static_cast<uint32_t>(o1 - o0);
+    unsigned char* base = smraw + static_cast<size_t>(st) * stage_bytes;
+    mbar_expect_tx(&full[st], ncol * T * 8 + sb);
+    tma_load_1d(base, Acol + static_cast<int64_t>(k) * T, T * 8, &full[st]);
+    if (ncol == 2) tma_load_1d(base + T * 8, Acol + p.lda + static_cast<int64_t>(k) * T, T * 8, &full[st]);
+    tma_load_1d(base + 2 * T * 8, p.sec + o0, sb, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < STG && k < ntl; ++k) issue(k, k);
+
+  double b0[BPT], b1[BPT];
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) b0[j] = b1[j] = 0.0;
+  int st = 0;
+  uint32_t ph = 0;
+  const unsigned char* base = smraw;
+  for (int k = 0; k < ntl; ++k) {
+    mbar_sleep_wait(&full[st], ph);
+    const uint16_t* hdr = reinterpret_cast<const uint16_t*>(base + 2 * T * 8);
+    const uint32_t span = *reinterpret_cast<const uint32_t*>(hdr + (w & ~1));  // hdr[w], hdr[w+1] (w even)
+    const int i0 = (w & 1) ? static_cast<int>(span >> 16) : static_cast<int>(span & 0xFFFFu);
+    const int i1 = (w & 1) ? hdr[w + 1] : static_cast<int>(span >> 16);
+    const uint16_t* ent = hdr + 64 + lane;
+    int it = i0;
+    for (; it + 1 < i1; it += 2) {  // two iterations per trip: independent shared loads in flight
+      const uint32_t e0 = ent[it * 32], e1 = ent[(it + 1) * 32];
+      owner_step<BPT, T>(e0, base, b0, b1);
+      owner_step<BPT, T>(e1, base, b0, b1);
+    }
+    if (it < i1) owner_step<BPT, T>(ent[it * 32], base, b0, b1);
+    __syncwarp();
+    if (lane == 0) {  // the last warp to finish the stage refills it
+      __threadfence_block();
+      if (atomicAdd(&done[st], 1u) == CS_WARPS - 1) {
+        done[st] = 0;
+        __threadfence_block();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        if (k + STG < ntl) issue(k + STG, st);
+      }
+    }
+    if (++st == STG) {
+      st = 0;
+      ph ^= 1u;
+      base = smraw;
+    } else {
+      base += stage_bytes;
+    }
+  }
+  double* P = p.P + ((p.split_base + split) * p.n + c0) * p.s;
+#pragma unroll
+  for (int j = 0; j < BPT; ++j) {
+    const int64_t b = static_cast<int64_t>(j) * CS_THREADS + threadIdx.x;
+    if (b < p.s) {
+      P[b] = b0[j];
+      if (ncol == 2) P[p.s + b] = b1[j];
+    }
+  }
+}
+
 __global__ void cs_reduce(const double* __restrict__ P, int64_t splits, int64_t s, int64_t n,
                           double* __restrict__ SA, int64_t ldsa) {
   const int64_t total = s * n;
@@ -394,7 +542,45 @@ bool use_tma_ring() {
   return v && std::string(v) == "tma";
 }
 
+template <int BPT, int T>
+int launch_owner(const CsOwnerParams& p0, int64_t splits, cudaStream_t st) {
+  CsOwnerParams p = p0;
+  const size_t stage = 2 * T * 8 + p.sec_bytes;
+  int dev = 0, optin = 0;
+  NSK_CUDA_OK(cudaGetDevice(&dev));
+  NSK_CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t budget = static_cast<size_t>(optin) - 2048;
+  p.stages = static_cast<int>(budget / stage);
+  if (p.stages > 4) p.stages = 4;
+  if (p.stages < 2) return fail(EINVAL_, "countsketch owner: schedule section too large");
+  const size_t smem = stage * static_cast<size_t>(p.stages);
+  auto kern = p.stages == 2 ? countsketch_owner_kernel<BPT, 2, T>
+            : p.stages == 3 ? countsketch_owner_kernel<BPT, 3, T>
+                            : countsketch_owner_kernel<BPT, 4, T>;
+  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  KernelTimer tm(st, true);
+  kern<<<dim3(static_cast<unsigned>((p.n + 1) / 2), static_cast<unsigned>(splits)), CS_THREADS, smem, st>>>(
+      p);
+  tm.stop();
+  count_launch();
+  NSK_CUDA_OK(cudaGetLastError());
+  return OK;
+}
+
 }  // namespace
+
+bool cs_owner_eligible(int64_t s, int64_t m) {
+  const char* v = std::getenv("NSK_CS_MODE");
+  if (v && (std::string(v) == "tma" || std::string(v) == "stream")) return false;
+  return s >= CS_THREADS && s <= 4 * CS_THREADS && m >= cs_tile_rows();
+}
+
+template <int T>
+int launch_owner_t(int bpt, const CsOwnerParams& p, int64_t splits, cudaStream_t st) {
+  return bpt == 1 ? launch_owner<1, T>(p, splits, st)
+       : bpt == 2 ? launch_owner<2, T>(p, splits, st)
+                  : launch_owner<4, T>(p, splits, st);
+}
 
 int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
                       int64_t ldsa, cudaStream_t st) {
@@ -417,8 +603,34 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   const bool gb = s * 8 > 96 * 1024;
   const int64_t groups = (n + NC - 1) / NC;
   const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda % 2) == 0;
-  const int64_t full = aligned ? mloc / CT : 0;          // tiles for the TMA kernel
-  const int64_t rest_rows = mloc - full * CT;
+  // Owner kernel over the leading T-row tiles that have a schedule.
+  const int T = tb->cs_T;
+  int64_t own_tiles = 0, splits_o = 0, per_o = 0;
+  if (aligned && tb->cs_sec && rows.row0 % T == 0) {
+    const int64_t g0 = rows.row0 / T;
+    own_tiles = mloc / T;
+    if (own_tiles > tb->cs_ntiles - g0) own_tiles = tb->cs_ntiles - g0 > 0 ? tb->cs_ntiles - g0 : 0;
+  }
+  if (own_tiles > 0) {
+    // waves of one CTA per SM: column pairs * splits a multiple of the SM count
+    const int64_t sms = sm_count(), pairs = (n + 1) / 2;
+    int64_t g = pairs, q = sms;
+    while (q) {
+      const int64_t r = g % q;
+      g = q;
+      q = r;
+    }
+    splits_o = sms / g;
+    while (pairs * splits_o < 2 * sms && splits_o * 2 <= own_tiles) splits_o *= 2;
+    if (splits_o > own_tiles) splits_o = own_tiles;
+    per_o = (own_tiles + splits_o - 1) / splits_o;
+    splits_o = (own_tiles + per_o - 1) / per_o;
+  }
+  const int64_t own_rows = own_tiles * T;
+  const double* Ar = A + own_rows;
+  const RowMap rest_map{rows.row0 + own_rows, 1, mloc - own_rows};
+  const int64_t full = aligned ? (mloc - own_rows) / CT : 0;  // tiles for the streaming kernel
+  const int64_t rest_rows = (mloc - own_rows) - full * CT;
   const int64_t rest_tiles = (rest_rows + CT - 1) / CT;  // tiles for the generic kernel
   const int ctas_per_sm = use_tma_ring() ? 2 : stream_occupancy(NC, gb, s);
   int64_t splits_f = 0, per_f = 0;
@@ -437,22 +649,32 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
     per_r = (rest_tiles + splits_r - 1) / splits_r;
     splits_r = (rest_tiles + per_r - 1) / per_r;
   }
-  const int64_t splits = splits_f + splits_r;
+  const int64_t splits = splits_o + splits_f + splits_r;
   Scratch part, gbins;
   NSK_CUDA_OK(part.alloc(sizeof(double) * splits * n * s, st));
-  if (gb) NSK_CUDA_OK(gbins.alloc(sizeof(double) * splits * groups * NC * s, st));
+  if (gb && splits_f + splits_r > 0)
+    NSK_CUDA_OK(gbins.alloc(sizeof(double) * (splits_f + splits_r) * groups * NC * s, st));
+  if (own_tiles > 0) {
+    CsOwnerParams p{A, lda, n, s, tb->cs_sec, tb->cs_off, rows.row0 / T, own_tiles, per_o,
+                    (tb->cs_sec_max + 127u) & ~127u, 0, 0, part.as<double>()};
+    const int bpt = static_cast<int>((s + CS_THREADS - 1) / CS_THREADS);
+    const int rc = T == 4096 ? launch_owner_t<4096>(bpt, p, splits_o, st) : launch_owner_t<3072>(bpt, p, splits_o, st);
+    if (rc) return rc;
+  }
   if (full > 0) {
-    CsParams p{A, lda, n, s, tb->cs_table, rows.row0, 0, full, per_f, CT, 0, part.as<double>(),
+    CsParams p{Ar, lda, n, s, tb->cs_table, rest_map.row0, 0, full, per_f, CT, splits_o, part.as<double>(),
                gb ? gbins.as<double>() : nullptr};
-    const int rc = use_tma_ring() ? launch_nc<TMA_RING>(NC, gb, p, groups, splits_f, st, true)
-                                  : launch_nc<STREAM>(NC, gb, p, groups, splits_f, st, true);
+    const bool timed = own_tiles == 0;  // one timed (dominant) kernel per apply
+    const int rc = use_tma_ring() ? launch_nc<TMA_RING>(NC, gb, p, groups, splits_f, st, timed)
+                                  : launch_nc<STREAM>(NC, gb, p, groups, splits_f, st, timed);
     if (rc) return rc;
   }
   if (rest_tiles > 0) {
     const int64_t last_rows = rest_rows - (rest_tiles - 1) * CT;
-    CsParams p{A, lda, n, s, tb->cs_table, rows.row0, full, rest_tiles, per_r, last_rows, splits_f, part.as<double>(),
+    CsParams p{Ar, lda, n, s, tb->cs_table, rest_map.row0, full, rest_tiles, per_r, last_rows, splits_o + splits_f,
+               part.as<double>(),
                gb ? gbins.as<double>() + splits_f * groups * NC * s : nullptr};
-    if (int rc = launch_nc<GENERIC>(NC, gb, p, groups, splits_r, st, full == 0)) return rc;
+    if (int rc = launch_nc<GENERIC>(NC, gb, p, groups, splits_r, st, full == 0 && own_tiles == 0)) return rc;
   }
   int64_t blocks = (s * n + 255) / 256;
   if (blocks > 8L * sm_count()) blocks = 8L * sm_count();

@@ -9,7 +9,7 @@ The SVD of the small SA then runs on the root rank (or every rank).
 Row maps:
   gaussian, countsketch, srht   contiguous shards (srht: multiples of 1024
                                 rows so the Hadamard split stays block-aligned;
-                                countsketch: multiples of 512 rows)
+                                countsketch: multiples of 12288 rows, or 512 for short matrices)
   srft, srdct                   cyclic shards: rank g holds rows g, g+P, ...
                                 (decimation in time keeps every local
                                 transform a plain strided DFT)
@@ -41,7 +41,11 @@ def row_partition(m: int, world: int, kind: str) -> List[RowShard]:
     if kind in ("srft", "srdct"):
         return [RowShard(g, world, (m - g + world - 1) // world if g < m else 0) for g in range(world)]
     align = _align_for(kind)
-    if m < align * world:
+    if kind == "countsketch":
+        # 12288 = lcm of the owner kernel's 3072/4096-row schedule tiles: every
+        # shard starts on a tile; short matrices keep the kernels' 512-row rule.
+        align = 12288 if m >= 12288 * world else 512
+    elif m < align * world:
         align = 1
     units = (m + align - 1) // align
     shards = []
