@@ -330,49 +330,45 @@ __global__ void __launch_bounds__(THREADS) countsketch_generic_kernel(CsParams p
 // Owner kernel (default when the schedule exists, cs_schedule.cpp): one CTA of
 // CS_THREADS threads per pair of columns and row split; thread t owns the
 // bins of the buckets b = t + j * CS_THREADS (j < BPT) of both columns in
-// registers.  Thread 0 streams each tile's two column segments (2 x 32 KiB)
-// and its schedule section into a shared-memory ring with 1-D TMA; each warp
-// then walks its iterations, in which every lane adds at most one staged row
-// (both columns) to one of its own bins, the 16 lanes of a half-warp reading
-// 16 distinct bank pairs.  No bin is shared: no shared-memory read-modify-
-// write, no barrier per tile; a stage is released through an mbarrier that
-// every warp arrives on.  Entry: row | slot << 12 | negative << 14 | valid << 15.
+// registers.  One thread streams each tile's two column segments (2 x 32 KiB)
+// into a STG-deep shared-memory ring with 1-D TMA; each warp walks its
+// iterations -- entries read straight from the L2-resident schedule, one
+// 8-byte group of four iterations per lane, prefetched a group and a tile
+// ahead -- and in every iteration each lane adds at most one staged row (both
+// columns) to one of its own bins, the 16 lanes of a half-warp reading 16
+// distinct bank pairs.  No bin is shared: no shared-memory read-modify-write
+// and no barrier per tile; the last warp to finish a stage refills it.
 struct CsOwnerParams {
   const double* A;
   int64_t lda;
   int64_t n;
   int64_t s;
-  const uint8_t* sec;
-  const uint64_t* off;
-  int64_t g0;          // global tile of local tile 0
-  int64_t ntiles;      // tiles handled by this launch
-  int64_t per;         // tiles per split
-  uint32_t sec_bytes;  // section stride in the stage (>= largest section, 128-byte multiple)
-  int stages;
+  const uint64_t* ent;  // schedule of global tile 0
+  const uint8_t* cnt;
+  int64_t g0;           // global tile of local tile 0
+  int64_t ntiles;       // tiles handled by this launch
+  int64_t per;          // tiles per split
   int64_t split_base;
-  double* P;           // partials [split][n][s]
+  double* P;            // partials [split][n][s]
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// One schedule entry: bin j of both columns += sigma * value, as an FMA with a
-// multiplier that is sigma for the entry's slot and 0 for the other slots
-// (ptxas if-converts predicated DADDs into DADD + 2 FSEL; the multiplier costs
-// one SEL per slot for both columns).  x * 0 = +-0 leaves a bin unchanged for
-// every finite x; a non-finite entry of A reaches all bins of its owner thread.
-template <int BPT, int T>
+// One schedule entry (bits 0-15 of e): bin j of both columns += sigma * value,
+// as an FMA with a multiplier that is sigma for the entry's slot and 0 for the
+// other slots (ptxas if-converts predicated DADDs into DADD + 2 FSEL; the
+// multiplier costs one SEL per slot for both columns).  x * 0 = +-0 leaves a
+// bin unchanged for every finite x; a non-finite entry of A reaches all bins
+// of its owner thread.
+template <int BPT>
 __device__ __forceinline__ void owner_step(uint32_t e, const unsigned char* base, double (&b0)[BPT],
                                            double (&b1)[BPT]) {
   const uint32_t off = (e & 0xFFFu) * 8u;
   const double v0 = *reinterpret_cast<const double*>(base + off);
-  const double v1 = *reinterpret_cast<const double*>(base + T * 8 + off);
-  const uint32_t one_hi = 0x3FF00000u | ((e & 0x4000u) << 17);  // +-1.0, high word
-  const uint32_t sel = e & 0xB000u;
+  const double v1 = *reinterpret_cast<const double*>(base + CS_T * 8 + off);
+  const uint32_t one_hi = 0x3FF00000u | ((e << 16) & 0x80000000u);  // +-1.0, high word
+  const uint32_t sel = e & 0x7000u;                                   // valid | slot
 #pragma unroll
   for (int j = 0; j < BPT; ++j) {
-    const uint32_t hi = sel == (0x8000u | (static_cast<uint32_t>(j) << 12)) ? one_hi : 0u;
+    const uint32_t hi = sel == (0x4000u | (static_cast<uint32_t>(j) << 12)) ? one_hi : 0u;
     const double mj = __hiloint2double(static_cast<int>(hi), 0);
     b0[j] = fma(v0, mj, b0[j]);
     b1[j] = fma(v1, mj, b1[j]);
@@ -393,15 +389,16 @@ __device__ __forceinline__ void mbar_sleep_wait(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
-template <int BPT, int STG, int T>
+template <int BPT, int STG>
 __global__ void __launch_bounds__(CS_THREADS, 1) countsketch_owner_kernel(CsOwnerParams p) {
-  extern __shared__ __align__(128) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];  // [STG][2][CS_T] doubles
   __shared__ __align__(8) uint64_t full[STG];
   __shared__ uint32_t done[STG];  // warps finished with the stage's current tile
+  constexpr uint32_t stage_bytes = 2 * CS_T * 8;
+  constexpr int64_t TILE_ENT = static_cast<int64_t>(CS_WARPS) * CS_GMAX * 32;  // u64 per tile
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = 2 * static_cast<int64_t>(blockIdx.x), split = blockIdx.y;
   const int ncol = p.n - c0 >= 2 ? 2 : 1;
-  const uint32_t stage_bytes = 2 * T * 8 + p.sec_bytes;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STG; ++i) {
       mbar_init(&full[i], 1);
@@ -412,20 +409,20 @@ __global__ void __launch_bounds__(CS_THREADS, 1) countsketch_owner_kernel(CsOwne
   __syncthreads();
   const int64_t tbeg = split * p.per;
   const int ntl = static_cast<int>((tbeg + p.per < p.ntiles ? tbeg + p.per : p.ntiles) - tbeg);
-  const double* Acol = p.A + c0 * p.lda + tbeg * T;
-  const uint64_t* off = p.off + p.g0 + tbeg;
+  const double* Acol = p.A + c0 * p.lda + tbeg * CS_T;
   auto issue = [&](int k, int st) {  // one thread: tile k into stage st
-    const uint64_t o0 = __ldg(off + k), o1 = __ldg(off + k + 1);
-    const uint32_t sb = static_cast<uint32_t>(o1 - o0);
     unsigned char* base = smraw + static_cast<size_t>(st) * stage_bytes;
-    mbar_expect_tx(&full[st], ncol * T * 8 + sb);
-    tma_load_1d(base, Acol + static_cast<int64_t>(k) * T, T * 8, &full[st]);
-    if (ncol == 2) tma_load_1d(base + T * 8, Acol + p.lda + static_cast<int64_t>(k) * T, T * 8, &full[st]);
-    tma_load_1d(base + 2 * T * 8, p.sec + o0, sb, &full[st]);
+    mbar_expect_tx(&full[st], ncol * CS_T * 8);
+    tma_load_1d(base, Acol + static_cast<int64_t>(k) * CS_T, CS_T * 8, &full[st]);
+    if (ncol == 2) tma_load_1d(base + CS_T * 8, Acol + p.lda + static_cast<int64_t>(k) * CS_T, CS_T * 8, &full[st]);
   };
   if (threadIdx.x == 0)
     for (int k = 0; k < STG && k < ntl; ++k) issue(k, k);
 
+  const uint64_t* ew = p.ent + (p.g0 + tbeg) * TILE_ENT + static_cast<int64_t>(w) * (CS_GMAX * 32) + lane;
+  const uint8_t* cw = p.cnt + (p.g0 + tbeg) * CS_WARPS + w;
+  int n_next = ntl > 0 ? __ldg(cw) : 0;
+  uint64_t g_next = ntl > 0 ? __ldg(ew) : 0;
   double b0[BPT], b1[BPT];
 #pragma unroll
   for (int j = 0; j < BPT; ++j) b0[j] = b1[j] = 0.0;
@@ -433,19 +430,31 @@ __global__ void __launch_bounds__(CS_THREADS, 1) countsketch_owner_kernel(CsOwne
   uint32_t ph = 0;
   const unsigned char* base = smraw;
   for (int k = 0; k < ntl; ++k) {
-    mbar_sleep_wait(&full[st], ph);
-    const uint16_t* hdr = reinterpret_cast<const uint16_t*>(base + 2 * T * 8);
-    const uint32_t span = *reinterpret_cast<const uint32_t*>(hdr + (w & ~1));  // hdr[w], hdr[w+1] (w even)
-    const int i0 = (w & 1) ? static_cast<int>(span >> 16) : static_cast<int>(span & 0xFFFFu);
-    const int i1 = (w & 1) ? hdr[w + 1] : static_cast<int>(span >> 16);
-    const uint16_t* ent = hdr + 64 + lane;
-    int it = i0;
-    for (; it + 1 < i1; it += 2) {  // two iterations per trip: independent shared loads in flight
-      const uint32_t e0 = ent[it * 32], e1 = ent[(it + 1) * 32];
-      owner_step<BPT, T>(e0, base, b0, b1);
-      owner_step<BPT, T>(e1, base, b0, b1);
+    int left = n_next;
+    uint64_t E = g_next;
+    const uint64_t* ek = ew + static_cast<int64_t>(k) * TILE_ENT;
+    if (k + 1 < ntl) {  // next tile's count and first group
+      n_next = __ldg(cw + static_cast<int64_t>(k + 1) * CS_WARPS);
+      g_next = __ldg(ek + TILE_ENT);
     }
-    if (it < i1) owner_step<BPT, T>(ent[it * 32], base, b0, b1);
+    mbar_sleep_wait(&full[st], ph);
+    for (; left > 4; left -= 4) {  // full groups that have a successor
+      ek += 32;
+      const uint64_t En = __ldg(ek);
+      const uint32_t lo = static_cast<uint32_t>(E), hi = static_cast<uint32_t>(E >> 32);
+      owner_step<BPT>(lo, base, b0, b1);
+      owner_step<BPT>(lo >> 16, base, b0, b1);
+      owner_step<BPT>(hi, base, b0, b1);
+      owner_step<BPT>(hi >> 16, base, b0, b1);
+      E = En;
+    }
+    {  // last group: 0..4 iterations (warp-uniform)
+      const uint32_t lo = static_cast<uint32_t>(E), hi = static_cast<uint32_t>(E >> 32);
+      if (left > 0) owner_step<BPT>(lo, base, b0, b1);
+      if (left > 1) owner_step<BPT>(lo >> 16, base, b0, b1);
+      if (left > 2) owner_step<BPT>(hi, base, b0, b1);
+      if (left > 3) owner_step<BPT>(hi >> 16, base, b0, b1);
+    }
     __syncwarp();
     if (lane == 0) {  // the last warp to finish the stage refills it
       __threadfence_block();
@@ -542,25 +551,15 @@ bool use_tma_ring() {
   return v && std::string(v) == "tma";
 }
 
-template <int BPT, int T>
-int launch_owner(const CsOwnerParams& p0, int64_t splits, cudaStream_t st) {
-  CsOwnerParams p = p0;
-  const size_t stage = 2 * T * 8 + p.sec_bytes;
-  int dev = 0, optin = 0;
-  NSK_CUDA_OK(cudaGetDevice(&dev));
-  NSK_CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t budget = static_cast<size_t>(optin) - 2048;
-  p.stages = static_cast<int>(budget / stage);
-  if (p.stages > 4) p.stages = 4;
-  if (p.stages < 2) return fail(EINVAL_, "countsketch owner: schedule section too large");
-  const size_t smem = stage * static_cast<size_t>(p.stages);
-  auto kern = p.stages == 2 ? countsketch_owner_kernel<BPT, 2, T>
-            : p.stages == 3 ? countsketch_owner_kernel<BPT, 3, T>
-                            : countsketch_owner_kernel<BPT, 4, T>;
+constexpr int CS_OWNER_STAGES = 3;  // 3 x 64 KiB of the 227 KiB
+
+template <int BPT>
+int launch_owner(const CsOwnerParams& p, int64_t splits, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(CS_OWNER_STAGES) * 2 * CS_T * 8;
+  auto kern = countsketch_owner_kernel<BPT, CS_OWNER_STAGES>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   KernelTimer tm(st, true);
-  kern<<<dim3(static_cast<unsigned>((p.n + 1) / 2), static_cast<unsigned>(splits)), CS_THREADS, smem, st>>>(
-      p);
+  kern<<<dim3(static_cast<unsigned>((p.n + 1) / 2), static_cast<unsigned>(splits)), CS_THREADS, smem, st>>>(p);
   tm.stop();
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
@@ -572,14 +571,7 @@ int launch_owner(const CsOwnerParams& p0, int64_t splits, cudaStream_t st) {
 bool cs_owner_eligible(int64_t s, int64_t m) {
   const char* v = std::getenv("NSK_CS_MODE");
   if (v && (std::string(v) == "tma" || std::string(v) == "stream")) return false;
-  return s >= CS_THREADS && s <= 4 * CS_THREADS && m >= cs_tile_rows();
-}
-
-template <int T>
-int launch_owner_t(int bpt, const CsOwnerParams& p, int64_t splits, cudaStream_t st) {
-  return bpt == 1 ? launch_owner<1, T>(p, splits, st)
-       : bpt == 2 ? launch_owner<2, T>(p, splits, st)
-                  : launch_owner<4, T>(p, splits, st);
+  return s >= CS_THREADS && s <= 4 * CS_THREADS && m >= CS_T;
 }
 
 int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
@@ -604,9 +596,9 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   const int64_t groups = (n + NC - 1) / NC;
   const bool aligned = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda % 2) == 0;
   // Owner kernel over the leading T-row tiles that have a schedule.
-  const int T = tb->cs_T;
+  const int T = CS_T;
   int64_t own_tiles = 0, splits_o = 0, per_o = 0;
-  if (aligned && tb->cs_sec && rows.row0 % T == 0) {
+  if (aligned && tb->cs_ent && rows.row0 % T == 0) {
     const int64_t g0 = rows.row0 / T;
     own_tiles = mloc / T;
     if (own_tiles > tb->cs_ntiles - g0) own_tiles = tb->cs_ntiles - g0 > 0 ? tb->cs_ntiles - g0 : 0;
@@ -655,10 +647,11 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   if (gb && splits_f + splits_r > 0)
     NSK_CUDA_OK(gbins.alloc(sizeof(double) * (splits_f + splits_r) * groups * NC * s, st));
   if (own_tiles > 0) {
-    CsOwnerParams p{A, lda, n, s, tb->cs_sec, tb->cs_off, rows.row0 / T, own_tiles, per_o,
-                    (tb->cs_sec_max + 127u) & ~127u, 0, 0, part.as<double>()};
+    CsOwnerParams p{A, lda, n, s, tb->cs_ent, tb->cs_cnt, rows.row0 / T, own_tiles, per_o, 0, part.as<double>()};
     const int bpt = static_cast<int>((s + CS_THREADS - 1) / CS_THREADS);
-    const int rc = T == 4096 ? launch_owner_t<4096>(bpt, p, splits_o, st) : launch_owner_t<3072>(bpt, p, splits_o, st);
+    const int rc = bpt == 1 ? launch_owner<1>(p, splits_o, st)
+                 : bpt == 2 ? launch_owner<2>(p, splits_o, st)
+                            : launch_owner<4>(p, splits_o, st);
     if (rc) return rc;
   }
   if (full > 0) {

@@ -7,20 +7,25 @@
 //   * the kernel runs CS_THREADS threads per CTA and every thread OWNS the
 //     buckets b with b % CS_THREADS == thread, holding their bins in registers
 //     (slot j = b / CS_THREADS), so no two threads ever update the same bin;
-//   * a T-row tile (T <= 4096) of one column is staged in shared memory; the rows of
-//     warp w (rows whose bucket's owner lives in warp w) are processed in
-//     "iterations": in each iteration a lane handles at most one of its rows;
+//   * a T-row tile (T <= 4096) of a column pair is staged in shared memory; the
+//     rows of warp w (rows whose bucket's owner lives in warp w) are processed
+//     in "iterations": in each iteration a lane handles at most one of its rows;
 //   * the rows of each half-warp form a bipartite multigraph (lane, r mod 16)
-//     -- r mod 16 is the shared-memory bank pair of the staged double -- and an
-//     iteration must be a matching so that the 16 lanes' 8-byte reads hit 16
-//     distinct bank pairs.  Bipartite edge colouring (Koenig: Delta colours,
-//     alternating-path recolouring) gives the fewest iterations.
+//     -- r mod 16 is the shared-memory bank pair of the staged double.  An
+//     iteration gives every lane at most one row and every bank pair at most
+//     two (a 2-way conflict costs one extra wavefront; demanding distinct bank
+//     pairs would add ~10% iterations, each ~30 instructions).  Splitting each
+//     bank pair into two vertices that take its rows alternately turns this
+//     into bipartite edge colouring (Koenig: Delta colours, alternating-path
+//     recolouring): iterations = max(lane degree, ceil(bank degree / 2)).
 //
-// Section of one tile (bytes, 16-byte multiple):
-//   u16 hdr[64]: hdr[w] = first iteration of warp w, hdr[32] = total
-//   u16 ent[total][32]: ent[it][lane] = row | slot << 12 | negative << 14 | 1 << 15
+// Layout (read by the kernel straight from global memory / L2):
+//   cnt[tile][warp]                         u8   iterations of the warp
+//   ent[tile][warp][group][lane]            u64  iterations 4*group + j in bits 16j..16j+15,
+//                                                group < CS_GMAX (fixed stride: no offsets)
+//   entry = row | slot << 12 | valid << 14 | negative << 15; an idle lane's
+//   entry has no valid bit and a row whose bank pair no active lane uses.
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -31,12 +36,12 @@ namespace nsk {
 
 namespace {
 
-constexpr int MAXC = 32;  // colours per half-warp (Delta ~ 8-10 at 3-4 rows per lane and tile)
+constexpr int MAXC = 4 * CS_GMAX;  // iterations per warp and tile (Delta ~ 9 at 4 rows per lane)
 
-// Edge-colours ne edges (L[e] in [0,16), R[e] in [0,16)); returns the colour
+// Edge-colours ne edges (L[e] in [0,16), R[e] in [0,32)); returns the colour
 // count or -1 if more than MAXC would be needed.
 int color_half(int ne, const uint8_t* L, const uint8_t* R, uint8_t* col) {
-  int16_t atL[16][MAXC], atR[16][MAXC];
+  int16_t atL[16][MAXC], atR[32][MAXC];
   std::memset(atL, 0xFF, sizeof atL);
   std::memset(atR, 0xFF, sizeof atR);
   int ncol = 0;
@@ -81,35 +86,38 @@ int color_half(int ne, const uint8_t* L, const uint8_t* R, uint8_t* col) {
   return ncol;
 }
 
-// Builds the section of one tile into out (cleared); returns false on overflow.
-bool build_tile(const uint32_t* bucket_sign, int T, std::vector<uint16_t>& out) {
-  // rows per warp, in increasing row order
-  std::vector<uint16_t> rows[CS_WARPS];
+// Builds one tile: ent (CS_WARPS * CS_GMAX * 32 u64, zeroed) and cnt
+// (CS_WARPS u8).  Returns false if a warp needs more than MAXC iterations.
+bool build_tile(const uint32_t* bucket_sign, int T, uint64_t* ent, uint8_t* cnt) {
+  std::vector<uint16_t> rows[CS_WARPS];  // rows per warp, in increasing row order
   for (int w = 0; w < CS_WARPS; ++w) rows[w].reserve(2 * T / CS_WARPS);
   for (int r = 0; r < T; ++r) {
     const uint32_t b = bucket_sign[r] & 0xFFFFu;
     rows[(b % CS_THREADS) / 32].push_back(static_cast<uint16_t>(r));
   }
-  out.assign(64, 0);
-  int total = 0;
   std::vector<uint8_t> L[2], R[2], C[2];
   std::vector<uint16_t> E[2];
+  uint16_t grid[MAXC][32];
   for (int w = 0; w < CS_WARPS; ++w) {
     for (int h = 0; h < 2; ++h) {
       L[h].clear();
       R[h].clear();
       E[h].clear();
     }
+    // Right vertices: the two copies of each bank pair (a bank pair may serve two
+    // lanes of a half-warp per iteration: at most one extra wavefront), the
+    // rows of a bank pair dealt to its copies alternately.
+    uint8_t seen[2][16] = {};
     for (uint16_t r : rows[w]) {
       const uint32_t e = bucket_sign[r];
       const uint32_t b = e & 0xFFFFu;
       const int lane = static_cast<int>(b % 32);
       const int h = lane >> 4;
       L[h].push_back(static_cast<uint8_t>(lane & 15));
-      R[h].push_back(static_cast<uint8_t>(r & 15));
+      R[h].push_back(static_cast<uint8_t>((r & 15) * 2 + (seen[h][r & 15]++ & 1)));
       const uint32_t slot = b / CS_THREADS;
-      const uint32_t sg = ((e >> 16) & 1u) ^ 1u;  // 1 = negative
-      E[h].push_back(static_cast<uint16_t>(r | (slot << 12) | (sg << 14) | (1u << 15)));
+      const uint32_t neg = ((e >> 16) & 1u) ^ 1u;
+      E[h].push_back(static_cast<uint16_t>(r | (slot << 12) | (1u << 14) | (neg << 15)));
     }
     int iters = 0;
     for (int h = 0; h < 2; ++h) {
@@ -118,50 +126,44 @@ bool build_tile(const uint32_t* bucket_sign, int T, std::vector<uint16_t>& out) 
       if (nc < 0) return false;
       iters = std::max(iters, nc);
     }
-    out[static_cast<size_t>(w)] = static_cast<uint16_t>(total);
-    const size_t base = out.size();
-    out.resize(base + static_cast<size_t>(iters) * 32, 0);
+    std::memset(grid, 0, sizeof grid);
     for (int h = 0; h < 2; ++h)
-      for (size_t x = 0; x < E[h].size(); ++x) {
-        const int lane = h * 16 + L[h][x];
-        out[base + static_cast<size_t>(C[h][x]) * 32 + static_cast<size_t>(lane)] = E[h][x];
-      }
+      for (size_t x = 0; x < E[h].size(); ++x) grid[C[h][x]][h * 16 + L[h][x]] = E[h][x];
     // Idle lanes still execute the shared loads: point each at a row whose bank
-    // pair no active lane of its half-warp uses (entry without the valid bit).
+    // pair no active lane of its half-warp uses (entry without the valid bit;
+    // k active lanes leave at least 16 - k bank pairs free).
     for (int k = 0; k < iters; ++k)
       for (int h = 0; h < 2; ++h) {
-        uint16_t* it = out.data() + base + static_cast<size_t>(k) * 32 + 16 * h;
+        uint16_t* it = grid[k] + 16 * h;
         uint32_t used = 0;
         for (int l = 0; l < 16; ++l)
-          if (it[l] & 0x8000u) used |= 1u << (it[l] & 15u);
+          if (it[l] & 0x4000u) used |= 1u << (it[l] & 15u);
         int p = 0;
         for (int l = 0; l < 16; ++l)
-          if (!(it[l] & 0x8000u)) {
+          if (!(it[l] & 0x4000u)) {
             while (used & (1u << p)) ++p;
             it[l] = static_cast<uint16_t>(p);
             used |= 1u << p;
           }
       }
-    total += iters;
-    if (total > 0xFFFF) return false;
+    cnt[w] = static_cast<uint8_t>(iters);
+    uint64_t* we = ent + static_cast<size_t>(w) * CS_GMAX * 32;
+    for (int k = 0; k < iters; ++k)
+      for (int l = 0; l < 32; ++l)
+        we[(k >> 2) * 32 + l] |= static_cast<uint64_t>(grid[k][l]) << (16 * (k & 3));
   }
-  out[CS_WARPS] = static_cast<uint16_t>(total);
   return true;
 }
 
 }  // namespace
 
-int cs_tile_rows() {
-  const char* v = std::getenv("NSK_CS_T");
-  if (v && std::atoi(v) == 3072) return 3072;
-  return 4096;
-}
-
-int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, std::vector<uint8_t>& sec,
-                      std::vector<uint64_t>& off, uint32_t& max_bytes) {
+int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, std::vector<uint64_t>& ent,
+                      std::vector<uint8_t>& cnt) {
   if (s < 1 || s > 4 * CS_THREADS) return EINVAL_;
   if (T < 16 || T > CS_T_MAX || T % 16) return EINVAL_;
-  std::vector<std::vector<uint16_t>> tiles(static_cast<size_t>(ntiles));
+  const size_t per_tile = static_cast<size_t>(CS_WARPS) * CS_GMAX * 32;
+  ent.assign(static_cast<size_t>(ntiles) * per_tile, 0);
+  cnt.assign(static_cast<size_t>(ntiles) * CS_WARPS, 0);
   unsigned nth = std::thread::hardware_concurrency();
   if (nth < 1) nth = 1;
   if (nth > 32) nth = 32;
@@ -171,7 +173,8 @@ int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, s
   for (unsigned q = 0; q < nth; ++q)
     pool.emplace_back([&, q]() {
       for (int64_t t = q; t < ntiles; t += nth)
-        if (!build_tile(table + t * T, T, tiles[static_cast<size_t>(t)])) {
+        if (!build_tile(table + t * T, T, ent.data() + static_cast<size_t>(t) * per_tile,
+                        cnt.data() + static_cast<size_t>(t) * CS_WARPS)) {
           ok[q] = 0;
           return;
         }
@@ -179,32 +182,24 @@ int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, s
   for (auto& th : pool) th.join();
   for (char c : ok)
     if (!c) return EINVAL_;
-  off.assign(static_cast<size_t>(ntiles) + 1, 0);
-  max_bytes = 0;
-  for (int64_t t = 0; t < ntiles; ++t) {
-    const uint64_t bytes = tiles[static_cast<size_t>(t)].size() * 2;  // 128 + 64 * total: 16-byte multiple
-    off[static_cast<size_t>(t) + 1] = off[static_cast<size_t>(t)] + bytes;
-    if (bytes > max_bytes) max_bytes = static_cast<uint32_t>(bytes);
-  }
-  sec.resize(off.back());
-  for (int64_t t = 0; t < ntiles; ++t)
-    std::memcpy(sec.data() + off[static_cast<size_t>(t)], tiles[static_cast<size_t>(t)].data(),
-                tiles[static_cast<size_t>(t)].size() * 2);
   return OK;
 }
 
 }  // namespace nsk
 
-// Test hook (not part of the public header): builds the schedule for a host
+// Test hook (not part of the public header): builds the schedule of a host
 // table of ntiles * T entries (bits 0-15 bucket, bit 16 sign) into caller
-// buffers.  Returns the section byte count, or -1 on failure / short buffers.
-extern "C" long long nsk_internal_cs_schedule(const uint32_t* table, long long ntiles, int T, long long s,
-                                              uint8_t* sec, long long sec_cap, unsigned long long* off) {
-  std::vector<uint8_t> v;
-  std::vector<uint64_t> o;
-  uint32_t mx = 0;
-  if (nsk::build_cs_schedule(table, ntiles, T, s, v, o, mx) != nsk::OK) return -1;
-  if (sec && static_cast<long long>(v.size()) <= sec_cap) std::memcpy(sec, v.data(), v.size());
-  if (off) std::memcpy(off, o.data(), o.size() * sizeof(uint64_t));
-  return static_cast<long long>(v.size());
+// buffers ent (ntiles * 32 * CS_GMAX * 32 u64) and cnt (ntiles * 32 u8).
+// Returns 0, or -1 when no schedule exists (the streaming kernel is used).
+extern "C" int nsk_internal_cs_schedule(const uint32_t* table, long long ntiles, int T, long long s, uint64_t* ent,
+                                        uint8_t* cnt) {
+  std::vector<uint64_t> e;
+  std::vector<uint8_t> c;
+  if (nsk::build_cs_schedule(table, ntiles, T, s, e, c) != nsk::OK) return -1;
+  if (ent) std::memcpy(ent, e.data(), e.size() * sizeof(uint64_t));
+  if (cnt) std::memcpy(cnt, c.data(), c.size());
+  return 0;
 }
+
+// Group capacity, for the test hook's callers.
+extern "C" int nsk_internal_cs_gmax() { return nsk::CS_GMAX; }

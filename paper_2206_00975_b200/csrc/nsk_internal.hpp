@@ -30,24 +30,20 @@ struct DeviceTables {
   uint32_t* sign_mask = nullptr;    // SRHT: m-bit Rademacher mask, lane-transposed per 1024 rows
   uint32_t* cs_table = nullptr;     // CountSketch: per-row bucket | sign | tile chain (4 B/row)
   uint32_t* sign_bits = nullptr;    // srft/srdct: bit j of word j/32 = Rademacher bit of row j
-  // CountSketch owner schedule (cs_schedule.cpp): sections of CS_T-row tiles.
-  uint8_t* cs_sec = nullptr;
-  uint64_t* cs_off = nullptr;       // ntiles + 1 byte offsets into cs_sec
+  // CountSketch owner schedule (cs_schedule.cpp) over CS_T-row tiles.
+  uint64_t* cs_ent = nullptr;       // [tile][warp][CS_GMAX][32] packed entries
+  uint8_t* cs_cnt = nullptr;        // [tile][warp] iterations
   int64_t cs_ntiles = 0;            // full tiles covered (global tiles 0 .. cs_ntiles-1)
-  uint32_t cs_sec_max = 0;          // largest section (bytes)
-  int cs_T = 0;                     // rows per tile of the schedule
 };
 
 // CountSketch owner kernel geometry (countsketch.cu / cs_schedule.cpp).
-constexpr int CS_T_MAX = 4096;    // rows per tile: 12-bit row field of an entry
+constexpr int CS_T = 4096;        // rows per tile (12-bit row field of an entry)
+constexpr int CS_T_MAX = 4096;
 constexpr int CS_THREADS = 1024;  // bin owners per CTA
 constexpr int CS_WARPS = CS_THREADS / 32;
-// Tile rows used for new schedules: 4096 (two 86 KB stages; measured faster
-// than 3072 with three stages, whose lower fill costs ~15% more
-// instructions); NSK_CS_T=3072 selects the latter.
-int cs_tile_rows();
-int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, std::vector<uint8_t>& sec,
-                      std::vector<uint64_t>& off, uint32_t& max_bytes);
+constexpr int CS_GMAX = 6;        // groups of 4 iterations per warp and tile
+int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, std::vector<uint64_t>& ent,
+                      std::vector<uint8_t>& cnt);
 // Whether the owner kernel applies (bins fit 4 registers per thread, s large
 // enough that ~4 rows per lane per tile spread over distinct owners, at least
 // one full tile; NSK_CS_MODE=stream|tma forces the older kernels).

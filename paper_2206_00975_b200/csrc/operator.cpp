@@ -208,26 +208,22 @@ const DeviceTables* Operator::tables() const {
   if (kind == SRHT && m >= 1024 && build_sign_mask(key0, m, &t.sign_mask) != OK) return nullptr;
   if (kind == COUNTSKETCH && s <= 65536 && build_cs_table(key0, m, s, &t.cs_table) != OK) return nullptr;
   if (kind == COUNTSKETCH && cs_owner_eligible(s, m)) {
-    // Owner schedule over the full T-row tiles, from the device row table.
-    const int T = cs_tile_rows();
-    const int64_t ntiles = m / T;
-    std::vector<uint32_t> tab(static_cast<size_t>(ntiles * T));
-    std::vector<uint8_t> sec;
-    std::vector<uint64_t> off;
-    uint32_t mx = 0;
+    // Owner schedule over the full CS_T-row tiles, from the device row table.
+    const int64_t ntiles = m / CS_T;
+    std::vector<uint32_t> tab(static_cast<size_t>(ntiles * CS_T));
+    std::vector<uint64_t> ent;
+    std::vector<uint8_t> cnt;
     if (cudaMemcpy(tab.data(), t.cs_table, tab.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
       cuda_fail(cudaGetLastError(), "countsketch table readback");
       return nullptr;
     }
-    if (ntiles > 0 && build_cs_schedule(tab.data(), ntiles, T, s, sec, off, mx) == OK) {
-      if (up(reinterpret_cast<void**>(&t.cs_sec), sec.data(), sec.size()) != cudaSuccess ||
-          up(reinterpret_cast<void**>(&t.cs_off), off.data(), off.size() * 8) != cudaSuccess) {
+    if (ntiles > 0 && build_cs_schedule(tab.data(), ntiles, CS_T, s, ent, cnt) == OK) {
+      if (up(reinterpret_cast<void**>(&t.cs_ent), ent.data(), ent.size() * 8) != cudaSuccess ||
+          up(reinterpret_cast<void**>(&t.cs_cnt), cnt.data(), cnt.size()) != cudaSuccess) {
         cuda_fail(cudaGetLastError(), "countsketch schedule upload");
         return nullptr;
       }
       t.cs_ntiles = ntiles;
-      t.cs_sec_max = mx;
-      t.cs_T = T;
     }  // else: the streaming kernel covers every tile
   }
   if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return nullptr;
@@ -279,8 +275,8 @@ Operator::~Operator() {
     if (t.sign_mask) cudaFree(t.sign_mask);
     if (t.cs_table) cudaFree(t.cs_table);
     if (t.sign_bits) cudaFree(t.sign_bits);
-    if (t.cs_sec) cudaFree(t.cs_sec);
-    if (t.cs_off) cudaFree(t.cs_off);
+    if (t.cs_ent) cudaFree(t.cs_ent);
+    if (t.cs_cnt) cudaFree(t.cs_cnt);
   }
   cudaSetDevice(cur);
 }
