@@ -146,6 +146,14 @@ cudaStream_t host_stream() {
   if (!st || dev != cur) {
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     dev = cur;
+    // Host entry points stage A in stream-ordered scratch: keep freed blocks
+    // in the device's default pool instead of unmapping them at every
+    // synchronisation, so repeated calls do not re-map gigabytes of HBM.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
   }
   return st;
 }

@@ -348,8 +348,10 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
   extern __shared__ __align__(16) double sm[];  // [2b][ld * NC]
   __shared__ int rot_count;
   __shared__ unsigned char ptab[31 * 16][2];    // inner round-robin pairs (2b <= 32)
+  __shared__ double red[4 * (BJT / 32)];        // per-warp partial inner products
   const int n = static_cast<int>(P.n), ld = 2 * n, colsz = ld * NC;
   const int b = P.b, twob = 2 * b;
+  const int wpp = (BJT / 32) / b > 0 ? (BJT / 32) / b : 1;  // warps per column pair
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < (twob - 1) * b; e += BJT) {
     int64_t lp, lq;
@@ -365,25 +367,48 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
         int64_t pb, qb;
         pair_of_round(P.B, r, i, pb, qb);
         if (threadIdx.x == 0) rot_count = 0;
-        for (int lc = 0; lc < twob; ++lc) {
-          const int64_t gc = lc < b ? pb * b + lc : qb * b + (lc - b);
-          const double* src = P.X + gc * colsz;
-          double* dst = sm + lc * colsz;
-          for (int e = threadIdx.x; e < colsz; e += BJT) dst[e] = gc < n ? __ldcg(src + e) : 0.0;
+        // Stage the block pair: each block is b contiguous columns of X, so both
+        // are one contiguous span; 16-byte loads, four in flight per thread.
+        for (int half = 0; half < 2; ++half) {
+          const int64_t blk = half ? qb : pb;
+          const int64_t c0 = blk * b;
+          const int ncols = static_cast<int>(c0 + b <= n ? b : (c0 < n ? n - c0 : 0));
+          const int64_t nv = static_cast<int64_t>(ncols) * colsz / 2;  // colsz is even (ld = 2n)
+          const double2* src = reinterpret_cast<const double2*>(P.X + c0 * colsz);
+          double2* dst = reinterpret_cast<double2*>(sm + half * b * colsz);
+          int64_t e = threadIdx.x;
+          for (; e + 3 * BJT < nv; e += 4 * BJT) {
+            const double2 v0 = __ldcg(src + e), v1 = __ldcg(src + e + BJT), v2 = __ldcg(src + e + 2 * BJT),
+                          v3 = __ldcg(src + e + 3 * BJT);
+            dst[e] = v0;
+            dst[e + BJT] = v1;
+            dst[e + 2 * BJT] = v2;
+            dst[e + 3 * BJT] = v3;
+          }
+          for (; e < nv; e += BJT) dst[e] = __ldcg(src + e);
+          for (int64_t z = nv * 2 + threadIdx.x; z < static_cast<int64_t>(b) * colsz; z += BJT)
+            sm[half * b * colsz + z] = 0.0;  // columns past n
         }
         __syncthreads();
         for (int t = 0; t < twob - 1; ++t) {
-          for (int pi = warp; pi < b; pi += BJT / 32) {
+          // WPP warps per pair: each sums a slice of rows, the slices meet in
+          // shared memory and are added in fixed order by every warp of the
+          // pair (identical rotation everywhere), then each rotates its slice.
+          const int pi = warp / wpp, sub = warp - pi * wpp;
+          const bool active = pi < b;
+          double* xp = nullptr;
+          double* xq = nullptr;
+          if (active) {
             const int lp = ptab[t * b + pi][0], lq = ptab[t * b + pi][1];
-            double* xp = sm + lp * colsz;
-            double* xq = sm + lq * colsz;
+            xp = sm + lp * colsz;
+            xq = sm + lq * colsz;
             double a = 0, bb = 0, cr = 0, ci = 0;
-            for (int row = lane; row < n; row += 32) {
+            for (int row = sub * 32 + lane; row < n; row += 32 * wpp) {
               if (NC == 1) {
                 const double up = xp[row], uq = xq[row];
-                a += up * up;
-                bb += uq * uq;
-                cr += up * uq;
+                a = fma(up, up, a);
+                bb = fma(uq, uq, bb);
+                cr = fma(up, uq, cr);
               } else {
                 const double pr = xp[2 * row], pim = xp[2 * row + 1], qr = xq[2 * row], qim = xq[2 * row + 1];
                 a += pr * pr + pim * pim;
@@ -398,6 +423,24 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
               cr += __shfl_xor_sync(0xffffffffu, cr, o);
               if (NC == 2) ci += __shfl_xor_sync(0xffffffffu, ci, o);
             }
+            if (lane == 0) {
+              double* r = red + 4 * warp;
+              r[0] = a;
+              r[1] = bb;
+              r[2] = cr;
+              r[3] = ci;
+            }
+          }
+          __syncthreads();
+          if (active) {
+            double a = 0, bb = 0, cr = 0, ci = 0;
+            for (int w2 = 0; w2 < wpp; ++w2) {
+              const double* r = red + 4 * (pi * wpp + w2);
+              a += r[0];
+              bb += r[1];
+              cr += r[2];
+              ci += r[3];
+            }
             const double c2 = cr * cr + ci * ci;
             if (c2 > tol2 * a * bb && c2 > 0.0) {
               const double cabs = NC == 1 ? fabs(cr) : sqrt(c2);
@@ -407,8 +450,8 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
               const double cs = rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
               const double inv = NC == 2 ? 1.0 / cabs : 1.0;
               const double ph_re = NC == 2 ? cr * inv : 1.0, ph_im = NC == 2 ? -ci * inv : 0.0;
-              if (lane == 0) atomicAdd(&rot_count, 1);
-              for (int row = lane; row < ld; row += 32) {
+              if (lane == 0 && sub == 0) rot_count = 1;  // any rotation keeps the sweep loop going
+              for (int row = sub * 32 + lane; row < ld; row += 32 * wpp) {
                 if (NC == 1) {
                   const double up = xp[row], uq = xq[row];
                   xp[row] = cs * up - sn * uq;
@@ -427,12 +470,14 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
           }
           __syncthreads();
         }
-        for (int lc = 0; lc < twob; ++lc) {
-          const int64_t gc = lc < b ? pb * b + lc : qb * b + (lc - b);
-          if (gc >= n) continue;
-          double* dst = P.X + gc * colsz;
-          const double* src = sm + lc * colsz;
-          for (int e = threadIdx.x; e < colsz; e += BJT) dst[e] = src[e];
+        for (int half = 0; half < 2; ++half) {
+          const int64_t blk = half ? qb : pb;
+          const int64_t c0 = blk * b;
+          const int ncols = static_cast<int>(c0 + b <= n ? b : (c0 < n ? n - c0 : 0));
+          const int64_t nv = static_cast<int64_t>(ncols) * colsz / 2;
+          double2* dst = reinterpret_cast<double2*>(P.X + c0 * colsz);
+          const double2* src = reinterpret_cast<const double2*>(sm + half * b * colsz);
+          for (int64_t e = threadIdx.x; e < nv; e += BJT) __stcg(dst + e, src[e]);
         }
         if (threadIdx.x == 0 && rot_count) atomicAdd(P.counter + sweep, rot_count);
         __syncthreads();
@@ -534,11 +579,12 @@ template <int NC>
 int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W, int64_t ldw, double* sigma,
         cudaStream_t st) {
   Scratch ws;
-  const size_t abytes = sizeof(double) * s * n * NC, xbytes = sizeof(double) * 2 * n * n * NC;
+  const size_t apad = (s * n * NC + 1) & ~static_cast<int64_t>(1);  // X 16-byte aligned (double2 staging)
+  const size_t abytes = sizeof(double) * apad, xbytes = sizeof(double) * 2 * n * n * NC;
   const size_t extra = sizeof(double) * (n + n * NC + n) + sizeof(int) * (MAX_SWEEPS + 2 + 2 * n) + 64;
   NSK_CUDA_OK(ws.alloc(abytes + xbytes + extra, st));
   double* A = ws.as<double>();
-  double* X = A + s * n * NC;
+  double* X = A + apad;
   double* tau = X + 2 * n * n * NC;
   double* rdiag = tau + n;
   double* norms = rdiag + n * NC;
@@ -568,7 +614,13 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   // carries ~sqrt(n) * eps relative rounding noise, so the tighter
   // sqrt(n) * eps of dgesvj can stall on 1e-10-graded spectra.
   const double tol = static_cast<double>(n) * 2.220446049250313e-16;
-  int b = 16;  // block width: a block pair of [R; I] columns must fit in shared memory
+  // Block width: the rotations of a round are FP64-throughput bound on the SMs
+  // that hold a block pair, so spread them -- the widest b in {16, 8, 4, 2}
+  // that still leaves >= 32 block pairs (CTAs) -- and a block pair of [R; I]
+  // columns must fit in shared memory.  NSK_SVD_B overrides (tuning).
+  int b = 16;
+  while (b > 2 && n / b < 64) b >>= 1;
+  if (const char* e = std::getenv("NSK_SVD_B")) b = std::atoi(e) >= 1 && std::atoi(e) <= 16 ? std::atoi(e) : b;
   while (b > 1 && sizeof(double) * 2 * b * 2 * n * NC > 200 * 1024) b >>= 1;
   const bool blocked = sizeof(double) * 2 * b * 2 * n * NC <= 200 * 1024 && std::getenv("NSK_SVD_PAIRS") == nullptr;
   if (n >= 2 && blocked) {  // 2. block one-sided Jacobi on [R; I]
