@@ -390,7 +390,12 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
             sm[half * b * colsz + z] = 0.0;  // columns past n
         }
         __syncthreads();
-        for (int t = 0; t < twob - 1; ++t) {
+        // Outer round 0 of a sweep pairs every block with its partner for the
+        // first time: full round-robin over the 2b columns (intra-block pairs
+        // included); later outer rounds only the b^2 cross pairs -- every
+        // column pair once per sweep.
+        const int inner = r == 0 ? twob - 1 : b;
+        for (int t = 0; t < inner; ++t) {
           // WPP warps per pair: each sums a slice of rows, the slices meet in
           // shared memory and are added in fixed order by every warp of the
           // pair (identical rotation everywhere), then each rotates its slice.
@@ -399,7 +404,8 @@ __global__ void __launch_bounds__(BJT) block_jacobi_kernel(BJParams P) {
           double* xp = nullptr;
           double* xq = nullptr;
           if (active) {
-            const int lp = ptab[t * b + pi][0], lq = ptab[t * b + pi][1];
+            const int lp = r == 0 ? ptab[t * b + pi][0] : pi;
+            const int lq = r == 0 ? ptab[t * b + pi][1] : b + (pi + t) % b;
             xp = sm + lp * colsz;
             xq = sm + lq * colsz;
             double a = 0, bb = 0, cr = 0, ci = 0;
@@ -623,7 +629,11 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   if (const char* e = std::getenv("NSK_SVD_B")) b = std::atoi(e) >= 1 && std::atoi(e) <= 16 ? std::atoi(e) : b;
   while (b > 1 && sizeof(double) * 2 * b * 2 * n * NC > 200 * 1024) b >>= 1;
   const bool blocked = sizeof(double) * 2 * b * 2 * n * NC <= 200 * 1024 && std::getenv("NSK_SVD_PAIRS") == nullptr;
-  if (n >= 2 && blocked) {  // 2. block one-sided Jacobi on [R; I]
+  int crc = NOTAPPLICABLE;
+  if (n >= 2) crc = cluster_jacobi(NC, X, n, tol, counter, st);  // 2a. whole [R; I] in one cluster
+  if (crc != OK && crc != NOTAPPLICABLE) return crc;
+  if (crc == OK) {
+  } else if (n >= 2 && blocked) {  // 2b. block one-sided Jacobi on [R; I] through L2
     BJParams P;
     P.X = X;
     P.n = n;

@@ -16,6 +16,7 @@ namespace nsk {
 
 enum Kind { GAUSSIAN = 0, SRFT = 1, SRDCT = 2, SRHT = 3, COUNTSKETCH = 4 };
 enum Status { OK = 0, EINVAL_ = 1, ERANGE_ = 2, ENOCONV = 3, ECUDA = 4, ENOMEM_ = 5 };
+constexpr int NOTAPPLICABLE = -100;  // internal: a specialised path declines, the caller falls back
 
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
@@ -114,6 +115,9 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
 int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
 
+// One-sided Jacobi on [R; I] (2n x n, ld 2n) inside one thread-block cluster
+// (cluster_jacobi.cu); NOTAPPLICABLE when it does not fit one cluster.
+int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cudaStream_t st);
 // One-sided Jacobi SVD of SA (s x n, ncomp = 1 real / 2 complex interleaved).
 // Writes the trailing k right singular vectors and all n singular values
 // (device, non-increasing).  Returns ENOCONV if the sweep limit is hit.
