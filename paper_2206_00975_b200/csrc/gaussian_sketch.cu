@@ -308,7 +308,8 @@ int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t 
     const int v = std::atoi(e);
     if (v == 128 || v == 256 || v == 512) BN = v;
   }
-  const int BM = 16384 / BN, BK = BN == 512 ? 8 : (BN == 256 ? 16 : 32);
+  // Must match Tile<BN>::BK: the kernel walks chunks of Tile<BN>::BK rows.
+  const int BM = 16384 / BN, BK = BN == 128 ? Tile<128>::BK : (BN == 256 ? Tile<256>::BK : Tile<512>::BK);
   const int64_t q_tiles = (nq + BN - 1) / BN;
   const int64_t s_tiles = (s + BM - 1) / BM;
   const int64_t chunks = (mloc + BK - 1) / BK;
