@@ -73,6 +73,7 @@ struct SrhtParams {
   const uint32_t* slot;  // s_pass slot values (idx), sorted by r_lo
   int nslots;
   double* P;           // partials [warp*2 + seg][NQ*32]
+  int pf;              // blocks of look-ahead for the L2 bulk prefetch (0: off; NSK_SRHT_PF)
 };
 
 __device__ __forceinline__ void bfly(double& a, double& b) {
@@ -117,6 +118,13 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
 
   for (; it < end; ++it) {
     const int64_t col = it / p.nb, blk = it - col * p.nb;
+    if (p.pf > 0 && lane == 0 && it + p.pf < end) {  // stage block it + pf in L2 (one bulk prefetch)
+      const int64_t c3 = (it + p.pf) / p.nb, b3 = (it + p.pf) - c3 * p.nb;
+      const double* a3 = p.A + c3 * p.lda + b3 * L;
+      if ((reinterpret_cast<uintptr_t>(a3) & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a3), "r"(static_cast<unsigned>(L * 8))
+                     : "memory");
+    }
     if (col != cur_col) {  // column boundary: flush segment 0
       double* P = p.P + (warp * 2 + seg) * (NQ * 32);
 #pragma unroll
@@ -291,8 +299,9 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
     const int NQ = nq <= 8 ? 8 : (nq <= 16 ? 16 : 32);
     Scratch part;
     NSK_CUDA_OK(part.alloc(sizeof(double) * warps * 2 * NQ * 32, st));
+    const char* pfe = std::getenv("NSK_SRHT_PF");
     SrhtParams p{A, lda, n, nb, rows.row0 / L, total, per, tb->sign_mask, tb->srht_slot + base, ns,
-                 part.as<double>()};
+                 part.as<double>(), pfe ? std::atoi(pfe) : 1};
     int rc = NQ == 8 ? launch_srht<8>(p, warps, lb, st)
                      : (NQ == 16 ? launch_srht<16>(p, warps, lb, st) : launch_srht<32>(p, warps, lb, st));
     if (rc != OK) return rc;
