@@ -192,6 +192,14 @@ int nsk_downdate_row(nsk_operator* op, int64_t j, int scalar_sa, int64_t n, int 
 int nsk_update_column(const nsk_operator* op, int scalar, int64_t m, const void* a_col, void* out,
                       void* stream);
 
+/* Host-buffer variants of the three calls above (SA, rows and columns in host
+ * memory, column-major; SA is updated in place, out receives the s entries). */
+int nsk_update_row_host(nsk_operator* op, int scalar_sa, int64_t n, int scalar_row, const void* a_row, void* SA,
+                        int64_t ldsa);
+int nsk_downdate_row_host(nsk_operator* op, int64_t j, int scalar_sa, int64_t n, int scalar_row,
+                          const void* a_row, void* SA, int64_t ldsa);
+int nsk_update_column_host(const nsk_operator* op, int scalar, int64_t m, const void* a_col, void* out);
+
 /* ---- sketched total least squares (tls.hpp:59-65, tls.cpp:97-113) ------- */
 
 /* X (n x k) = -V_k1 V_k2^{-1} from the trailing k right singular vectors Vk

@@ -12,6 +12,9 @@
 //   solve_k(A, k, S) -> NullspaceResult         solve_k(A, k, S) -> NullspaceResult
 //   solve_tol(A, eps, S)                        solve_tol(A, eps, S)
 //   residual_certificate(A, W)                  residual_certificate(A, W)
+//   update_row / downdate_row (sketch.hpp:90-109) same (S mutated, SA returned)
+//   update_column / downdate_column             same
+//   tls_solve_sketched(p, S, options) (tls.hpp) same, TlsExistenceError / TlsConditionError
 //   std::invalid_argument / std::out_of_range   same (from NSK_EINVAL / NSK_ERANGE)
 //   SvdConvergenceError                         SvdConvergenceError (NSK_ENOCONV)
 //
@@ -156,7 +159,12 @@ class SketchOperator {
   SketchKind kind() const { return static_cast<SketchKind>(info().kind); }
   Index s() const { return info().s; }
   Index m() const { return info().m; }
-  Index m_effective() const { return m(); }
+  Index m_effective() const {  // m plus rows appended by update_row (sketch.hpp:52)
+    int64_t me = 0;
+    check(nsk_op_state(h_, &me, nullptr, nullptr, nullptr, 0));
+    return me;
+  }
+  nsk_operator* mutable_handle() { return h_; }
   uint64_t seed() const { return info().seed; }
   uint64_t id() const { return info().id; }
   std::vector<int64_t> sample_indices() const {
@@ -256,6 +264,149 @@ inline double residual_certificate(const Matrix& A, const Matrix& W) {
   check(nsk_residual_fro_host(static_cast<int>(A.kind()), A.rows(), A.cols(), A.data(),
                               A.rows() > 0 ? A.rows() : 1, W.cols(), W.data(), W.rows() > 0 ? W.rows() : 1, &out));
   return out;
+}
+
+// ---- incremental maintenance (sketch.hpp:90-109) ---------------------------
+
+namespace detail {
+inline Matrix promote(const Matrix& x) {
+  if (!x.is_real()) return x;
+  Matrix c(x.rows(), x.cols(), ScalarKind::complex);
+  for (Index j = 0; j < x.cols(); ++j)
+    for (Index i = 0; i < x.rows(); ++i) c.set(i, j, x.at(i, j));
+  return c;
+}
+inline void same_operator(const SketchedMatrix& sa, const SketchOperator& S) {  // sketch.cpp:75-79
+  if (sa.operator_id != S.id())
+    throw std::invalid_argument("sketched matrix was produced by a different sketch operator");
+}
+}  // namespace detail
+
+// Append row a_row (1 x n): SA + g a_row / sqrt(s) with g the next Gaussian
+// column of stream (seed, 1); mutates S (m_effective grows by one).
+inline SketchedMatrix update_row(const SketchedMatrix& sa, SketchOperator& S, const Matrix& a_row) {
+  detail::same_operator(sa, S);
+  if (a_row.rows() != 1 || a_row.cols() != sa.data.cols())
+    throw std::invalid_argument("update_row: expected a 1 x " + std::to_string(sa.data.cols()) + " row");
+  SketchedMatrix out{a_row.is_real() ? sa.data : detail::promote(sa.data), sa.operator_id};
+  check(nsk_update_row_host(S.mutable_handle(), static_cast<int>(out.data.kind()), out.data.cols(),
+                            static_cast<int>(a_row.kind()), a_row.data(), out.data.data(), out.data.rows()));
+  return out;
+}
+
+// Remove row j whose current content is a_row_j (1 x n): SA - (S e_j) a_row_j.
+inline SketchedMatrix downdate_row(const SketchedMatrix& sa, SketchOperator& S, Index j, const Matrix& a_row_j) {
+  detail::same_operator(sa, S);
+  if (a_row_j.rows() != 1 || a_row_j.cols() != sa.data.cols())
+    throw std::invalid_argument("downdate_row: expected a 1 x " + std::to_string(sa.data.cols()) + " row");
+  SketchedMatrix out{a_row_j.is_real() ? sa.data : detail::promote(sa.data), sa.operator_id};
+  check(nsk_downdate_row_host(S.mutable_handle(), j, static_cast<int>(out.data.kind()), out.data.cols(),
+                              static_cast<int>(a_row_j.kind()), a_row_j.data(), out.data.data(), out.data.rows()));
+  return out;
+}
+
+// Insert the sketch of a_col (m_effective x 1; entries at zeroed rows are
+// forced to zero) as column `position` of SA.
+inline SketchedMatrix update_column(const SketchedMatrix& sa, const SketchOperator& S, const Matrix& a_col,
+                                    Index position) {
+  detail::same_operator(sa, S);
+  if (position < 0 || position > sa.data.cols()) throw std::out_of_range("update_column: position out of range");
+  if (a_col.cols() != 1) throw std::invalid_argument("update_column: expected a single column");
+  Matrix col(S.s(), 1, out_kind(S, a_col));
+  check(nsk_update_column_host(S.handle(), static_cast<int>(a_col.kind()), a_col.rows(), a_col.data(), col.data()));
+  const bool cplx = !sa.data.is_real() || !col.is_real();
+  Matrix out(sa.data.rows(), sa.data.cols() + 1, cplx ? ScalarKind::complex : ScalarKind::real);
+  for (Index j = 0; j < out.cols(); ++j)
+    for (Index i = 0; i < out.rows(); ++i)
+      out.set(i, j, j < position ? sa.data.at(i, j) : (j == position ? col.at(i, 0) : sa.data.at(i, j - 1)));
+  return {std::move(out), sa.operator_id};
+}
+
+// Remove column `position`: an exact splice.
+inline SketchedMatrix downdate_column(const SketchedMatrix& sa, Index position) {
+  if (position < 0 || position >= sa.data.cols()) throw std::out_of_range("downdate_column: position out of range");
+  Matrix out(sa.data.rows(), sa.data.cols() - 1, sa.data.kind());
+  for (Index j = 0; j < out.cols(); ++j)
+    for (Index i = 0; i < out.rows(); ++i) out.set(i, j, sa.data.at(i, j < position ? j : j + 1));
+  return {std::move(out), sa.operator_id};
+}
+
+// ---- sketched total least squares (tls.hpp) ---------------------------------
+
+struct TlsProblem {
+  Matrix A;  // m x n
+  Matrix B;  // m x k, m >= n + k, n >= k
+};
+
+struct TlsOptions {
+  bool allow_marginal = false;
+  bool certificate = false;  // exact ||[A|B] Vk||_F (one pass on the device)
+  double cond_limit = 1e12;
+};
+
+struct TlsSolution {
+  Matrix X;                                     // n x k, X = -V_k1 V_k2^{-1}
+  Matrix Vk;                                    // (n+k) x k trailing subspace of S [A|B]
+  double tls_residual = 0.0;                    // sqrt(sum of the k trailing sketched sigma^2)
+  double cond_Vk2 = 0.0;
+  std::vector<double> augmented_singular_values;
+  bool has_residual_certificate = false;
+  double residual_certificate = 0.0;
+};
+
+class TlsExistenceError : public std::runtime_error {
+ public:
+  TlsExistenceError(double sigma_n_a, double sigma_trailing)
+      : std::runtime_error("tls: solution does not exist (sigma_n(A) = " + std::to_string(sigma_n_a) +
+                           " <= sigma_{n+1}([A|B]) = " + std::to_string(sigma_trailing) + ")"),
+        sigma_n_a_(sigma_n_a),
+        sigma_trailing_(sigma_trailing) {}
+  double sigma_n_A() const { return sigma_n_a_; }
+  double sigma_trailing() const { return sigma_trailing_; }
+
+ private:
+  double sigma_n_a_, sigma_trailing_;
+};
+
+class TlsConditionError : public std::runtime_error {
+ public:
+  explicit TlsConditionError(double cond)
+      : std::runtime_error("tls: V_k2 is too ill-conditioned (cond = " + std::to_string(cond) + ")"), cond_(cond) {}
+  double cond() const { return cond_; }
+
+ private:
+  double cond_;
+};
+
+// tls.hpp: tls_solve_sketched -- the trailing subspace comes from S [A|B].
+inline TlsSolution tls_solve_sketched(const TlsProblem& p, const SketchOperator& S, const TlsOptions& options = {}) {
+  const Index m = p.A.rows(), n = p.A.cols(), k = p.B.cols();
+  if (p.B.rows() != m) throw std::invalid_argument("tls: A and B must have the same number of rows");
+  const bool cplx = !p.A.is_real() || !p.B.is_real();
+  const Matrix A = cplx ? detail::promote(p.A) : p.A, B = cplx ? detail::promote(p.B) : p.B;
+  const ScalarKind ok = (cplx || S.kind() == SketchKind::srft) ? ScalarKind::complex : ScalarKind::real;
+  TlsSolution r;
+  r.X = Matrix(n, k, ok);
+  r.Vk = Matrix(n + k, k, ok);
+  r.augmented_singular_values.resize(static_cast<size_t>(n + k));
+  double info[4] = {0, 0, 0, 0};
+  const int rc = nsk_tls_solve_sketched_host(S.handle(), static_cast<int>(A.kind()), m, n, k, A.data(),
+                                             m > 0 ? m : 1, B.data(), m > 0 ? m : 1, options.cond_limit,
+                                             options.allow_marginal ? 1 : 0, r.X.data(), n, r.Vk.data(), n + k,
+                                             r.augmented_singular_values.data(), info);
+  if (rc == NSK_ETLS_EXISTENCE) throw TlsExistenceError(info[2], info[3]);
+  if (rc == NSK_ETLS_CONDITION) throw TlsConditionError(info[1]);
+  check(rc);
+  r.tls_residual = info[0];
+  r.cond_Vk2 = info[1];
+  if (options.certificate) {
+    Matrix AB(m, n + k, A.kind());
+    for (Index j = 0; j < n + k; ++j)
+      for (Index i = 0; i < m; ++i) AB.set(i, j, j < n ? A.at(i, j) : B.at(i, j - n));
+    r.residual_certificate = residual_certificate(AB, r.Vk);
+    r.has_residual_certificate = true;
+  }
+  return r;
 }
 
 }  // namespace nullsketch_b200

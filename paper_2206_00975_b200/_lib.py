@@ -26,7 +26,8 @@ EXPORTS = (
     "nsk_apply_shard", "nsk_svd_trailing", "nsk_solve_k", "nsk_solve_tol", "nsk_residual_fro",
     "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_residual_fro_host", "nsk_kernel_launches",
     "nsk_timing_enable", "nsk_timing_collect", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
-    "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host",
+    "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_update_row_host",
+    "nsk_downdate_row_host", "nsk_update_column_host",
 )
 
 
@@ -80,6 +81,9 @@ def load():
     L.nsk_update_row.argtypes = [vp, c_int, i64, c_int, vp, vp, i64, vp]
     L.nsk_downdate_row.argtypes = [vp, i64, c_int, i64, c_int, vp, vp, i64, vp]
     L.nsk_update_column.argtypes = [vp, c_int, i64, vp, vp, vp]
+    L.nsk_update_row_host.argtypes = [vp, c_int, i64, c_int, vp, vp, i64]
+    L.nsk_downdate_row_host.argtypes = [vp, i64, c_int, i64, c_int, vp, vp, i64]
+    L.nsk_update_column_host.argtypes = [vp, c_int, i64, vp, vp]
     L.nsk_tls_solve_sketched.argtypes = [vp, c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp, i64,
                                          vp, i64, vp, dp, vp]
     L.nsk_tls_solve_sketched_host.argtypes = [vp, c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp,

@@ -544,6 +544,60 @@ int nsk_update_column(const nsk_operator* h, int scalar, int64_t m, const void* 
   return dispatch_apply(op, nc, rows, 1, c.as<double>(), m > 0 ? m : 1, static_cast<double*>(out), op.s, st);
 }
 
+// Host-buffer variants (the C++ mirror's update_row / downdate_row /
+// update_column): stage SA and the row or column in, call the device entry
+// point on the library's host stream, copy SA or the sketched column back.
+int nsk_update_row_host(nsk_operator* h, int scalar_sa, int64_t n, int scalar_row, const void* a_row, void* SA,
+                        int64_t ldsa) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (n < 0 || ldsa < op.s || (n > 0 && (!a_row || !SA))) return nsk::fail(nsk::EINVAL_, "update_row: bad arguments");
+  cudaStream_t st = host_stream();
+  const int nc_sa = scalar_sa == NSK_COMPLEX ? 2 : 1, nc_row = scalar_row == NSK_COMPLEX ? 2 : 1;
+  nsk::Scratch dsa, drow;
+  double *pSA = nullptr, *pRow = nullptr;
+  if (int rc = copy_in(SA, op.s, n, ldsa, nc_sa, &pSA, dsa, st)) return rc;
+  if (int rc = copy_in(a_row, 1, n, 1, nc_row, &pRow, drow, st)) return rc;
+  if (int rc = nsk_update_row(h, scalar_sa, n, scalar_row, pRow, pSA, op.s, st)) return rc;
+  if (int rc = copy_out(SA, ldsa, pSA, op.s, n, nc_sa, st)) return rc;
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return nsk::OK;
+}
+
+int nsk_downdate_row_host(nsk_operator* h, int64_t j, int scalar_sa, int64_t n, int scalar_row, const void* a_row,
+                          void* SA, int64_t ldsa) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (n < 0 || ldsa < op.s || (n > 0 && (!a_row || !SA)))
+    return nsk::fail(nsk::EINVAL_, "downdate_row: bad arguments");
+  cudaStream_t st = host_stream();
+  const int nc_sa = scalar_sa == NSK_COMPLEX ? 2 : 1, nc_row = scalar_row == NSK_COMPLEX ? 2 : 1;
+  nsk::Scratch dsa, drow;
+  double *pSA = nullptr, *pRow = nullptr;
+  if (int rc = copy_in(SA, op.s, n, ldsa, nc_sa, &pSA, dsa, st)) return rc;
+  if (int rc = copy_in(a_row, 1, n, 1, nc_row, &pRow, drow, st)) return rc;
+  if (int rc = nsk_downdate_row(h, j, scalar_sa, n, scalar_row, pRow, pSA, op.s, st)) return rc;
+  if (int rc = copy_out(SA, ldsa, pSA, op.s, n, nc_sa, st)) return rc;
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return nsk::OK;
+}
+
+int nsk_update_column_host(const nsk_operator* h, int scalar, int64_t m, const void* a_col, void* out) {
+  if (int rc = check_op(h)) return rc;
+  const Operator& op = *OP(h);
+  if (m < 0 || (m > 0 && !a_col) || !out) return nsk::fail(nsk::EINVAL_, "update_column: bad arguments");
+  cudaStream_t st = host_stream();
+  const int nc = scalar == NSK_COMPLEX ? 2 : 1, nc_out = out_ncomp(op, nc);
+  nsk::Scratch dcol, dout;
+  double* pCol = nullptr;
+  if (int rc = copy_in(a_col, m, 1, m > 0 ? m : 1, nc, &pCol, dcol, st)) return rc;
+  NSK_CUDA_OK(dout.alloc(sizeof(double) * op.s * nc_out, st));
+  if (int rc = nsk_update_column(h, scalar, m, pCol, dout.p, st)) return rc;
+  if (int rc = copy_out(out, op.s, dout.as<double>(), op.s, 1, nc_out, st)) return rc;
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return nsk::OK;
+}
+
 // ---- sketched total least squares (tls.cpp:97-113) ------------------------
 
 int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,

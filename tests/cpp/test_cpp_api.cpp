@@ -149,6 +149,70 @@ int main() {
     CHECK_THROWS_AS(residual_certificate(a, w3), std::invalid_argument);
   }
 
+  // Row and column updates (test_sketch.cpp: update_row keeps SA = S_eff A_eff,
+  // downdate_row removes a row's contribution, update_column appends S a_col).
+  {
+    const Index m = 300, n = 6, s = 40;
+    Matrix A = random_real(m, n, 21);
+    auto S = SketchOperator::draw(SketchKind::srdct, s, m, 31);
+    SketchedMatrix SA = apply(S, A);
+    Matrix row = random_real(1, n, 22);
+    SketchedMatrix up = update_row(SA, S, row);
+    CHECK(S.m_effective() == m + 1);
+    Matrix Aext(m + 1, n);
+    for (Index j = 0; j < n; ++j) {
+      for (Index i = 0; i < m; ++i) Aext(i, j) = A(i, j);
+      Aext(m, j) = row(0, j);
+    }
+    const SketchedMatrix ref = apply(S, Aext);  // the operator now spans m + 1 rows
+    CHECK(max_abs_diff(up.data, ref.data) < 1e-12 * fro(ref.data));
+    // downdate row 5: same as applying to A with row 5 zeroed
+    Matrix r5(1, n);
+    for (Index j = 0; j < n; ++j) r5(0, j) = Aext(5, j);
+    SketchedMatrix dn = downdate_row(up, S, 5, r5);
+    Matrix Az = Aext;
+    for (Index j = 0; j < n; ++j) Az(5, j) = 0.0;
+    CHECK(max_abs_diff(dn.data, apply(S, Az).data) < 1e-12 * fro(dn.data));
+    CHECK_THROWS_AS(downdate_row(dn, S, 5, r5), std::invalid_argument);     // already removed
+    CHECK_THROWS_AS(downdate_row(dn, S, m + 7, r5), std::out_of_range);
+    // update_column / downdate_column
+    Matrix col = random_real(m + 1, 1, 23);
+    SketchedMatrix wide = update_column(dn, S, col, 2);
+    CHECK(wide.data.cols() == n + 1);
+    Matrix colz = col;
+    colz(5, 0) = 0.0;
+    const SketchedMatrix sc = apply(S, colz);
+    double e = 0;
+    for (Index i = 0; i < s; ++i) e = std::max(e, std::abs(wide.data.at(i, 2) - sc.data.at(i, 0)));
+    CHECK(e < 1e-12 * fro(sc.data));
+    SketchedMatrix back = downdate_column(wide, 2);
+    CHECK(max_abs_diff(back.data, dn.data) == 0.0);
+    CHECK_THROWS_AS(downdate_column(wide, n + 1), std::out_of_range);
+    auto other = SketchOperator::draw(SketchKind::srdct, s, m, 32);
+    CHECK_THROWS_AS(update_row(SA, other, row), std::invalid_argument);  // operator ids differ
+  }
+  // Sketched TLS (test_tls.cpp): X recovers x_true at low noise; existence error at rank deficiency.
+  {
+    const Index m = 2000, n = 5, k = 1;
+    Matrix A = random_real(m, n, 41), xt = random_real(n, k, 42), noise = random_real(m, k, 43);
+    Matrix B(m, k);
+    for (Index i = 0; i < m; ++i) {
+      double v = 0;
+      for (Index j = 0; j < n; ++j) v += A(i, j) * xt(j, 0);
+      B(i, 0) = v + 1e-6 * noise(i, 0);
+    }
+    auto S = SketchOperator::draw(SketchKind::gaussian, 4 * (n + k), m, 44);
+    TlsOptions opt;
+    opt.certificate = true;
+    TlsSolution sol = tls_solve_sketched({A, B}, S, opt);
+    CHECK(sol.X.rows() == n && sol.X.cols() == k && sol.Vk.rows() == n + k);
+    CHECK(max_abs_diff(sol.X, xt) < 1e-4);
+    CHECK(sol.has_residual_certificate && sol.residual_certificate < 1e-3);
+    CHECK(sol.augmented_singular_values.size() == static_cast<size_t>(n + k));
+    Matrix A0 = A;  // rank-deficient A: the solvability check must fire
+    for (Index i = 0; i < m; ++i) A0(i, n - 1) = A0(i, 0);
+    CHECK_THROWS_AS(tls_solve_sketched({A0, B}, S), TlsExistenceError);
+  }
   if (failures) {
     std::fprintf(stderr, "%d check(s) failed\n", failures);
     return 1;
