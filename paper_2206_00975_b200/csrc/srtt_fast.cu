@@ -21,6 +21,7 @@
 // acc += w_m^{a (k1)} F_{k1}[a mod 1024] in registers.  Per-CTA partials
 // are reduced in fixed order.  Requires m % 4096 == 0; other sizes use the
 // direct evaluator.
+#include "fft32.cuh"
 #include "nsk_internal.hpp"
 
 namespace nsk {
@@ -65,59 +66,7 @@ constexpr int T = 32 * W;       // threads per CTA
 constexpr int UPAD = 32 * 33;   // per-warp buffer: 1024 values or a padded 32 x 33 transpose
 constexpr int REANCHOR = 32;    // exact twiddle every REANCHOR blocks
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-
-// v * e^{+2 pi i k/32}, k < 16 (compile-time k after unrolling).
-__device__ __forceinline__ double2 twmul32(double2 v, int k) {
-  // cos(pi k / 16), k = 0..8; sin(pi k/16) = cos(pi (8 - k)/16)
-  constexpr double C[9] = {1.0,
-                           0.98078528040323044912618223613,
-                           0.92387953251128675612818318939,
-                           0.83146961230254523707878837761,
-                           0.70710678118654752440084436210,
-                           0.55557023301960222474283081394,
-                           0.38268343236508977172845998403,
-                           0.19509032201612826784828486847,
-                           0.0};
-  if (k == 0) return v;
-  if (k == 8) return make_double2(-v.y, v.x);  // * i
-  const double c = k < 8 ? C[k] : -C[16 - k];
-  const double s = k < 8 ? C[8 - k] : C[k - 8];
-  return make_double2(fma(v.x, c, -v.y * s), fma(v.x, s, v.y * c));
-}
-
-__device__ __forceinline__ constexpr int brev5(int i) {
-  return ((i & 1) << 4) | ((i & 2) << 2) | (i & 4) | ((i & 8) >> 2) | ((i & 16) >> 4);
-}
-
-// In-register 32-point DFT, kernel e^{+2 pi i nk/32}, natural order in and out.
-__device__ __forceinline__ void dft32(double2 (&x)[32]) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const int r = brev5(i);
-    if (r > i) {
-      const double2 t = x[i];
-      x[i] = x[r];
-      x[r] = t;
-    }
-  }
-#pragma unroll
-  for (int stage = 1; stage <= 5; ++stage) {
-    const int half = 1 << (stage - 1);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {  // 16 butterflies per stage
-      const int j = e & (half - 1), i = (e >> (stage - 1)) << stage;
-      const double2 u = x[i + j];
-      const double2 t = twmul32(x[i + j + half], j << (5 - stage));
-      x[i + j] = cadd(u, t);
-      x[i + j + half] = csub(u, t);
-    }
-  }
-}
+using namespace fft;
 
 struct SrttParams {
   const double* A;

@@ -17,6 +17,8 @@
 
 namespace nsk {
 
+int srtt_tile_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                    double* SA, int64_t ldsa, cudaStream_t st);
 int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                     int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
 
@@ -110,6 +112,10 @@ int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
 
 int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                double* SA, int64_t ldsa, cudaStream_t st) {
+  // Tiled single-pass FFT (srtt_tile.cu) when the shape allows, else the
+  // strided FFT (srtt_fast.cu), else the direct evaluator.
+  const int rc = srtt_tile_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+  if (rc != NOTAPPLICABLE) return rc;
   return srtt_fast_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
 }
 
