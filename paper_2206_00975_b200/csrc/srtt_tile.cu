@@ -52,6 +52,10 @@ struct TileParams {
   double* part;    // [column][range][TNQ * TT] complex
 };
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
@@ -75,6 +79,7 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
   double2* U = sm2;                 // [TL][TROW]
   double2* tw = U + TL * TROW;      // w_1024^k, k < 1024
   double2* tw2 = tw + TL;           // srdct: w_2048^k, k < 512
+  uint32_t* SB = reinterpret_cast<uint32_t*>(tw2 + TL / 2);  // [ROWS] sign words of the tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t col = blockIdx.x / p.ranges, range = blockIdx.x % p.ranges;
   const int64_t t0 = range * p.per;
@@ -90,17 +95,18 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
     for (int k = threadIdx.x; k < TL / 2; k += TT) tw2[k] = unit(static_cast<uint64_t>(k), 2 * TL);
 
   // Output slots of this thread: g = frequency (srft f, srdct 2a+1) in w_N.
-  uint64_t g[TNQ];
-  int qidx[TNQ];
+  // Only the accumulators and the two twiddles stay in registers; the slot's
+  // frequency is re-read (L1) when it is needed (register budget of the FFT).
+  auto freq_of = [&](int q) -> uint64_t {
+    const int o = threadIdx.x + TT * q;
+    return o < p.nslots ? static_cast<uint64_t>(__ldg(p.freq + o)) : 0;
+  };
   double2 acc[TNQ], step[TNQ], base[TNQ];
 #pragma unroll
   for (int q = 0; q < TNQ; ++q) {
-    const int o = threadIdx.x + TT * q;
-    const uint64_t f = o < p.nslots ? static_cast<uint64_t>(p.freq[o]) : 0;
-    g[q] = KIND == 1 ? 2 * f + 1 : f;
-    qidx[q] = static_cast<int>(f & (TL - 1));
+    const uint64_t f = freq_of(q);
     acc[q] = make_double2(0.0, 0.0);
-    step[q] = unit(g[q] % N, N);  // w_N^g: one k1 column
+    step[q] = unit((KIND == 1 ? 2 * f + 1 : f) % N, N);  // w_N^g: one k1 column
   }
   const double c0 = sqrt(1.0 / static_cast<double>(p.m)), c1 = sqrt(2.0 / static_cast<double>(p.m));
 
@@ -112,6 +118,8 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
       const int k2 = c >> 2, ch = c & 3;
       cp_async16(U + k2 * TROW + ch, Acol + (K + p.P * k2) * NCIN + 2 * ch);
     }
+    for (int k2 = threadIdx.x; k2 < ROWS; k2 += TT)  // sign word of each row (bits K .. K + KT - 1)
+      cp_async4(SB + k2, p.sign_bits + ((static_cast<uint64_t>(K) + static_cast<uint64_t>(p.P) * k2) >> 5));
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     // ---- warp `warp`: in-place 1024-point FFT of sequence `warp` (column of U)
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
         double2 v = U[k2 * TROW + warp];
         if (NCIN == 1) {  // v = (u_e, u_o) of columns K + 2 warp, K + 2 warp + 1
           const uint64_t j = static_cast<uint64_t>(K + 2 * warp) + static_cast<uint64_t>(p.P) * k2;
-          const uint32_t bits = __ldg(p.sign_bits + (j >> 5)) >> (j & 31);
+          const uint32_t bits = SB[k2] >> (j & 31);
           if (!(bits & 1u)) v.x = -v.x;
           if (!(bits & 2u)) v.y = -v.y;
           if (KIND == 1) {
@@ -137,7 +145,7 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
           }
         } else {
           const uint64_t j = static_cast<uint64_t>(K + warp) + static_cast<uint64_t>(p.P) * k2;
-          if (!((__ldg(p.sign_bits + (j >> 5)) >> (j & 31)) & 1u)) v = make_double2(-v.x, -v.y);
+          if (!((SB[k2] >> (j & 31)) & 1u)) v = make_double2(-v.x, -v.y);
         }
         x[tt] = v;
       }
@@ -160,9 +168,10 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
     const bool anchor = ((t - t0) % TANCHOR) == 0;
 #pragma unroll
     for (int q = 0; q < TNQ; ++q) {
-      if (anchor) base[q] = unit(mulmod(g[q] % N, static_cast<uint64_t>(K) % N, N), N);  // w_N^{g K}
-      double2 w = base[q];
-      const int qi = qidx[q];
+      const uint64_t f = freq_of(q);
+      if (anchor) base[q] = unit(mulmod((KIND == 1 ? 2 * f + 1 : f) % N, static_cast<uint64_t>(K) % N, N), N);
+      double2 w = base[q];  // w_N^{g K}
+      const int qi = static_cast<int>(f & (TL - 1));
       if (NCIN == 1) {
         const int qm = KIND == 1 ? TL - 1 - qi : (TL - qi) & (TL - 1);
         const double2 st = step[q], st2 = cmul(st, st);
@@ -222,7 +231,7 @@ __global__ void srtt_tile_reduce(const double2* __restrict__ part, int64_t range
 
 template <int KIND, int NCIN>
 int launch_tile(const TileParams& p, int64_t ctas, cudaStream_t st) {
-  const size_t smem = sizeof(double2) * (TL * TROW + TL + (KIND == 1 ? TL / 2 : 0));
+  const size_t smem = sizeof(double2) * (TL * TROW + TL + TL / 2) + sizeof(uint32_t) * TL;
   auto kern = srtt_tile_kernel<KIND, NCIN>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   KernelTimer tm(st);
