@@ -286,8 +286,8 @@ def run_ours(args):
         achieved = byts / (kernel_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
-    roof.update({"kernel": {"srht": "srht_kernel", "srdct": "srtt main", "srft": "srtt main",
-                            "countsketch": "countsketch_kernel", "gaussian": "gaussian_sketch_kernel"}[kind],
+    roof.update({"kernel": {"srht": "srht_kernel", "srdct": "srtt_tile_kernel", "srft": "srtt_tile_kernel",
+                            "countsketch": "countsketch_owner_kernel", "gaussian": "gaussian_sketch_kernel"}[kind],
                  "kernel_ms": round(kernel_ms, 4), "algorithmic_bytes": byts, "algorithmic_flops": flops,
                  "traffic": traffic_from_profiles(kind)})
 
@@ -403,12 +403,25 @@ def e2e_sharded(nsk, S, Ah, k, kind, steps, rank, mloc):
 
 
 def traffic_from_profiles(kind):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if not os.path.exists(p):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    `ncu --set full` capture of this kind (profiles/r01_<kind>_ncu.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_{kind}_ncu.json")))
+    if not files:
         return None
-    with open(p) as f:
+    with open(files[-1]) as f:
         d = json.load(f)
-    return d.get(kind)
+    e = d[0] if isinstance(d, list) and d else d
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+    def nbytes(v):  # ncu_summary stores [value, unit]
+        if isinstance(v, (list, tuple)):
+            return float(v[0]) * scale.get(v[1], 1.0)
+        return float(v)
+    try:
+        return int(nbytes(e["dram__bytes_read.sum"]) + nbytes(e["dram__bytes_write.sum"]))
+    except (KeyError, TypeError, ValueError):
+        return None
 
 
 # ----------------------------------------------------------------------------- reference arm
