@@ -172,6 +172,24 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     // still landing; stage c-LAG is published once its group has completed.
     constexpr int LAG = T::STAGES - 2;
     const int pt = threadIdx.x - CONSUMERS;
+    // Real, 16-byte aligned A: this thread's cp.async slots are the same in
+    // every chunk up to the row offset k0, so their source offsets and k4
+    // destinations are computed once (the producers' register budget is the
+    // consumers'): a full chunk then costs ~3 instructions per 16-byte copy.
+    constexpr int PER = (BN * (T::BK / 2)) / PRODUCERS;
+    int64_t aoff[PER];
+    uint32_t soff[PER];
+    uint32_t okmask = 0;
+    if (NCOMP == 1 && VEC16) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int cc = pt + PRODUCERS * i, colx = cc / (T::BK / 2), r2 = (cc % (T::BK / 2)) * 2;
+        const int64_t q = q0 + colx;
+        aoff[i] = q < p.nq ? r2 + q * p.lda : 0;
+        soff[i] = static_cast<uint32_t>(k4(colx, r2, BN));
+        okmask |= (q < p.nq ? 1u : 0u) << i;
+      }
+    }
     for (int64_t c = 0; c < nchunks + LAG; ++c) {
       if (c < nchunks) {
         const int st = static_cast<int>(c % T::STAGES);
@@ -179,7 +197,16 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         double* sa = smem + st * T::STAGE;
         double* sb = sa + T::BM * T::BK;
         const int64_t k0 = kbeg + c * T::BK;
-        load_a_tile<BN, NCOMP, VEC16>(p, sb, k0, q0, pt);
+        if (NCOMP == 1 && VEC16 && k0 + T::BK <= p.mloc) {
+          const double* a0 = p.A + k0;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const bool ok = (okmask >> i) & 1u;
+            cp_async16(sb + soff[i], ok ? a0 + aoff[i] : p.A, ok ? 16 : 0);
+          }
+        } else {
+          load_a_tile<BN, NCOMP, VEC16>(p, sb, k0, q0, pt);
+        }
         cp_async_commit();
         gen_g_tile<BN>(p, sa, i0, k0, pt);
       }
