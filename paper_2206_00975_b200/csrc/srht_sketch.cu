@@ -189,7 +189,9 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
       const uint32_t v = sslot[q * 32 + lane];
       const uint32_t rlo = v & (L - 1), rhi = v >> LB;
       const double zz = z[rlo + (rlo >> 5)];
-      acc[q] += (__popc(rhi & jh) & 1) ? -zz : zz;
+      // (-1)^popc(r_hi & j_hi) applied to the sign bit (no selects)
+      const int par = static_cast<int>(__popc(rhi & jh) << 31);
+      acc[q] += __hiloint2double(__double2hiint(zz) ^ par, __double2loint(zz));
     }
     __syncwarp();
   }
