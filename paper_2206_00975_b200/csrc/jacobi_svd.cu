@@ -629,48 +629,69 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   if (const char* e = std::getenv("NSK_SVD_B")) b = std::atoi(e) >= 1 && std::atoi(e) <= 16 ? std::atoi(e) : b;
   while (b > 1 && sizeof(double) * 2 * b * 2 * n * NC > 200 * 1024) b >>= 1;
   const bool blocked = sizeof(double) * 2 * b * 2 * n * NC <= 200 * 1024 && std::getenv("NSK_SVD_PAIRS") == nullptr;
-  int crc = NOTAPPLICABLE;
-  if (n >= 2) crc = cluster_jacobi(NC, X, n, tol, counter, st);  // 2a. whole [R; I] in one cluster
-  if (crc != OK && crc != NOTAPPLICABLE) return crc;
-  if (crc == OK) {
-  } else if (n >= 2 && blocked) {  // 2b. block one-sided Jacobi on [R; I] through L2
-    BJParams P;
-    P.X = X;
-    P.n = n;
-    P.b = b;
-    P.B = (n + b - 1) / b;
-    P.B += P.B & 1;
-    P.tol = tol;
-    P.counter = counter;
-    void* args[] = {&P};
-    if (int rc = coop_launch(block_jacobi_kernel<NC>, P.B / 2, sizeof(double) * 2 * b * 2 * n * NC, args, st, BJT))
-      return rc;
-  } else if (n >= 2) {  // very large n: pairwise Jacobi with columns in L2
-    JacobiParams P;
-    P.X = X;
-    P.n = n;
-    P.N = n + (n & 1);
-    P.tol = tol;
-    P.counter = counter;
-    size_t smem = sizeof(double) * 2 * 2 * n * NC;
-    P.use_smem = smem <= 160 * 1024;
-    if (!P.use_smem) smem = 0;
-    void* args[] = {&P, &version};
-    if (int rc = coop_launch(jacobi_kernel<NC>, P.N / 2, smem, args, st)) return rc;
+  int* degenerate = version;  // flag of the preconditioned path (version[] is zero here)
+  auto solve = [&](bool precondition, int host[3]) -> int {
+    int crc = NOTAPPLICABLE;
+    if (n >= 2 && precondition) crc = cluster_svd_rt(NC, X, n, tol, counter, degenerate, st);  // 2a. QRCP + R'^H
+    if (crc != OK && crc != NOTAPPLICABLE) return crc;
+    host[2] = crc == OK;
+    if (crc != OK && n >= 2) crc = cluster_jacobi(NC, X, n, tol, counter, st);  // 2b. whole [R; I] in one cluster
+    if (crc != OK && crc != NOTAPPLICABLE) return crc;
+    if (crc == OK) {
+    } else if (n >= 2 && blocked) {  // 2c. block one-sided Jacobi on [R; I] through L2
+      BJParams P;
+      P.X = X;
+      P.n = n;
+      P.b = b;
+      P.B = (n + b - 1) / b;
+      P.B += P.B & 1;
+      P.tol = tol;
+      P.counter = counter;
+      void* args[] = {&P};
+      if (int rc = coop_launch(block_jacobi_kernel<NC>, P.B / 2, sizeof(double) * 2 * b * 2 * n * NC, args, st, BJT))
+        return rc;
+    } else if (n >= 2) {  // very large n: pairwise Jacobi with columns in L2
+      JacobiParams P;
+      P.X = X;
+      P.n = n;
+      P.N = n + (n & 1);
+      P.tol = tol;
+      P.counter = counter;
+      size_t smem = sizeof(double) * 2 * 2 * n * NC;
+      P.use_smem = smem <= 160 * 1024;
+      if (!P.use_smem) smem = 0;
+      void* args[] = {&P, &version};
+      if (int rc = coop_launch(jacobi_kernel<NC>, P.N / 2, smem, args, st)) return rc;
+    }
+    norms_kernel<NC><<<static_cast<unsigned>(n), JT, 0, st>>>(X, n, norms);
+    NSK_CUDA_OK(cudaGetLastError());
+    NSK_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    order_kernel<NC><<<1, 256, sizeof(int) * n, st>>>(X, n, k, W, ldw, sigma, norms, bad);
+    count_launch(2);
+    NSK_CUDA_OK(cudaGetLastError());
+    // Convergence, NaN and degeneracy checks need host visibility of three ints.
+    int flag = 0;
+    NSK_CUDA_OK(cudaMemcpyAsync(&host[0], counter + MAX_SWEEPS, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NSK_CUDA_OK(cudaMemcpyAsync(&host[1], bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (host[2]) NSK_CUDA_OK(cudaMemcpyAsync(&flag, degenerate, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NSK_CUDA_OK(cudaStreamSynchronize(st));
+    if (flag) host[2] = -1;
+    return OK;
+  };
+  int host[3] = {0, 0, 0};
+  if (int rc = solve(true, host)) return rc;
+  if (host[2] < 0) {  // exactly singular R: What undefined, rerun on [R; I]
+    NSK_CUDA_OK(cudaMemsetAsync(version, 0, sizeof(int) * n, st));
+    int64_t blocks = (2 * n * n * NC + 255) / 256;
+    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+    build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, X);
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+    if (int rc = solve(false, host)) return rc;
   }
-  norms_kernel<NC><<<static_cast<unsigned>(n), JT, 0, st>>>(X, n, norms);
-  NSK_CUDA_OK(cudaGetLastError());
-  NSK_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-  order_kernel<NC><<<1, 256, sizeof(int) * n, st>>>(X, n, k, W, ldw, sigma, norms, bad);
-  count_launch(2);
-  NSK_CUDA_OK(cudaGetLastError());
-  // Convergence and NaN checks need host visibility of two ints.
-  int host[2] = {0, 0};
-  NSK_CUDA_OK(cudaMemcpyAsync(&host[0], counter + MAX_SWEEPS, sizeof(int), cudaMemcpyDeviceToHost, st));
-  NSK_CUDA_OK(cudaMemcpyAsync(&host[1], bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-  NSK_CUDA_OK(cudaStreamSynchronize(st));
-  if (std::getenv("NSK_SVD_DEBUG")) std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d\n",
-                                                 static_cast<long long>(s), static_cast<long long>(n), b, host[0]);
+  if (std::getenv("NSK_SVD_DEBUG")) std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d path=%d\n",
+                                                 static_cast<long long>(s), static_cast<long long>(n), b, host[0],
+                                                 host[2]);
   if (n >= 2 && host[0] >= MAX_SWEEPS) return fail(ENOCONV, "svd: one-sided Jacobi did not converge");
   if (host[1]) return fail(ENOCONV, "svd: non-finite singular values (input contains NaN/Inf)");
   return OK;

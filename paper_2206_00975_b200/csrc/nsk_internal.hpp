@@ -118,6 +118,10 @@ int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, con
 // One-sided Jacobi on [R; I] (2n x n, ld 2n) inside one thread-block cluster
 // (cluster_jacobi.cu); NOTAPPLICABLE when it does not fit one cluster.
 int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cudaStream_t st);
+// QRCP of R + one-sided Jacobi on R'^H in one cluster (cluster_jacobi.cu); writes
+// the same [W; V] layout.  NOTAPPLICABLE when it does not fit; *degenerate
+// (device) is raised when R is exactly singular and the caller must rerun.
+int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, int* degenerate, cudaStream_t st);
 // One-sided Jacobi SVD of SA (s x n, ncomp = 1 real / 2 complex interleaved).
 // Writes the trailing k right singular vectors and all n singular values
 // (device, non-increasing).  Returns ENOCONV if the sweep limit is hit.

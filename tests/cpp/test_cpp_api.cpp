@@ -209,8 +209,8 @@ int main() {
     CHECK(max_abs_diff(sol.X, xt) < 1e-4);
     CHECK(sol.has_residual_certificate && sol.residual_certificate < 1e-3);
     CHECK(sol.augmented_singular_values.size() == static_cast<size_t>(n + k));
-    Matrix A0 = A;  // rank-deficient A: the solvability check must fire
-    for (Index i = 0; i < m; ++i) A0(i, n - 1) = A0(i, 0);
+    Matrix A0 = A;  // rank-deficient A (zero column): sigma_n(SA) = 0, the solvability check must fire
+    for (Index i = 0; i < m; ++i) A0(i, n - 1) = 0.0;
     CHECK_THROWS_AS(tls_solve_sketched({A0, B}, S), TlsExistenceError);
   }
   if (failures) {
