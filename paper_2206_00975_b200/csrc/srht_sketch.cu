@@ -104,22 +104,30 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
   int seg = 0;
-  int64_t cur_col = it < end ? it / p.nb : -1;
+  // (col, blk) of item it, advanced incrementally (no 64-bit divisions in the loop).
+  int64_t col = it < end ? it / p.nb : -1, blk = it < end ? it - col * p.nb : 0;
+  int64_t cur_col = col;
   // Lane holds rows lane + 32 t (coalesced 256 B per load), streamed once.  The
-  // next block is issued into the same registers as soon as the current one has
-  // been written to shared memory, so its loads overlap the gather phase.
+  // next block and its sign-mask words are issued into the same registers as
+  // soon as the current one has been written to shared memory, so the loads
+  // overlap the gather phase.
   double x[T];
+  uint32_t smk[T / 32];
   if (it < end) {
-    const int64_t col = it / p.nb, blk = it - col * p.nb;
     const double* a = p.A + col * p.lda + blk * L + lane;
 #pragma unroll
     for (int t = 0; t < T; ++t) x[t] = __ldcs(a + 32 * t);
+#pragma unroll
+    for (int h = 0; h < T / 32; ++h) smk[h] = __ldg(p.mask + ((p.jhi0 + blk) * (T / 32) + h) * 32 + lane);
   }
 
   for (; it < end; ++it) {
-    const int64_t col = it / p.nb, blk = it - col * p.nb;
     if (p.pf > 0 && lane == 0 && it + p.pf < end) {  // stage block it + pf in L2 (one bulk prefetch)
-      const int64_t c3 = (it + p.pf) / p.nb, b3 = (it + p.pf) - c3 * p.nb;
+      int64_t c3 = col, b3 = blk + p.pf;
+      while (b3 >= p.nb) {
+        b3 -= p.nb;
+        ++c3;
+      }
       const double* a3 = p.A + c3 * p.lda + b3 * L;
       if ((reinterpret_cast<uintptr_t>(a3) & 15) == 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a3), "r"(static_cast<unsigned>(L * 8))
@@ -139,7 +147,7 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
     // D: flip the sign where the stream bit is 0 (rng.hpp:57); masks are per 1024 rows.
 #pragma unroll
     for (int h = 0; h < T / 32; ++h) {
-      const uint32_t sm = __ldg(p.mask + (jhi * (T / 32) + h) * 32 + lane);
+      const uint32_t sm = smk[h];
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
         const uint32_t flip = ((~sm) >> t) & 1u;
@@ -175,11 +183,17 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
     for (int w = 0; w < T / 32; ++w)
 #pragma unroll
       for (int u = 0; u < 32; ++u) z[u + 33 * lane + 1056 * w] = x[w * 32 + u];
+    int64_t c2 = col, b2 = blk + 1;
+    if (b2 == p.nb) {
+      b2 = 0;
+      ++c2;
+    }
     if (it + 1 < end) {  // prefetch the next block into the now free registers
-      const int64_t c2 = (it + 1) / p.nb, b2 = (it + 1) - c2 * p.nb;
       const double* a2 = p.A + c2 * p.lda + b2 * L + lane;
 #pragma unroll
       for (int t = 0; t < T; ++t) x[t] = __ldcs(a2 + 32 * t);
+#pragma unroll
+      for (int h = 0; h < T / 32; ++h) smk[h] = __ldg(p.mask + ((p.jhi0 + b2) * (T / 32) + h) * 32 + lane);
     }
     __syncwarp();
     // Sampled second stage: acc += (-1)^popc(r_hi & j_hi) Z[r_lo].
@@ -194,6 +208,8 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
       acc[q] += __hiloint2double(__double2hiint(zz) ^ par, __double2loint(zz));
     }
     __syncwarp();
+    col = c2;
+    blk = b2;
   }
   if (cur_col >= 0) {
     double* P = p.P + (warp * 2 + seg) * (NQ * 32);
@@ -202,24 +218,34 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
   }
 }
 
-// SA[row(t), c] = scale * sum over the warps that touched column c, in warp order.
-__global__ void srht_reduce(const double* __restrict__ P, int64_t nb, int64_t per, int64_t n, int nslots,
-                            int slot_stride, const int32_t* __restrict__ row_of_slot, double scale,
-                            double* __restrict__ SA, int64_t ldsa, int slot_base) {
-  const int64_t total = n * nslots;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t c = e / nslots;
-    const int t = static_cast<int>(e % nslots);
-    const int64_t first = c * nb, last = (c + 1) * nb - 1;
-    const int64_t w0 = first / per, w1 = last / per;
-    double v = 0.0;
+// SA[row(t), c] = scale * sum over the warps that touched column c, in warp
+// order.  One CTA per column: the warp range and segments are uniform, the
+// threads walk the slots (coalesced partial reads, several sums in flight).
+__global__ void __launch_bounds__(256) srht_reduce(const double* __restrict__ P, int64_t nb, int64_t per,
+                                                   int nslots, int slot_stride,
+                                                   const int32_t* __restrict__ row_of_slot, double scale,
+                                                   double* __restrict__ SA, int64_t ldsa) {
+  const int64_t c = blockIdx.x;
+  const int64_t w0 = (c * nb) / per, w1 = ((c + 1) * nb - 1) / per;
+  constexpr int U = 4;
+  for (int t0 = threadIdx.x; t0 < nslots; t0 += 256 * U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = 0.0;
     for (int64_t w = w0; w <= w1; ++w) {
-      const int64_t wstart = w * per;
-      const int seg = (wstart / nb == c) ? 0 : 1;
-      v += P[(w * 2 + seg) * slot_stride + t];
+      const int seg = w * per >= c * nb ? 0 : 1;  // the warp's first item lies in column c
+      const double* Pw = P + (w * 2 + seg) * slot_stride;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + 256 * u;
+        if (t < nslots) v[u] += Pw[t];
+      }
     }
-    SA[row_of_slot[slot_base + t] + c * ldsa] = scale * v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + 256 * u;
+      if (t < nslots) SA[row_of_slot[t] + c * ldsa] = scale * v[u];
+    }
   }
 }
 
@@ -303,15 +329,12 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
     NSK_CUDA_OK(part.alloc(sizeof(double) * warps * 2 * NQ * 32, st));
     const char* pfe = std::getenv("NSK_SRHT_PF");
     SrhtParams p{A, lda, n, nb, rows.row0 / L, total, per, tb->sign_mask, tb->srht_slot + base, ns,
-                 part.as<double>(), pfe ? std::atoi(pfe) : 1};
+                 part.as<double>(), pfe ? std::atoi(pfe) : 2};
     int rc = NQ == 8 ? launch_srht<8>(p, warps, lb, st)
                      : (NQ == 16 ? launch_srht<16>(p, warps, lb, st) : launch_srht<32>(p, warps, lb, st));
     if (rc != OK) return rc;
-    int64_t blocks = (n * ns + 255) / 256;
-    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-    srht_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double>(), nb, per, n, ns, NQ * 32,
-                                                               tb->srht_row, scale, SA, ldsa,
-                                                               static_cast<int>(base));
+    srht_reduce<<<static_cast<unsigned>(n), 256, 0, st>>>(part.as<double>(), nb, per, ns, NQ * 32,
+                                                          tb->srht_row + base, scale, SA, ldsa);
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
   }
