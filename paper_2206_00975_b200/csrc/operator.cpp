@@ -227,6 +227,21 @@ const DeviceTables* Operator::tables() const {
     }  // else: the streaming kernel covers every tile
   }
   if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return nullptr;
+  if ((kind == SRFT || kind == SRDCT) && !idx.empty()) {
+    // Slots sorted by FFT bin (idx mod 1024) for the tile kernel (srtt_tile.cu).
+    std::vector<int32_t> order(idx.size());
+    for (size_t r = 0; r < idx.size(); ++r) order[r] = static_cast<int32_t>(r);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return (idx[static_cast<size_t>(a)] & 1023) < (idx[static_cast<size_t>(b)] & 1023);
+    });
+    std::vector<int64_t> freq(idx.size());
+    for (size_t r = 0; r < idx.size(); ++r) freq[r] = idx[static_cast<size_t>(order[r])];
+    if (up(reinterpret_cast<void**>(&t.srtt_freq), freq.data(), freq.size() * 8) != cudaSuccess ||
+        up(reinterpret_cast<void**>(&t.srtt_row), order.data(), order.size() * 4) != cudaSuccess) {
+      cuda_fail(cudaGetLastError(), "srtt slot table upload");
+      return nullptr;
+    }
+  }
   dev.push_back(t);
   return &dev.back();
 }
@@ -275,6 +290,8 @@ Operator::~Operator() {
     if (t.sign_mask) cudaFree(t.sign_mask);
     if (t.cs_table) cudaFree(t.cs_table);
     if (t.sign_bits) cudaFree(t.sign_bits);
+    if (t.srtt_freq) cudaFree(t.srtt_freq);
+    if (t.srtt_row) cudaFree(t.srtt_row);
     if (t.cs_ent) cudaFree(t.cs_ent);
     if (t.cs_cnt) cudaFree(t.cs_cnt);
   }

@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
 // srdct the real part (the pair unpacking's factor 1/2 folded into scale).
 template <int KIND>
 __global__ void srtt_tile_reduce(const double2* __restrict__ part, int64_t ranges, int64_t n, int nslots, int stride,
-                                 int slot_base, double scale, double* __restrict__ SA, int64_t ldsa) {
+                                 const int32_t* __restrict__ row_of_slot, double scale, double* __restrict__ SA,
+                                 int64_t ldsa) {
   const int64_t total = n * nslots;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -219,7 +220,7 @@ __global__ void srtt_tile_reduce(const double2* __restrict__ part, int64_t range
       v.x += x.x;
       v.y += x.y;
     }
-    const int64_t row = slot_base + o;
+    const int64_t row = row_of_slot[o];
     if (KIND == 0) {
       SA[2 * (row + c * ldsa)] = scale * v.x;
       SA[2 * (row + c * ldsa) + 1] = scale * v.y;
@@ -259,11 +260,10 @@ int srtt_tile_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
   if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (ncomp == 1 && (lda & 1) != 0)) return NOTAPPLICABLE;
   const DeviceTables* tb = op.tables();
   if (!tb || !tb->sign_bits) return ECUDA;
-  std::vector<int64_t> freq(static_cast<size_t>(s));
-  for (int64_t r = 0; r < s; ++r) freq[static_cast<size_t>(r)] = op.idx[static_cast<size_t>(r)];
-  Scratch dfreq;
-  NSK_CUDA_OK(dfreq.alloc(sizeof(int64_t) * s, st));
-  NSK_CUDA_OK(cudaMemcpyAsync(dfreq.p, freq.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, st));
+  // Slots sorted by their FFT bin (idx mod TL, operator tables): the threads
+  // of a warp then gather neighbouring rows of the tile (conflict-free in the
+  // padded layout); the reduce scatters slot t to output row srtt_row[t].
+  if (!tb->srtt_freq || !tb->srtt_row) return ECUDA;
   const int64_t tiles = P / KT;
   const int64_t target = 2L * sm_count();
   int64_t ranges = (target + n - 1) / n;
@@ -278,7 +278,7 @@ int srtt_tile_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
     const int ns = static_cast<int>((s - base) < TNQ * TT ? (s - base) : TNQ * TT);
     Scratch part;
     NSK_CUDA_OK(part.alloc(sizeof(double2) * n * ranges * TNQ * TT, st));
-    TileParams p{A, lda, m, n, P, tiles, ranges, per, tb->sign_bits, dfreq.as<int64_t>() + base, ns,
+    TileParams p{A, lda, m, n, P, tiles, ranges, per, tb->sign_bits, tb->srtt_freq + base, ns,
                  part.as<double>()};
     const int64_t ctas = n * ranges;
     int rc = kind == 0 ? (ncomp == 1 ? launch_tile<0, 1>(p, ctas, st) : launch_tile<0, 2>(p, ctas, st))
@@ -288,10 +288,10 @@ int srtt_tile_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
     if (kind == 0)
       srtt_tile_reduce<0><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-          reinterpret_cast<const double2*>(part.p), ranges, n, ns, TNQ * TT, static_cast<int>(base), scale, SA, ldsa);
+          reinterpret_cast<const double2*>(part.p), ranges, n, ns, TNQ * TT, tb->srtt_row + base, scale, SA, ldsa);
     else
       srtt_tile_reduce<1><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-          reinterpret_cast<const double2*>(part.p), ranges, n, ns, TNQ * TT, static_cast<int>(base), scale, SA, ldsa);
+          reinterpret_cast<const double2*>(part.p), ranges, n, ns, TNQ * TT, tb->srtt_row + base, scale, SA, ldsa);
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
   }
