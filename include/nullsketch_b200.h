@@ -216,6 +216,21 @@ int nsk_tls_solve_sketched_host(const nsk_operator* op, int scalar, int64_t m, i
                                 int allow_marginal, void* X, int64_t ldx, void* Vk, int64_t ldv,
                                 double* sigma, double* info);
 
+/* ---- exact total least squares (tls.hpp:59-61, tls.cpp:83-95) ----------- */
+
+/* Same outputs as nsk_tls_solve_sketched, from the thin QR of [A | B] (no
+ * sketch): R = shifted CholeskyQR3 factor on the device (cuBLAS level-3
+ * Gram products and triangular solves), then the SVDs of the (n+k)^2
+ * triangle; sigma = singular values of [A|B], info[2] = sigma_n(A).
+ * Replaces tls_solve_exact (tls.cpp:83).  NSK_ENOCONV on a Cholesky
+ * breakdown (NaN/Inf input). */
+int nsk_tls_solve_exact(int scalar, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                        int64_t ldb, double cond_limit, int allow_marginal, void* X, int64_t ldx, void* Vk,
+                        int64_t ldv, double* sigma, double* info, void* stream);
+int nsk_tls_solve_exact_host(int scalar, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                             const void* B, int64_t ldb, double cond_limit, int allow_marginal, void* X,
+                             int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info);
+
 /* ---- instrumentation (bench.py; no effect on results) ------------------- */
 
 /* Number of CUDA kernels this library has launched in this process. */

@@ -15,6 +15,7 @@
 //   update_row / downdate_row (sketch.hpp:90-109) same (S mutated, SA returned)
 //   update_column / downdate_column             same
 //   tls_solve_sketched(p, S, options) (tls.hpp) same, TlsExistenceError / TlsConditionError
+//   tls_solve_exact(p, options), tls_error_metrics(exact, sk) (tls.hpp:60,73)
 //   std::invalid_argument / std::out_of_range   same (from NSK_EINVAL / NSK_ERANGE)
 //   SvdConvergenceError                         SvdConvergenceError (NSK_ENOCONV)
 //
@@ -24,6 +25,8 @@
 // available to callers that keep A resident in HBM.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <stdexcept>
@@ -378,6 +381,18 @@ class TlsConditionError : public std::runtime_error {
   double cond_;
 };
 
+namespace detail {
+// ||[A|B] Vk||_F, one pass on the device (tls.cpp:55-58).
+inline void certify(TlsSolution& r, const Matrix& A, const Matrix& B) {
+  const Index m = A.rows(), n = A.cols(), k = B.cols();
+  Matrix AB(m, n + k, A.kind());
+  for (Index j = 0; j < n + k; ++j)
+    for (Index i = 0; i < m; ++i) AB.set(i, j, j < n ? A.at(i, j) : B.at(i, j - n));
+  r.residual_certificate = residual_certificate(AB, r.Vk);
+  r.has_residual_certificate = true;
+}
+}  // namespace detail
+
 // tls.hpp: tls_solve_sketched -- the trailing subspace comes from S [A|B].
 inline TlsSolution tls_solve_sketched(const TlsProblem& p, const SketchOperator& S, const TlsOptions& options = {}) {
   const Index m = p.A.rows(), n = p.A.cols(), k = p.B.cols();
@@ -399,14 +414,129 @@ inline TlsSolution tls_solve_sketched(const TlsProblem& p, const SketchOperator&
   check(rc);
   r.tls_residual = info[0];
   r.cond_Vk2 = info[1];
-  if (options.certificate) {
-    Matrix AB(m, n + k, A.kind());
-    for (Index j = 0; j < n + k; ++j)
-      for (Index i = 0; i < m; ++i) AB.set(i, j, j < n ? A.at(i, j) : B.at(i, j - n));
-    r.residual_certificate = residual_certificate(AB, r.Vk);
-    r.has_residual_certificate = true;
-  }
+  if (options.certificate) detail::certify(r, A, B);
   return r;
+}
+
+// tls.hpp: tls_solve_exact -- thin QR of [A|B] on the device (shifted
+// CholeskyQR3), then the SVDs of the (n+k)^2 triangle (tls.cpp:83-95).
+inline TlsSolution tls_solve_exact(const TlsProblem& p, const TlsOptions& options = {}) {
+  const Index m = p.A.rows(), n = p.A.cols(), k = p.B.cols();
+  if (p.B.rows() != m) throw std::invalid_argument("tls: A and B row counts differ");
+  const bool cplx = !p.A.is_real() || !p.B.is_real();
+  const Matrix A = cplx ? detail::promote(p.A) : p.A, B = cplx ? detail::promote(p.B) : p.B;
+  const ScalarKind ok = cplx ? ScalarKind::complex : ScalarKind::real;
+  TlsSolution r;
+  r.X = Matrix(n, k, ok);
+  r.Vk = Matrix(n + k, k, ok);
+  r.augmented_singular_values.resize(static_cast<size_t>(n + k));
+  double info[4] = {0, 0, 0, 0};
+  const int rc = nsk_tls_solve_exact_host(static_cast<int>(A.kind()), m, n, k, A.data(), m > 0 ? m : 1, B.data(),
+                                          m > 0 ? m : 1, options.cond_limit, options.allow_marginal ? 1 : 0,
+                                          r.X.data(), n, r.Vk.data(), n + k, r.augmented_singular_values.data(), info);
+  if (rc == NSK_ETLS_EXISTENCE) throw TlsExistenceError(info[2], info[3]);
+  if (rc == NSK_ETLS_CONDITION) throw TlsConditionError(info[1]);
+  check(rc);
+  r.tls_residual = info[0];
+  r.cond_Vk2 = info[1];
+  if (options.certificate) detail::certify(r, A, B);
+  return r;
+}
+
+// ---- tls_error_metrics (tls.cpp:115-131), small host-side linear algebra -----
+
+struct TlsErrorMetrics {
+  double rel_err = 0.0;  // ||X - Xs||_2 / ||X||_2
+  double sin_X = 0.0;    // spectral sin between the column spans of X and Xs
+  double sin_Vk = 0.0;   // spectral sin between the trailing subspaces
+};
+
+namespace detail {
+using cd = std::complex<double>;
+using Dense = std::vector<std::vector<cd>>;  // column list
+
+inline Dense columns(const Matrix& a) {
+  Dense c(static_cast<size_t>(a.cols()), std::vector<cd>(static_cast<size_t>(a.rows())));
+  for (Index j = 0; j < a.cols(); ++j)
+    for (Index i = 0; i < a.rows(); ++i) c[static_cast<size_t>(j)][static_cast<size_t>(i)] = a.at(i, j);
+  return c;
+}
+
+inline cd dot(const std::vector<cd>& x, const std::vector<cd>& y) {  // x^H y
+  cd s = 0.0;
+  for (size_t i = 0; i < x.size(); ++i) s += std::conj(x[i]) * y[i];
+  return s;
+}
+
+// Largest singular value of a small column list (one-sided Jacobi, host).
+inline double spectral_norm(Dense c) {
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rotated = false;
+    for (size_t p = 0; p + 1 < c.size(); ++p)
+      for (size_t q = p + 1; q < c.size(); ++q) {
+        const double a = std::real(dot(c[p], c[p])), b = std::real(dot(c[q], c[q]));
+        const cd g = dot(c[p], c[q]);
+        if (std::abs(g) <= 1e-15 * std::sqrt(a * b) || std::abs(g) == 0.0) continue;
+        rotated = true;
+        const double zeta = (b - a) / (2.0 * std::abs(g));
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = cs * t;
+        const cd ph = std::conj(g) / std::abs(g);
+        for (size_t i = 0; i < c[p].size(); ++i) {
+          const cd up = c[p][i], uq = c[q][i] * ph;
+          c[p][i] = cs * up - sn * uq;
+          c[q][i] = sn * up + cs * uq;
+        }
+      }
+    if (!rotated) break;
+  }
+  double best = 0.0;
+  for (auto& x : c) best = std::max(best, std::sqrt(std::real(dot(x, x))));
+  return best;
+}
+
+inline Dense orthonormal(Dense c) {  // modified Gram-Schmidt, twice
+  for (int pass = 0; pass < 2; ++pass)
+    for (size_t j = 0; j < c.size(); ++j) {
+      for (size_t i = 0; i < j; ++i) {
+        const cd r = dot(c[i], c[j]);
+        for (size_t e = 0; e < c[j].size(); ++e) c[j][e] -= r * c[i][e];
+      }
+      const double nr = std::sqrt(std::real(dot(c[j], c[j])));
+      if (nr > 0)
+        for (auto& v : c[j]) v /= nr;
+    }
+  return c;
+}
+
+// Largest sine between two orthonormal column spans: ||(I - U U^H) V||_2 (kernels.cpp:153-167).
+inline double sin_theta(const Dense& u, const Dense& v) {
+  const Dense& big = u.size() >= v.size() ? u : v;
+  Dense small = u.size() >= v.size() ? v : u;
+  if (big.empty() || small.empty()) return 0.0;
+  for (auto& x : small)
+    for (const auto& b : big) {
+      const cd r = dot(b, x);
+      for (size_t e = 0; e < x.size(); ++e) x[e] -= r * b[e];
+    }
+  return std::min(1.0, spectral_norm(small));
+}
+}  // namespace detail
+
+inline TlsErrorMetrics tls_error_metrics(const TlsSolution& exact, const TlsSolution& sk) {
+  if (exact.X.rows() != sk.X.rows() || exact.X.cols() != sk.X.cols())
+    throw std::invalid_argument("tls_error_metrics: X shapes differ");
+  const detail::Dense x = detail::columns(exact.X), xs = detail::columns(sk.X);
+  const double xn = detail::spectral_norm(x);
+  if (xn == 0.0) throw std::invalid_argument("tls_error_metrics: exact X is zero; rel_err undefined");
+  detail::Dense d = x;
+  for (size_t j = 0; j < d.size(); ++j)
+    for (size_t i = 0; i < d[j].size(); ++i) d[j][i] -= xs[j][i];
+  TlsErrorMetrics m;
+  m.rel_err = detail::spectral_norm(d) / xn;
+  m.sin_X = detail::sin_theta(detail::orthonormal(x), detail::orthonormal(xs));
+  m.sin_Vk = detail::sin_theta(detail::columns(exact.Vk), detail::columns(sk.Vk));
+  return m;
 }
 
 }  // namespace nullsketch_b200

@@ -484,6 +484,30 @@ def tls_solve_sketched(A, B, op, cond_limit=1e12, allow_marginal=False):
     return X, vk, sv, math.sqrt(np.sum(sv[n:] ** 2)), cond
 
 
+def tls_solve_exact(A, B, cond_limit=1e12, allow_marginal=False):
+    """Exact TLS (tls.cpp:83-95): Householder thin QR of [A|B] (LAPACK), SVD of R,
+    sigma_n(A) from the leading n columns of R; returns (X, Vk, sigma, residual, cond)."""
+    A = np.asarray(A)
+    B = np.asarray(B).reshape(A.shape[0], -1)
+    m, n = A.shape
+    k = B.shape[1]
+    if k < 1 or n < k or m < n + k:
+        raise ValueError("tls: bad shape")
+    R = np.linalg.qr(np.concatenate([A, B], axis=1), mode="r")
+    _, sv, v = svd(R)
+    sa = np.linalg.svd(R[:, :n], compute_uv=False)
+    if not (sa[n - 1] > sv[n]) and not allow_marginal:
+        raise RuntimeError("tls: solution existence check failed")
+    vk = v[:, n:n + k]
+    v1, v2 = vk[:n], vk[n:]
+    s2 = np.linalg.svd(v2, compute_uv=False)
+    cond = np.inf if s2[-1] == 0 else s2[0] / s2[-1]
+    if not (cond <= cond_limit):
+        raise RuntimeError("tls: V_k2 ill conditioned")
+    X = np.linalg.solve(v2.T, -v1.T).T
+    return X, vk, sv, math.sqrt(np.sum(sv[n:] ** 2)), cond
+
+
 def doubles(seed, stream, first, count):
     """next_double #first.. of a stream (rng.hpp:36-39): (u64 >> 11) * 2^-53, u64 = words (2i+1 : 2i)."""
     w = words(seed, stream, 2 * first, 2 * count).astype(np.uint64).reshape(count, 2)

@@ -8,9 +8,9 @@ C ABI declared in include/nullsketch_b200.h.
 from .sketch import (KINDS, NullspaceResult, SketchedMatrix, SketchOperator, SvdConvergenceError, TlsConditionError,
                      TlsExistenceError, TlsSolution, apply, apply_shard, default_sketch_size, downdate_column,
                      downdate_row, residual_certificate, solve_k, solve_tol, svd_trailing, tls_solve_sketched,
-                     update_column, update_row)
+                     tls_solve_exact, tls_error_metrics, TlsErrorMetrics, update_column, update_row)
 
 __all__ = ["KINDS", "NullspaceResult", "SketchedMatrix", "SketchOperator", "SvdConvergenceError", "TlsConditionError",
            "TlsExistenceError", "TlsSolution", "apply", "apply_shard", "default_sketch_size", "downdate_column",
            "downdate_row", "residual_certificate", "solve_k", "solve_tol", "svd_trailing", "tls_solve_sketched",
-           "update_column", "update_row"]
+           "tls_solve_exact", "tls_error_metrics", "TlsErrorMetrics", "update_column", "update_row"]

@@ -26,7 +26,7 @@ EXPORTS = (
     "nsk_apply_shard", "nsk_svd_trailing", "nsk_solve_k", "nsk_solve_tol", "nsk_residual_fro",
     "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_residual_fro_host", "nsk_kernel_launches",
     "nsk_timing_enable", "nsk_timing_collect", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
-    "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_update_row_host",
+    "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_tls_solve_exact", "nsk_tls_solve_exact_host", "nsk_update_row_host",
     "nsk_downdate_row_host", "nsk_update_column_host",
 )
 
@@ -88,6 +88,10 @@ def load():
                                          vp, i64, vp, dp, vp]
     L.nsk_tls_solve_sketched_host.argtypes = [vp, c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp,
                                               i64, vp, i64, vp, dp]
+    L.nsk_tls_solve_exact.argtypes = [c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp, i64, vp,
+                                      i64, vp, dp, vp]
+    L.nsk_tls_solve_exact_host.argtypes = [c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp, i64,
+                                           vp, i64, vp, dp]
     L.nsk_kernel_launches.restype = i64
     L.nsk_timing_enable.argtypes = [c_int]
     L.nsk_timing_enable.restype = None

@@ -22,7 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 SOURCES = ["operator.cpp", "capi.cpp", "gaussian_sketch.cu", "srht_sketch.cu", "countsketch.cu",
            "srtt_sketch.cu", "srtt_fast.cu", "jacobi_svd.cu", "residual.cu", "instrument.cpp", "updates.cu",
-           "cs_schedule.cpp", "cluster_jacobi.cu", "srtt_tile.cu"]
+           "cs_schedule.cpp", "cluster_jacobi.cu", "srtt_tile.cu", "tall_qr.cu"]
 
 
 def _deps():
@@ -56,7 +56,7 @@ def build(force=False, verbose=False):
     for obj, err in results:
         if verbose and err.strip():
             print(err, file=sys.stderr)
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *[o for o, _ in results]]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *[o for o, _ in results], "-lcublas"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -146,14 +146,6 @@ cudaStream_t host_stream() {
   if (!st || dev != cur) {
     cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     dev = cur;
-    // Host entry points stage A in stream-ordered scratch: keep freed blocks
-    // in the device's default pool instead of unmapping them at every
-    // synchronisation, so repeated calls do not re-map gigabytes of HBM.
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
   }
   return st;
 }
@@ -598,6 +590,49 @@ int nsk_update_column_host(const nsk_operator* h, int scalar, int64_t m, const v
   return nsk::OK;
 }
 
+// ---- total least squares (tls.cpp:26-62) -----------------------------------
+// Shared tail of the sketched and exact solvers: M (rows x (n + k), ld ldm) is
+// S [A|B] or the R factor of [A|B].  Trailing k right singular vectors and
+// the full spectrum of M, sigma_n of its leading n columns, the existence
+// check (tls.cpp:46-50), the V_k2 condition estimate and X = -V_k1 V_k2^{-1}.
+static int tls_finish(int nc, int64_t rows, const double* M, int64_t ldm, int64_t n, int64_t k, double cond_limit,
+                      int allow_marginal, void* X, int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info,
+                      cudaStream_t st) {
+  const int64_t nk = n + k;
+  nsk::Scratch siga, v2s, v2w;
+  NSK_CUDA_OK(siga.alloc(sizeof(double) * n, st));
+  NSK_CUDA_OK(v2s.alloc(sizeof(double) * k, st));
+  NSK_CUDA_OK(v2w.alloc(sizeof(double) * k * k * nc, st));
+  if (int rc = nsk::jacobi_trailing(nc, rows, nk, M, ldm, k, static_cast<double*>(Vk), ldv, sigma, st)) return rc;
+  if (int rc = nsk::jacobi_trailing(nc, rows, n, M, ldm, 0, nullptr, 1, siga.as<double>(), st)) return rc;
+  std::vector<double> s_aug(static_cast<size_t>(nk)), s_a(static_cast<size_t>(n));
+  NSK_CUDA_OK(cudaMemcpyAsync(s_aug.data(), sigma, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaMemcpyAsync(s_a.data(), siga.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  double tail = 0.0;
+  for (int64_t i = n; i < nk; ++i) tail += s_aug[static_cast<size_t>(i)] * s_aug[static_cast<size_t>(i)];
+  info[0] = std::sqrt(tail);                   // tls_residual
+  info[2] = s_a[static_cast<size_t>(n - 1)];   // sigma_n(A) (of the sketch / of R)
+  info[3] = s_aug[static_cast<size_t>(n)];     // sigma_{n+1}([A|B])
+  if (!(info[2] > info[3]) && !allow_marginal)
+    return nsk::fail(NSK_ETLS_EXISTENCE, "tls: solution existence check failed: sigma_n(A) = " +
+                                             std::to_string(info[2]) + " is not above sigma_{n+1}([A|B]) = " +
+                                             std::to_string(info[3]));
+  // Condition estimate of the k x k corner V_k2 (tls.cpp:32-37), then X = -V_k1 V_k2^{-1}.
+  NSK_CUDA_OK(cudaMemcpy2DAsync(v2w.p, sizeof(double) * k * nc, static_cast<double*>(Vk) + n * nc,
+                                sizeof(double) * ldv * nc, sizeof(double) * k * nc, k, cudaMemcpyDeviceToDevice, st));
+  if (int rc = nsk::jacobi_trailing(nc, k, k, v2w.as<double>(), k, 0, nullptr, 1, v2s.as<double>(), st)) return rc;
+  std::vector<double> sv2(static_cast<size_t>(k));
+  NSK_CUDA_OK(cudaMemcpyAsync(sv2.data(), v2s.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  const double smin = sv2[static_cast<size_t>(k - 1)];
+  info[1] = smin == 0.0 ? HUGE_VAL : sv2[0] / smin;
+  if (!(info[1] <= cond_limit))
+    return nsk::fail(NSK_ETLS_CONDITION, "tls: V_k2 is ill conditioned (cond estimate " + std::to_string(info[1]) +
+                                             "); X = -V_k1 V_k2^{-1} is unreliable");
+  return nsk::tls_corner(nc, static_cast<const double*>(Vk), ldv, n, k, static_cast<double*>(X), ldx, st);
+}
+
 // ---- sketched total least squares (tls.cpp:97-113) ------------------------
 
 int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,
@@ -616,11 +651,8 @@ int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t
   cudaStream_t st = ST(stream);
   const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_ncomp(op, nc_in);
   const int64_t nk = n + k;
-  nsk::Scratch sa, siga, v2s, v2w;
+  nsk::Scratch sa;
   NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * nk * nc, st));
-  NSK_CUDA_OK(siga.alloc(sizeof(double) * n, st));
-  NSK_CUDA_OK(v2s.alloc(sizeof(double) * k, st));
-  NSK_CUDA_OK(v2w.alloc(sizeof(double) * k * k * nc, st));
   nsk::RowMap rows{0, 1, m};
   // S [A | B] without forming [A | B] (tls.cpp:108-109): two applies into adjacent columns.
   if (int rc = dispatch_apply(op, nc_in, rows, n, static_cast<const double*>(A), lda, sa.as<double>(), op.s, st))
@@ -628,37 +660,58 @@ int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t
   if (int rc = dispatch_apply(op, nc_in, rows, k, static_cast<const double*>(B), ldb, sa.as<double>() + op.s * n * nc,
                               op.s, st))
     return rc;
-  // Trailing k right singular vectors of S[A|B] and its full spectrum; sigma_n(S A).
-  if (int rc = nsk::jacobi_trailing(nc, op.s, nk, sa.as<double>(), op.s, k, static_cast<double*>(Vk), ldv, sigma, st))
+  return tls_finish(nc, op.s, sa.as<double>(), op.s, n, k, cond_limit, allow_marginal, X, ldx, Vk, ldv, sigma, info,
+                    st);
+}
+
+// ---- exact total least squares (tls.cpp:83-95) ----------------------------
+// Thin QR of [A|B] on the device (tall_qr.cu), then the same SVD tail on the
+// (n + k) x (n + k) triangle.
+int nsk_tls_solve_exact(int scalar, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                        int64_t ldb, double cond_limit, int allow_marginal, void* X, int64_t ldx, void* Vk,
+                        int64_t ldv, double* sigma, double* info, void* stream) {
+  if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "tls: bad scalar kind");
+  if (k < 1) return nsk::fail(nsk::EINVAL_, "tls: B must have at least one column");
+  if (n < k) return nsk::fail(nsk::EINVAL_, "tls: need n >= k");
+  if (m < n + k) return nsk::fail(nsk::EINVAL_, "tls: need m >= n + k");
+  if (!A || !B || lda < m || ldb < m) return nsk::fail(nsk::EINVAL_, "tls: bad A / B");
+  if (!X || !Vk || !sigma || !info || ldx < n || ldv < n + k) return nsk::fail(nsk::EINVAL_, "tls: bad outputs");
+  cudaStream_t st = ST(stream);
+  const int nc = scalar == NSK_COMPLEX ? 2 : 1;
+  const int64_t nk = n + k;
+  nsk::Scratch r;
+  NSK_CUDA_OK(r.alloc(sizeof(double) * nk * nk * nc, st));
+  if (int rc = nsk::tall_qr_r(nc, m, n, static_cast<const double*>(A), lda, k, static_cast<const double*>(B), ldb,
+                              r.as<double>(), st))
     return rc;
-  if (int rc = nsk::jacobi_trailing(nc, op.s, n, sa.as<double>(), op.s, 0, nullptr, 1, siga.as<double>(), st))
-    return rc;
-  std::vector<double> s_aug(static_cast<size_t>(nk)), s_a(static_cast<size_t>(n));
-  NSK_CUDA_OK(cudaMemcpyAsync(s_aug.data(), sigma, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
-  NSK_CUDA_OK(cudaMemcpyAsync(s_a.data(), siga.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  return tls_finish(nc, nk, r.as<double>(), nk, n, k, cond_limit, allow_marginal, X, ldx, Vk, ldv, sigma, info, st);
+}
+
+int nsk_tls_solve_exact_host(int scalar, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                             int64_t ldb, double cond_limit, int allow_marginal, void* X, int64_t ldx, void* Vk,
+                             int64_t ldv, double* sigma, double* info) {
+  if (lda < m || ldb < m || k < 1 || n < 1) return nsk::fail(nsk::EINVAL_, "tls: bad dimensions");
+  cudaStream_t st = host_stream();
+  const int nc = scalar == NSK_COMPLEX ? 2 : 1;
+  nsk::Scratch a, b, x, v, sg;
+  double *dA = nullptr, *dB = nullptr;
+  if (int rc = copy_in(A, m, n, lda, nc, &dA, a, st)) return rc;
+  if (int rc = copy_in(B, m, k, ldb, nc, &dB, b, st)) return rc;
+  NSK_CUDA_OK(x.alloc(sizeof(double) * n * k * nc, st));
+  NSK_CUDA_OK(v.alloc(sizeof(double) * (n + k) * k * nc, st));
+  NSK_CUDA_OK(sg.alloc(sizeof(double) * (n + k), st));
+  const int rc = nsk_tls_solve_exact(scalar, m, n, k, dA, m, dB, m, cond_limit, allow_marginal, x.p, n, v.p, n + k,
+                                     sg.as<double>(), info, st);
+  if (rc != NSK_OK && rc != NSK_ETLS_CONDITION) return rc;
+  if (rc == NSK_OK && X) {
+    if (int r2 = copy_out(X, ldx, x.as<double>(), n, k, nc, st)) return r2;
+  }
+  if (Vk) {
+    if (int r2 = copy_out(Vk, ldv, v.as<double>(), n + k, k, nc, st)) return r2;
+  }
+  if (sigma) NSK_CUDA_OK(cudaMemcpyAsync(sigma, sg.p, sizeof(double) * (n + k), cudaMemcpyDeviceToHost, st));
   NSK_CUDA_OK(cudaStreamSynchronize(st));
-  double tail = 0.0;
-  for (int64_t i = n; i < nk; ++i) tail += s_aug[static_cast<size_t>(i)] * s_aug[static_cast<size_t>(i)];
-  info[0] = std::sqrt(tail);                   // tls_residual
-  info[2] = s_a[static_cast<size_t>(n - 1)];   // sigma_n(S A)
-  info[3] = s_aug[static_cast<size_t>(n)];     // sigma_{n+1}(S [A|B])
-  if (!(info[2] > info[3]) && !allow_marginal)
-    return nsk::fail(NSK_ETLS_EXISTENCE, "tls: solution existence check failed: sigma_n(A) = " +
-                                             std::to_string(info[2]) + " is not above sigma_{n+1}([A|B]) = " +
-                                             std::to_string(info[3]));
-  // Condition estimate of the k x k corner V_k2 (tls.cpp:32-37), then X = -V_k1 V_k2^{-1}.
-  NSK_CUDA_OK(cudaMemcpy2DAsync(v2w.p, sizeof(double) * k * nc, static_cast<double*>(Vk) + n * nc,
-                                sizeof(double) * ldv * nc, sizeof(double) * k * nc, k, cudaMemcpyDeviceToDevice, st));
-  if (int rc = nsk::jacobi_trailing(nc, k, k, v2w.as<double>(), k, 0, nullptr, 1, v2s.as<double>(), st)) return rc;
-  std::vector<double> sv2(static_cast<size_t>(k));
-  NSK_CUDA_OK(cudaMemcpyAsync(sv2.data(), v2s.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-  NSK_CUDA_OK(cudaStreamSynchronize(st));
-  const double smin = sv2[static_cast<size_t>(k - 1)];
-  info[1] = smin == 0.0 ? HUGE_VAL : sv2[0] / smin;
-  if (!(info[1] <= cond_limit))
-    return nsk::fail(NSK_ETLS_CONDITION, "tls: V_k2 is ill conditioned (cond estimate " + std::to_string(info[1]) +
-                                             "); X = -V_k1 V_k2^{-1} is unreliable");
-  return nsk::tls_corner(nc, static_cast<const double*>(Vk), ldv, n, k, static_cast<double*>(X), ldx, st);
+  return rc;
 }
 
 int nsk_tls_solve_sketched_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,

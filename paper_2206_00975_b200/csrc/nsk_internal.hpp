@@ -130,6 +130,11 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
 int jacobi_trailing(int ncomp, int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k,
                     double* W, int64_t ldw, double* sigma, cudaStream_t st);
 
+// R factor (N x N upper, ld N, N = n + k) of the thin QR of [A | B] (m x N),
+// shifted CholeskyQR3 (tall_qr.cu).  B may be null when k = 0.
+int tall_qr_r(int nc, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k, const double* B, int64_t ldb,
+              double* R, cudaStream_t st);
+
 int residual_fro(int ncomp, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k,
                  const double* W, int64_t ldw, double* out_host, cudaStream_t st);
 
@@ -162,7 +167,25 @@ struct Scratch {
   }
   cudaError_t alloc(size_t bytes, cudaStream_t s) {
     st = s;
+    keep_pool();
     return cudaMallocAsync(&p, bytes ? bytes : 8, s);
+  }
+  // Keep freed blocks in the device's default pool instead of unmapping them
+  // at every synchronisation (once per device): repeated calls with
+  // gigabyte-sized scratch (host staging, the exact solver's Q) would
+  // otherwise re-map HBM on every call.
+  static void keep_pool() {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+    const uint64_t bit = uint64_t(1) << dev;
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done.fetch_or(bit, std::memory_order_relaxed);
   }
   template <class T>
   T* as() const {

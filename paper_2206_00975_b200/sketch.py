@@ -37,7 +37,8 @@ from ._lib import (KIND_CODES, KIND_NAMES, NSK_COMPLEX, NSK_REAL, SvdConvergence
 
 __all__ = ["SketchOperator", "SketchedMatrix", "NullspaceResult", "apply", "apply_shard", "solve_k",
            "solve_tol", "residual_certificate", "svd_trailing", "default_sketch_size", "update_column",
-           "downdate_column", "update_row", "downdate_row", "tls_solve_sketched", "TlsSolution",
+           "downdate_column", "update_row", "downdate_row", "tls_solve_sketched", "tls_solve_exact",
+           "tls_error_metrics", "TlsErrorMetrics", "TlsSolution",
            "SvdConvergenceError", "TlsExistenceError", "TlsConditionError", "KINDS"]
 
 KINDS = tuple(KIND_CODES)
@@ -431,11 +432,8 @@ class TlsSolution:
     residual_certificate: Optional[float] = None
 
 
-def tls_solve_sketched(A, B, S: SketchOperator, cond_limit: float = 1e12, allow_marginal: bool = False,
-                       certificate: bool = False) -> TlsSolution:
-    """Sketched total least squares (tls.cpp:97-113): trailing subspace of S [A|B], X = -V_k1 V_k2^{-1}."""
+def _tls_inputs(A, B):
     torch = _torch()
-    L = _lib.load()
     A = _as_device(A)
     B = _as_device(B, A)
     if B.dim() == 1:
@@ -447,6 +445,79 @@ def tls_solve_sketched(A, B, S: SketchOperator, cond_limit: float = 1e12, allow_
         A, B = A.to(torch.complex128), B.to(torch.complex128)
     A, lda = _colmajor(A)
     B, ldb = _colmajor(B)
+    return A, lda, B, ldb, scalar
+
+
+def _tls_certify(sol, A, B, n, k):
+    """||[A|B] Vk||_F = ||A V_k1 + B V_k2||_F (tls.cpp:55-58), opt-in check."""
+    torch = _torch()
+    pd = sol.Vk.dtype
+    prod = A.to(pd) @ sol.Vk[:n, :k] + B.to(pd) @ sol.Vk[n:, :k]
+    sol.residual_certificate = float(torch.linalg.norm(prod).item())
+
+
+def tls_solve_exact(A, B, cond_limit: float = 1e12, allow_marginal: bool = False,
+                    certificate: bool = False) -> TlsSolution:
+    """Exact total least squares (tls.cpp:83-95): thin QR of [A|B] on the device
+    (shifted CholeskyQR3), SVD of the (n+k)^2 triangle, X = -V_k1 V_k2^{-1}."""
+    torch = _torch()
+    L = _lib.load()
+    A, lda, B, ldb, scalar = _tls_inputs(A, B)
+    m, n = A.shape
+    k = B.shape[1]
+    dt = torch.complex128 if scalar == NSK_COMPLEX else torch.float64
+    X = _empty_colmajor(n, max(k, 1), dt, A.device)
+    Vk = _empty_colmajor(n + k, max(k, 1), dt, A.device)
+    sig = torch.empty(n + k, dtype=torch.float64, device=A.device)
+    info = np.zeros(4)
+    check(L.nsk_tls_solve_exact(scalar, m, n, k, ctypes.c_void_p(A.data_ptr()), lda, ctypes.c_void_p(B.data_ptr()),
+                                ldb, float(cond_limit), int(bool(allow_marginal)), ctypes.c_void_p(X.data_ptr()),
+                                max(n, 1), ctypes.c_void_p(Vk.data_ptr()), n + k, ctypes.c_void_p(sig.data_ptr()),
+                                info.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _stream_ptr()))
+    sol = TlsSolution(X[:, :k], Vk[:, :k], float(info[0]), float(info[1]), sig)
+    if certificate:
+        _tls_certify(sol, A, B, n, k)
+    return sol
+
+
+@dataclasses.dataclass
+class TlsErrorMetrics:
+    rel_err: float  # ||X - Xs||_2 / ||X||_2
+    sin_X: float    # spectral sin between the column spans of X and Xs
+    sin_Vk: float   # spectral sin between the trailing subspaces
+
+
+def _sin_theta_spectral(U, V):
+    """Largest complement sine between two column spans (kernels.cpp:121-167, 153-167)."""
+    big, small = (U, V) if U.shape[1] >= V.shape[1] else (V, U)
+    if big.shape[1] == 0 or small.shape[1] == 0:
+        return 0.0
+    r = small - big @ (big.conj().T @ small)
+    return min(1.0, float(np.linalg.svd(r, compute_uv=False)[0]))
+
+
+def tls_error_metrics(exact: TlsSolution, sk: TlsSolution) -> TlsErrorMetrics:
+    """Errors of a sketched solution against the exact one (tls.cpp:115-131)."""
+    def host(x):
+        return x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+    X, Xs = host(exact.X), host(sk.X)
+    if X.shape != Xs.shape:
+        raise ValueError("tls_error_metrics: X shapes differ")
+    x_norm = float(np.linalg.svd(X, compute_uv=False)[0])
+    if x_norm == 0.0:
+        raise ValueError("tls_error_metrics: exact X is zero; rel_err undefined")
+    rel = float(np.linalg.svd(X.astype(np.complex128) - Xs.astype(np.complex128), compute_uv=False)[0]) / x_norm
+    qe, _ = np.linalg.qr(X)
+    qs, _ = np.linalg.qr(Xs)
+    return TlsErrorMetrics(rel, _sin_theta_spectral(qe, qs), _sin_theta_spectral(host(exact.Vk), host(sk.Vk)))
+
+
+def tls_solve_sketched(A, B, S: SketchOperator, cond_limit: float = 1e12, allow_marginal: bool = False,
+                       certificate: bool = False) -> TlsSolution:
+    """Sketched total least squares (tls.cpp:97-113): trailing subspace of S [A|B], X = -V_k1 V_k2^{-1}."""
+    torch = _torch()
+    L = _lib.load()
+    A, lda, B, ldb, scalar = _tls_inputs(A, B)
     m, n = A.shape
     k = B.shape[1]
     cplx_out = _out_dtype_is_complex(S, scalar)
@@ -461,8 +532,6 @@ def tls_solve_sketched(A, B, S: SketchOperator, cond_limit: float = 1e12, allow_
                                    ctypes.c_void_p(sig.data_ptr()), info.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                    _stream_ptr()))
     sol = TlsSolution(X[:, :k], Vk[:, :k], float(info[0]), float(info[1]), sig)
-    if certificate:  # ||[A|B] Vk||_F = ||A V_k1 + B V_k2||_F (tls.cpp:55-58), opt-in check
-        pd = Vk.dtype
-        prod = A.to(pd) @ Vk[:n, :k] + B.to(pd) @ Vk[n:, :k]
-        sol.residual_certificate = float(torch.linalg.norm(prod).item())
+    if certificate:
+        _tls_certify(sol, A, B, n, k)
     return sol

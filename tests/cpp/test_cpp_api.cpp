@@ -212,6 +212,15 @@ int main() {
     Matrix A0 = A;  // rank-deficient A (zero column): sigma_n(SA) = 0, the solvability check must fire
     for (Index i = 0; i < m; ++i) A0(i, n - 1) = 0.0;
     CHECK_THROWS_AS(tls_solve_sketched({A0, B}, S), TlsExistenceError);
+    // exact solver (tls.cpp:83-95) and the error metrics (tls.cpp:115-131)
+    TlsSolution ex = tls_solve_exact({A, B}, opt);
+    CHECK(max_abs_diff(ex.X, xt) < 1e-5);
+    CHECK(ex.has_residual_certificate && std::abs(ex.residual_certificate - ex.tls_residual) < 1e-8 * ex.tls_residual);
+    TlsErrorMetrics met = tls_error_metrics(ex, sol);
+    CHECK(met.rel_err >= 0.0 && met.rel_err < 1e-3 && met.sin_Vk < 1e-3 && met.sin_X <= 1.0);
+    TlsErrorMetrics self = tls_error_metrics(ex, ex);
+    CHECK(self.rel_err == 0.0 && self.sin_Vk < 1e-12);
+    CHECK_THROWS_AS(tls_solve_exact({A0, B}), TlsExistenceError);
   }
   if (failures) {
     std::fprintf(stderr, "%d check(s) failed\n", failures);

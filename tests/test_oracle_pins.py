@@ -151,3 +151,21 @@ def test_angles_complement_projection(oracle):
     V = (U + ep) / np.linalg.norm(U + ep)
     expect = np.linalg.norm(ep) / math.sqrt(1 + np.linalg.norm(ep) ** 2)
     assert abs(oracle.sin_theta(U, V) - expect) < 1e-3 * expect
+
+
+def test_tls_exact_oracle_equals_svd_of_augmented(oracle):
+    # tls.cpp:83-95: the R factor of [A|B] shares singular values and right
+    # singular vectors with [A|B]; X = -V_k1 V_k2^{-1} of the trailing subspace.
+    rng = np.random.default_rng(3)
+    m, n, k = 300, 8, 2
+    A = rng.standard_normal((m, n))
+    X = rng.standard_normal((n, k))
+    B = A @ X + 1e-3 * rng.standard_normal((m, k))
+    Xo, Vo, so, res, cond = oracle.tls_solve_exact(A, B)
+    _, s, vh = np.linalg.svd(np.concatenate([A, B], axis=1))
+    v = vh.T[:, n:]
+    assert np.max(np.abs(so - s)) <= 1e-13 * s[0]
+    assert oracle.sin_theta(Vo, v) < 1e-12
+    assert np.linalg.norm(Xo - np.linalg.solve(v[n:].T, -v[:n].T).T) <= 1e-10 * np.linalg.norm(Xo)
+    assert abs(res - math.sqrt(np.sum(s[n:] ** 2))) <= 1e-12 * res
+    assert np.linalg.norm(Xo - X) / np.linalg.norm(X) < 1e-2

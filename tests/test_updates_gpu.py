@@ -262,3 +262,56 @@ def test_tls_validation(nsk, oracle):
     Adef[:, -1] = 0.0
     with pytest.raises(nsk.TlsExistenceError):
         nsk.tls_solve_sketched(dev(Adef), dev(B), S)
+
+
+# ---- exact TLS (tls.cpp:83-95) on the device: shifted CholeskyQR3 + SVD of R
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_tls_exact_matches_oracle(nsk, oracle, cplx):
+    m, n, k = 3000, 24, 2
+    A, B, X = _tls_problem(oracle, m, n, k, 1e-3, 31)
+    if cplx:
+        A = A + 1j * oracle.random_real(m, n, 41)
+        B = A @ (X + 1j * oracle.random_real(n, k, 42)) + 1e-3 * oracle.random_real(m, k, 43)
+    sol = nsk.tls_solve_exact(dev(A), dev(B), certificate=True)
+    Xr, Vr, svr, resr, condr = oracle.tls_solve_exact(A, B)
+    assert np.max(np.abs(host(sol.augmented_singular_values) - svr)) <= 1e-12 * svr[0]
+    assert oracle.sin_theta(host(sol.Vk), Vr) < 1e-10
+    assert np.linalg.norm(host(sol.X) - Xr) <= 1e-9 * np.linalg.norm(Xr)
+    assert abs(sol.tls_residual - resr) <= 1e-10 * resr
+    assert abs(sol.cond_Vk2 - condr) <= 1e-8 * condr
+    # the certificate of the exact solution is its residual (||[A|B] Vk|| = sigma tail)
+    assert abs(sol.residual_certificate - resr) <= 1e-8 * resr
+
+
+def test_tls_exact_ill_conditioned(nsk, oracle):
+    # kappa([A|B]) = 1e11 (plain CholeskyQR breaks down above ~1e8): the shift
+    # keeps the first Cholesky alive, two more passes restore orthogonality;
+    # sigma and the trailing subspace (gap 1e-8) match Householder.
+    m, n, k = 2000, 16, 1
+    sig = np.concatenate([np.logspace(0, -8, n), [1e-11]])
+    C = oracle.make_test_matrix(m, n + k, sig, 51)
+    A, B = C[:, :n], C[:, n:]
+    sol = nsk.tls_solve_exact(dev(A), dev(B), allow_marginal=True)
+    _, Vr, svr, _, _ = oracle.tls_solve_exact(A, B, allow_marginal=True)
+    assert np.max(np.abs(host(sol.augmented_singular_values) - svr)) <= 1e-12 * svr[0]
+    assert oracle.sin_theta(host(sol.Vk), Vr) < 1e-6
+
+
+def test_tls_exact_validation_and_metrics(nsk, oracle):
+    m, n, k = 400, 10, 1
+    A, B, X = _tls_problem(oracle, m, n, k, 1e-4, 61)
+    with pytest.raises(ValueError):
+        nsk.tls_solve_exact(dev(A[:, :0]), dev(B))
+    with pytest.raises(ValueError):
+        nsk.tls_solve_exact(dev(A[: n, :]), dev(B[: n, :]))  # m < n + k
+    Adef = A.copy()
+    Adef[:, -1] = 0.0
+    with pytest.raises(nsk.TlsExistenceError):
+        nsk.tls_solve_exact(dev(Adef), dev(B))
+    ex = nsk.tls_solve_exact(dev(A), dev(B))
+    sk = nsk.tls_solve_sketched(dev(A), dev(B), nsk.SketchOperator.draw("gaussian", 8 * (n + k), m, 62))
+    met = nsk.tls_error_metrics(ex, sk)
+    assert 0 <= met.rel_err < 1e-2 and 0 <= met.sin_X <= 1 and 0 <= met.sin_Vk < 1e-2
+    same = nsk.tls_error_metrics(ex, ex)
+    assert same.rel_err == 0.0 and same.sin_X < 1e-12 and same.sin_Vk < 1e-12
