@@ -63,5 +63,25 @@ def build(force=False, verbose=False):
     return OUT
 
 
+CLI_SRC = os.path.join(HERE, "..", "tools", "cli", "nullsketch_main.cpp")
+CLI_OUT = os.path.join(HERE, "nullsketch_b200")
+
+
+def build_cli(force=False):
+    """The reference-compatible command-line tool (tools/cli), linked against the library."""
+    lib = build()
+    if not force and os.path.exists(CLI_OUT) and os.path.getmtime(CLI_OUT) >= max(
+            os.path.getmtime(CLI_SRC), os.path.getmtime(lib),
+            os.path.getmtime(os.path.join(HERE, "..", "include", "nullsketch_b200.hpp"))):
+        return CLI_OUT
+    cmd = ["g++", "-O2", "-std=c++17", "-I", os.path.join(HERE, "..", "include"), CLI_SRC, "-o", CLI_OUT,
+           "-L", HERE, "-lnullsketch_b200", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI_OUT
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_cli(force="--force" in sys.argv))

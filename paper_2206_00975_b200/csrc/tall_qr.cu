@@ -275,8 +275,10 @@ namespace {
 // the two re-orthogonalisation passes (exactly rank-deficient [A|B]: a zero
 // direction of C gives a zero column of Q1 and an exactly singular G2).
 // cols: device pointers of the N columns of C (m entries x nc each).
-int tall_qr_attempt(int nc, int64_t m, const std::vector<const double*>& cols, double* R, bool shift_all, int* hb,
-                    cudaStream_t st) {
+// cols: device pointers of the N columns of C (m entries x nc each); src: the
+// array each column lives in (a 2-D copy must not span two allocations).
+int tall_qr_attempt(int nc, int64_t m, const std::vector<const double*>& cols, const std::vector<int>& src,
+                    double* R, bool shift_all, int* hb, cudaStream_t st) {
   const int64_t N = static_cast<int64_t>(cols.size());
   cublasHandle_t h = cublas_for(st);
   if (!h) return fail(ECUDA, "tall QR: cublasCreate failed");
@@ -293,12 +295,16 @@ int tall_qr_attempt(int nc, int64_t m, const std::vector<const double*>& cols, d
   // Q <- C (column runs with a common stride are one 2-D copy)
   for (int64_t j = 0; j < N;) {
     int64_t e = j + 1;
-    int64_t stride = e < N ? cols[e] - cols[j] : m * nc;
-    if (stride < m * nc) stride = m * nc;  // not a forward run: copy column j alone
+    int64_t stride = e < N && src[e] == src[j] ? cols[e] - cols[j] : m * nc;
+    if (stride < m * nc) stride = m * nc;  // not a forward run: column j alone
     else
-      while (e < N && cols[e] - cols[e - 1] == stride) ++e;
-    NSK_CUDA_OK(cudaMemcpy2DAsync(Q + j * m * nc, sizeof(double) * m * nc, cols[j], sizeof(double) * stride,
-                                  sizeof(double) * m * nc, e - j, cudaMemcpyDeviceToDevice, st));
+      while (e < N && src[e] == src[j] && cols[e] - cols[e - 1] == stride) ++e;
+    const cudaError_t ce = cudaMemcpy2DAsync(Q + j * m * nc, sizeof(double) * m * nc, cols[j], sizeof(double) * stride,
+                                             sizeof(double) * m * nc, e - j, cudaMemcpyDeviceToDevice, st);
+    if (ce != cudaSuccess)
+      return fail(ECUDA, std::string("tall QR: copy of columns ") + std::to_string(j) + ".." + std::to_string(e) +
+                             " (m " + std::to_string(m) + ", pitch " + std::to_string(stride) + "): " +
+                             cudaGetErrorString(ce));
     j = e;
   }
   const double u = 1.1102230246251565e-16;
@@ -360,10 +366,12 @@ int tall_qr_r(int nc, int64_t m, int64_t n, const double* A, int64_t lda, int64_
   NSK_CUDA_OK(cudaMemcpyAsync(nz.data(), zs.p, sizeof(int) * N, cudaMemcpyDeviceToHost, st));
   NSK_CUDA_OK(cudaStreamSynchronize(st));
   std::vector<const double*> cols;
+  std::vector<int> src;
   std::vector<int64_t> where;
   for (int64_t j = 0; j < N; ++j)
     if (nz[static_cast<size_t>(j)]) {
       cols.push_back(j < n ? A + j * lda * nc : B + (j - n) * ldb * nc);
+      src.push_back(j < n ? 0 : 1);
       where.push_back(j);
     }
   const int64_t Nz = static_cast<int64_t>(cols.size());
@@ -376,10 +384,10 @@ int tall_qr_r(int nc, int64_t m, int64_t n, const double* A, int64_t lda, int64_
     Rz = rs.as<double>();
   }
   int hb = 0;
-  if (int rc = tall_qr_attempt(nc, m, cols, Rz, false, &hb, st)) return rc;
+  if (int rc = tall_qr_attempt(nc, m, cols, src, Rz, false, &hb, st)) return rc;
   if (hb) {  // exactly rank-deficient C: shift every pass
     hb = 0;
-    if (int rc = tall_qr_attempt(nc, m, cols, Rz, true, &hb, st)) return rc;
+    if (int rc = tall_qr_attempt(nc, m, cols, src, Rz, true, &hb, st)) return rc;
   }
   if (hb) return fail(ENOCONV, "tall QR: Cholesky breakdown (input contains NaN/Inf)");
   if (Nz < N)  // R[0:Nz, where[c]] = Rz[:, c]: R^H R = C^H C with zero columns in place
