@@ -25,9 +25,16 @@
 namespace nsk {
 namespace {
 
-constexpr int CONSUMERS = 256;  // 8 MMA warps
-constexpr int PRODUCERS = 128;  // 4 generator / loader warps
+constexpr int CONSUMERS = 256;  // 8 MMA warps (warpgroups 0, 1)
+#ifndef NSK_GAUSS_PRODUCERS
+#define NSK_GAUSS_PRODUCERS 256
+#endif
+constexpr int PRODUCERS = NSK_GAUSS_PRODUCERS;  // generator / loader warps (warpgroups 2, 3)
 constexpr int THREADS = CONSUMERS + PRODUCERS;
+// With two producer warpgroups the register file is re-split with setmaxnreg:
+// consumers hold 64 FP64 accumulators (128 registers) plus fragments,
+// producers only Philox / Box-Muller state.
+constexpr int REG_CONSUMER = 168, REG_PRODUCER = 88;
 
 // Shared-memory tiles use a "k4-interleaved" layout: element (row x, k) of a
 // tile with X rows sits at (k / 4) * (4 X) + 4 x + (k % 4).  An m8n8k4
@@ -166,6 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
   const int64_t nchunks = kend > kbeg ? (kend - kbeg + T::BK - 1) / T::BK : 0;
 
   if (threadIdx.x >= CONSUMERS) {
+    if (PRODUCERS == 256) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_PRODUCER));
     // ---------------- producers ----------------
     // Loads of LAG + 1 stages are in flight at once: stage c is issued (one
     // cp.async group) and its G tile generated while stages c-1 .. c-LAG are
@@ -222,6 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
   }
 
   // ---------------- consumers ----------------
+  if (PRODUCERS == 256) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_CONSUMER));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp % T::WGM, wn = warp / T::WGM;
   double acc[TM][TN][2];
