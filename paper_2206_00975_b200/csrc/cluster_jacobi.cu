@@ -106,7 +106,7 @@ __device__ void circle_init(Circle& cc, int c, int b) {
 // each, inner products over rows [0, n), rotations over rows [0, ld)) until a
 // sweep rotates nothing.  Entered and left with the cluster synchronised.
 // Returns the number of sweeps (CTA 0 also records per-sweep counts).
-template <int NC>
+template <int NC, int RPL>
 __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc, int n, int ld, int b, double tol2,
                              int* counter, unsigned long long* prof = nullptr) {
   long long t_inner = 0, t_move = 0, t0 = 0, t1 = 0;
@@ -133,7 +133,11 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
           const int lq = r == 0 ? cc.ptab[t * b + warp][1] : b + (warp + t) % b;
           double* xp = cols[lp / b] + (lp % b) * colsz;
           double* xq = cols[lq / b] + (lq % b) * colsz;
-          if (jacobi_pair<NC>(xp, xq, n, ld, lane, tol2) && lane == 0) cc.rotated = 1;
+          // register-resident step (n <= 32 RPL); complex with 16 rows per lane
+          // would exceed the register budget of a 512-thread CTA
+          const bool rot = (NC == 2 && RPL > 8) ? jacobi_pair<NC>(xp, xq, n, ld, lane, tol2)
+                                                : jacobi_pair_reg<NC, RPL>(xp, xq, n, ld, lane, tol2);
+          if (rot && lane == 0) cc.rotated = 1;
         }
         __syncthreads();
       }
@@ -211,7 +215,7 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
   return sweep;
 }
 
-template <int NC>
+template <int NC, int RPL>
 __global__ void __launch_bounds__(512) cluster_jacobi_kernel(CJParams p) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double buf[];  // [4 block buffers][b][colsz]
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(512) cluster_jacobi_kernel(CJParams p) {
   }
   __syncthreads();
   cluster.sync();
-  circle_sweeps<NC>(cluster, buf, cc, n, ld, b, p.tol * p.tol, p.counter);
+  circle_sweeps<NC, RPL>(cluster, buf, cc, n, ld, b, p.tol * p.tol, p.counter);
   // ---- write back the two live blocks by their global block index
   for (int s = 0; s < 2; ++s) {
     const int bi = cc.blockid[cc.slotbuf[s]];
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  //
 
   // ---- 3. one-sided Jacobi on X (no V accumulation)
   stamp(p.stamps, 2);
-  circle_sweeps<NC>(cluster, buf, cc, n, n, b, p.tol * p.tol, p.counter, p.stamps ? p.stamps + 4 : nullptr);
+  circle_sweeps<NC, RPL>(cluster, buf, cc, n, n, b, p.tol * p.tol, p.counter, p.stamps ? p.stamps + 4 : nullptr);
   stamp(p.stamps, 3);
 
   // ---- 4. [W; P What] in the [R; I] layout
@@ -618,7 +622,11 @@ int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cu
   if (smem > 220 * 1024) return NOTAPPLICABLE;
   const int threads = 32 * (b < 1 ? 1 : b);
   CJParams prm{X, static_cast<int>(n), b, tol, counter};
-  auto kern = ncomp == 1 ? cluster_jacobi_kernel<1> : cluster_jacobi_kernel<2>;
+  const int rpl = n <= 128 ? 4 : n <= 256 ? 8 : 16;
+  auto kern = ncomp == 1 ? (rpl == 4 ? cluster_jacobi_kernel<1, 4> : rpl == 8 ? cluster_jacobi_kernel<1, 8>
+                                                                              : cluster_jacobi_kernel<1, 16>)
+                         : (rpl == 4 ? cluster_jacobi_kernel<2, 4> : rpl == 8 ? cluster_jacobi_kernel<2, 8>
+                                                                              : cluster_jacobi_kernel<2, 16>);
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (C > 8) NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};

@@ -145,3 +145,117 @@ __device__ __forceinline__ bool jacobi_pair(double* __restrict__ xp, double* __r
 }
 
 }  // namespace nsk
+
+namespace nsk {
+
+// ---- register-resident pair step (cluster kernels) ---------------------------
+// Fast double-precision reciprocal / reciprocal square root: the hardware
+// approximation (~2^-22) refined by two Newton steps (quadratic convergence,
+// ~1 ulp).  Used only for the rotation angle, whose rounding does not affect
+// orthogonality: cs = rsqrt(1 + t^2), sn = cs t is a rotation for any t.
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double h = 0.5 * x * y;
+    y = fma(y, fma(-h, y, 0.5), y);
+  }
+  return y;
+}
+
+// One-sided Jacobi step on the pair (xp, xq) with the leading n rows held in
+// registers between the inner products and the rotation (shared memory is
+// read once and written once; rows [n, ld) -- the V part of [R; I] -- are
+// rotated in place).  RPL >= ceil(n / 32).  Same rotation as jacobi_pair
+// (t = tan of the Rutishauser angle), written as
+//   t = sign(d) 2c / (|d| + sqrt(d^2 + 4 c^2)),  d = ||q||^2 - ||p||^2,
+// on power-of-two-scaled d, 2c (no overflow), with fast rcp / rsqrt.
+template <int NC, int RPL>
+__device__ __forceinline__ bool jacobi_pair_reg(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
+                                                int lane, double tol2) {
+  double pr[RPL], pim[RPL], qr[RPL], qim[RPL];
+  double a = 0, bb = 0, cr = 0, ci = 0;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int r = lane + 32 * k;
+    pr[k] = pim[k] = qr[k] = qim[k] = 0.0;
+    if (r < n) {
+      if (NC == 1) {
+        pr[k] = xp[r];
+        qr[k] = xq[r];
+      } else {
+        const double2 u = reinterpret_cast<const double2*>(xp)[r], v = reinterpret_cast<const double2*>(xq)[r];
+        pr[k] = u.x;
+        pim[k] = u.y;
+        qr[k] = v.x;
+        qim[k] = v.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    a = fma(pr[k], pr[k], a);
+    bb = fma(qr[k], qr[k], bb);
+    cr = fma(pr[k], qr[k], cr);
+    if (NC == 2) {
+      a = fma(pim[k], pim[k], a);
+      bb = fma(qim[k], qim[k], bb);
+      cr = fma(pim[k], qim[k], cr);
+      ci = fma(pr[k], qim[k], ci);
+      ci = fma(-pim[k], qr[k], ci);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {  // fixed butterfly order: deterministic
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    bb += __shfl_xor_sync(0xffffffffu, bb, o);
+    cr += __shfl_xor_sync(0xffffffffu, cr, o);
+    if (NC == 2) ci += __shfl_xor_sync(0xffffffffu, ci, o);
+  }
+  const double c2 = cr * cr + ci * ci;
+  if (!(c2 > tol2 * a * bb && c2 > 0.0)) return false;
+  double ph_re = 1.0, ph_im = 0.0, c = cr;
+  if (NC == 2) {
+    const double inv = rsqrt_fast(c2);
+    c = c2 * inv;  // |c|
+    ph_re = cr * inv;
+    ph_im = -ci * inv;
+  }
+  const double d = bb - a, e = 2.0 * c;
+  const double mx = fmax(fabs(d), fabs(e));
+  // 2^(1023 - exponent(mx)): exact scaling into [1, 2) (mx is normal: c2 > 0 passed)
+  int ex = (__double2hiint(mx) >> 20) & 0x7ff;
+  ex = ex < 1 ? 1 : (ex > 2045 ? 2045 : ex);
+  const double sc = __hiloint2double((2046 - ex) << 20, 0);
+  const double ds = d * sc, es = e * sc;
+  const double h2 = fma(ds, ds, es * es);
+  const double hs = h2 * rsqrt_fast(h2);
+  const double tt = copysign(1.0, d) * es * rcp_fast(fabs(ds) + hs);
+  const double cs = rsqrt_fast(fma(tt, tt, 1.0)), sn = cs * tt;
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int r = lane + 32 * k;
+    if (r < n) {
+      if (NC == 1) {
+        xp[r] = cs * pr[k] - sn * qr[k];
+        xq[r] = sn * pr[k] + cs * qr[k];
+      } else {
+        const double q1 = qr[k] * ph_re - qim[k] * ph_im, q2 = qr[k] * ph_im + qim[k] * ph_re;
+        reinterpret_cast<double2*>(xp)[r] = make_double2(cs * pr[k] - sn * q1, cs * pim[k] - sn * q2);
+        reinterpret_cast<double2*>(xq)[r] = make_double2(sn * pr[k] + cs * q1, sn * pim[k] + cs * q2);
+      }
+    }
+  }
+  if (ld > n) rotate_cols<NC>(xp + n * NC, xq + n * NC, ld - n, lane, cs, sn, ph_re, ph_im);
+  return true;
+}
+
+}  // namespace nsk
