@@ -293,6 +293,7 @@ def run_ours(args):
 
     # ---- breakdown: SVD and solve_k device time (rank 0's view).
     SA = step()
+    nsk.svd_trailing(SA, k)  # warm: first-launch module loading and scratch-pool growth stay out
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)

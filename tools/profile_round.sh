@@ -23,4 +23,4 @@ cap countsketch countsketch_owner "--kind countsketch"
 cap gaussian gaussian_sketch "--kind gaussian"
 cap srft srtt_tile_kernel "--kind srft"
 cap srdct srtt_tile_kernel "--kind srdct"
-cap svd cluster_jacobi "--kind srht"
+cap svd cluster_svd_kernel "--kind srht"
