@@ -126,20 +126,43 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
       // column pair exactly once.
       if (prof) t0 = clock64();
       double* const cols[2] = {buf + cc.slotbuf[0] * blksz, buf + cc.slotbuf[1] * blksz};
-      const int inner = r == 0 ? twob - 1 : b;
-      for (int t = 0; t < inner; ++t) {
-        if (warp < b) {
-          const int lp = r == 0 ? cc.ptab[t * b + warp][0] : warp;
-          const int lq = r == 0 ? cc.ptab[t * b + warp][1] : b + (warp + t) % b;
-          double* xp = cols[lp / b] + (lp % b) * colsz;
-          double* xq = cols[lq / b] + (lq % b) * colsz;
-          // register-resident step (n <= 32 RPL); complex with 16 rows per lane
-          // would exceed the register budget of a 512-thread CTA
-          const bool rot = (NC == 2 && RPL > 8) ? jacobi_pair<NC>(xp, xq, n, ld, lane, tol2)
-                                                : jacobi_pair_reg<NC, RPL>(xp, xq, n, ld, lane, tol2);
-          if (rot && lane == 0) cc.rotated = 1;
+      // complex with 16 rows per lane would exceed the register budget of a
+      // 512-thread CTA: that case keeps the shared-memory step
+      constexpr bool REG = !(NC == 2 && RPL > 8);
+      if (r == 0 || !REG) {
+        const int inner = r == 0 ? twob - 1 : b;
+        for (int t = 0; t < inner; ++t) {
+          if (warp < b) {
+            const int lp = r == 0 ? cc.ptab[t * b + warp][0] : warp;
+            const int lq = r == 0 ? cc.ptab[t * b + warp][1] : b + (warp + t) % b;
+            double* xp = cols[lp / b] + (lp % b) * colsz;
+            double* xq = cols[lq / b] + (lq % b) * colsz;
+            const bool rot = REG ? jacobi_pair_reg<NC, RPL>(xp, xq, n, ld, lane, tol2)
+                                 : jacobi_pair<NC>(xp, xq, n, ld, lane, tol2);
+            if (rot && lane == 0) cc.rotated = 1;
+          }
+          __syncthreads();
         }
-        __syncthreads();
+      } else if (warp < b) {
+        // cross rounds: warp w keeps top column w in registers for all b
+        // rounds; only the bottom columns pass through shared memory
+        double* xp = cols[0] + warp * colsz;
+        double pr[RPL], pim[RPL];
+        load_col<NC, RPL>(xp, n, lane, pr, pim);
+        bool any = false;
+        for (int t = 0; t < b; ++t) {
+          double* xq = cols[1] + ((warp + t) % b) * colsz;
+          any |= jacobi_step_preg<NC, RPL>(pr, pim, xp, xq, n, ld, lane, tol2);
+          __syncthreads();
+        }
+        if (any) {
+          store_col<NC, RPL>(xp, n, lane, pr, pim);
+          if (lane == 0) cc.rotated = 1;
+        }
+        __syncwarp();
+        __syncthreads();  // p columns visible before the move copies them
+      } else {
+        for (int t = 0; t <= b; ++t) __syncthreads();  // idle warps keep the barrier count
       }
       if (prof) {
         t1 = clock64();

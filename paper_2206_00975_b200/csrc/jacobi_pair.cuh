@@ -179,28 +179,49 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
 // (t = tan of the Rutishauser angle), written as
 //   t = sign(d) 2c / (|d| + sqrt(d^2 + 4 c^2)),  d = ||q||^2 - ||p||^2,
 // on power-of-two-scaled d, 2c (no overflow), with fast rcp / rsqrt.
+// Rows r = lane + 32 k < n of a column into / out of registers.
 template <int NC, int RPL>
-__device__ __forceinline__ bool jacobi_pair_reg(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
-                                                int lane, double tol2) {
-  double pr[RPL], pim[RPL], qr[RPL], qim[RPL];
-  double a = 0, bb = 0, cr = 0, ci = 0;
+__device__ __forceinline__ void load_col(const double* __restrict__ x, int n, int lane, double (&re)[RPL],
+                                         double (&im)[RPL]) {
 #pragma unroll
   for (int k = 0; k < RPL; ++k) {
     const int r = lane + 32 * k;
-    pr[k] = pim[k] = qr[k] = qim[k] = 0.0;
+    re[k] = im[k] = 0.0;
     if (r < n) {
       if (NC == 1) {
-        pr[k] = xp[r];
-        qr[k] = xq[r];
+        re[k] = x[r];
       } else {
-        const double2 u = reinterpret_cast<const double2*>(xp)[r], v = reinterpret_cast<const double2*>(xq)[r];
-        pr[k] = u.x;
-        pim[k] = u.y;
-        qr[k] = v.x;
-        qim[k] = v.y;
+        const double2 u = reinterpret_cast<const double2*>(x)[r];
+        re[k] = u.x;
+        im[k] = u.y;
       }
     }
   }
+}
+template <int NC, int RPL>
+__device__ __forceinline__ void store_col(double* __restrict__ x, int n, int lane, const double (&re)[RPL],
+                                          const double (&im)[RPL]) {
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int r = lane + 32 * k;
+    if (r < n) {
+      if (NC == 1)
+        x[r] = re[k];
+      else
+        reinterpret_cast<double2*>(x)[r] = make_double2(re[k], im[k]);
+    }
+  }
+}
+
+// Core of the register step: p held in registers (pr, pim; updated in place),
+// q read from and written back to shared memory; rows [n, ld) of both (the V
+// part of [R; I]) rotated in place.
+template <int NC, int RPL>
+__device__ __forceinline__ bool jacobi_step_preg(double (&pr)[RPL], double (&pim)[RPL], double* __restrict__ xp,
+                                                 double* __restrict__ xq, int n, int ld, int lane, double tol2) {
+  double qr[RPL], qim[RPL];
+  load_col<NC, RPL>(xq, n, lane, qr, qim);
+  double a = 0, bb = 0, cr = 0, ci = 0;
 #pragma unroll
   for (int k = 0; k < RPL; ++k) {
     a = fma(pr[k], pr[k], a);
@@ -231,7 +252,7 @@ __device__ __forceinline__ bool jacobi_pair_reg(double* __restrict__ xp, double*
   }
   const double d = bb - a, e = 2.0 * c;
   const double mx = fmax(fabs(d), fabs(e));
-  // 2^(1023 - exponent(mx)): exact scaling into [1, 2) (mx is normal: c2 > 0 passed)
+  // 2^(1023 - exponent(mx)): exact scaling of d, e into [1, 4)
   int ex = (__double2hiint(mx) >> 20) & 0x7ff;
   ex = ex < 1 ? 1 : (ex > 2045 ? 2045 : ex);
   const double sc = __hiloint2double((2046 - ex) << 20, 0);
@@ -242,20 +263,39 @@ __device__ __forceinline__ bool jacobi_pair_reg(double* __restrict__ xp, double*
   const double cs = rsqrt_fast(fma(tt, tt, 1.0)), sn = cs * tt;
 #pragma unroll
   for (int k = 0; k < RPL; ++k) {
-    const int r = lane + 32 * k;
-    if (r < n) {
-      if (NC == 1) {
-        xp[r] = cs * pr[k] - sn * qr[k];
-        xq[r] = sn * pr[k] + cs * qr[k];
-      } else {
-        const double q1 = qr[k] * ph_re - qim[k] * ph_im, q2 = qr[k] * ph_im + qim[k] * ph_re;
-        reinterpret_cast<double2*>(xp)[r] = make_double2(cs * pr[k] - sn * q1, cs * pim[k] - sn * q2);
-        reinterpret_cast<double2*>(xq)[r] = make_double2(sn * pr[k] + cs * q1, sn * pim[k] + cs * q2);
-      }
+    if (NC == 1) {
+      const double up = pr[k], uq = qr[k];
+      pr[k] = cs * up - sn * uq;
+      qr[k] = sn * up + cs * uq;
+    } else {
+      const double q1 = qr[k] * ph_re - qim[k] * ph_im, q2 = qr[k] * ph_im + qim[k] * ph_re;
+      const double p1 = pr[k], p2 = pim[k];
+      pr[k] = cs * p1 - sn * q1;
+      pim[k] = cs * p2 - sn * q2;
+      qr[k] = sn * p1 + cs * q1;
+      qim[k] = sn * p2 + cs * q2;
     }
   }
+  store_col<NC, RPL>(xq, n, lane, qr, qim);
   if (ld > n) rotate_cols<NC>(xp + n * NC, xq + n * NC, ld - n, lane, cs, sn, ph_re, ph_im);
   return true;
+}
+
+// One-sided Jacobi step on the pair (xp, xq) with the leading n rows held in
+// registers between the inner products and the rotation (shared memory is
+// read once and written once; rows [n, ld) -- the V part of [R; I] -- are
+// rotated in place).  RPL >= ceil(n / 32).  Same rotation as jacobi_pair
+// (t = tan of the Rutishauser angle), written as
+//   t = sign(d) 2c / (|d| + sqrt(d^2 + 4 c^2)),  d = ||q||^2 - ||p||^2,
+// on power-of-two-scaled d, 2c (no overflow), with fast rcp / rsqrt.
+template <int NC, int RPL>
+__device__ __forceinline__ bool jacobi_pair_reg(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
+                                                int lane, double tol2) {
+  double pr[RPL], pim[RPL];
+  load_col<NC, RPL>(xp, n, lane, pr, pim);
+  const bool rot = jacobi_step_preg<NC, RPL>(pr, pim, xp, xq, n, ld, lane, tol2);
+  if (rot) store_col<NC, RPL>(xp, n, lane, pr, pim);
+  return rot;
 }
 
 }  // namespace nsk
