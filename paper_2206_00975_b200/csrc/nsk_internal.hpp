@@ -33,6 +33,8 @@ struct DeviceTables {
   uint32_t* sign_bits = nullptr;    // srft/srdct: bit j of word j/32 = Rademacher bit of row j
   int64_t* srtt_freq = nullptr;     // srft/srdct: sample indices sorted by idx mod 1024 (tile FFT bin)
   int32_t* srtt_row = nullptr;      // output row of each sorted slot
+  int64_t* dct_freq = nullptr;      // srdct (srdct_tile.cu): v index n(a) of each sample, sorted by n mod 1024
+  int32_t* dct_row = nullptr;       // output row of each sorted srdct slot
   // CountSketch owner schedule (cs_schedule.cpp) over CS_T-row tiles.
   uint64_t* cs_ent = nullptr;       // [tile][warp][CS_GMAX][32] packed entries
   uint8_t* cs_cnt = nullptr;        // [tile][warp] iterations

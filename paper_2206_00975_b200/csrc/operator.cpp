@@ -242,6 +242,26 @@ const DeviceTables* Operator::tables() const {
       return nullptr;
     }
   }
+  if (kind == SRDCT && !idx.empty()) {
+    // Makhoul index of each sample (srdct_tile.cu): y_{2n} = v_n, y_{2n+1} = v_{m-1-n}.
+    std::vector<int64_t> nv(idx.size());
+    for (size_t r = 0; r < idx.size(); ++r) {
+      const int64_t a = idx[r];
+      nv[r] = (a & 1) == 0 ? a / 2 : m - 1 - (a - 1) / 2;
+    }
+    std::vector<int32_t> order(idx.size());
+    for (size_t r = 0; r < idx.size(); ++r) order[r] = static_cast<int32_t>(r);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+      return (nv[static_cast<size_t>(a)] & 1023) < (nv[static_cast<size_t>(b)] & 1023);
+    });
+    std::vector<int64_t> freq(idx.size());
+    for (size_t r = 0; r < idx.size(); ++r) freq[r] = nv[static_cast<size_t>(order[r])];
+    if (up(reinterpret_cast<void**>(&t.dct_freq), freq.data(), freq.size() * 8) != cudaSuccess ||
+        up(reinterpret_cast<void**>(&t.dct_row), order.data(), order.size() * 4) != cudaSuccess) {
+      cuda_fail(cudaGetLastError(), "srdct slot table upload");
+      return nullptr;
+    }
+  }
   dev.push_back(t);
   return &dev.back();
 }
@@ -292,6 +312,8 @@ Operator::~Operator() {
     if (t.sign_bits) cudaFree(t.sign_bits);
     if (t.srtt_freq) cudaFree(t.srtt_freq);
     if (t.srtt_row) cudaFree(t.srtt_row);
+    if (t.dct_freq) cudaFree(t.dct_freq);
+    if (t.dct_row) cudaFree(t.dct_row);
     if (t.cs_ent) cudaFree(t.cs_ent);
     if (t.cs_cnt) cudaFree(t.cs_cnt);
   }

@@ -21,6 +21,8 @@ int srtt_tile_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
                     double* SA, int64_t ldsa, cudaStream_t st);
 int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                     int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
+int srdct_tile_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
+                     int64_t ldsa, cudaStream_t st);
 
 namespace {
 
@@ -112,8 +114,13 @@ int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
 
 int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                double* SA, int64_t ldsa, cudaStream_t st) {
-  // Tiled single-pass FFT (srtt_tile.cu) when the shape allows, else the
-  // strided FFT (srtt_fast.cu), else the direct evaluator.
+  // srdct: Makhoul-paired tiles (srdct_tile.cu); then the tiled single-pass
+  // FFT (srtt_tile.cu) when the shape allows, else the strided FFT
+  // (srtt_fast.cu), else the direct evaluator.
+  if (op.kind == SRDCT && ncomp == 1) {
+    const int rd = srdct_tile_apply(op, rows, n, A, lda, SA, ldsa, st);
+    if (rd != NOTAPPLICABLE) return rd;
+  }
   const int rc = srtt_tile_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
   if (rc != NOTAPPLICABLE) return rc;
   return srtt_fast_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);

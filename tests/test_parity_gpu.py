@@ -91,6 +91,24 @@ def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
     assert rel(got, ref) <= SA_TOL
 
 
+@pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
+                                   (1500, 1 << 16, 9)])
+def test_srdct_makhoul_parity(nsk, oracle, s, m, n):
+    """Makhoul-paired srdct tiles (srdct_tile.cu, m % 16384 == 0) against scipy's DCT-III, and
+    against the zero-padded tile path on the same operator."""
+    import os
+    A = oracle.random_real(m, n, 13)
+    got, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
+    ref = oracle.apply(oracle.draw("srdct", s, m, 91), A)
+    assert rel(got, ref) <= SA_TOL
+    os.environ["NSK_SRDCT_NOMAKHOUL"] = "1"
+    try:
+        other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
+    finally:
+        del os.environ["NSK_SRDCT_NOMAKHOUL"]
+    assert rel(got, other) <= SA_TOL
+
+
 def test_srft_complex_parity(nsk, oracle, golden):
     sa = golden["sa"]
     A = sa["A_srft"]
