@@ -36,12 +36,17 @@ namespace {
 using namespace fft;
 
 constexpr int DL = 1024;      // FFT length
-constexpr int DW = 8;         // warps = k1 columns per tile
-constexpr int DT = 32 * DW;   // threads
-constexpr int RS = 18;        // doubles per staged row: 8 main | 9 mirror | pad (16-byte aligned, conflict-free)
-constexpr int RS2 = RS / 2;   // ... in double2
-constexpr int DNQ = 4;        // output slots per thread (DT * DNQ = 1024 per pass)
 constexpr int DANCHOR = 16;   // exact twiddles every DANCHOR tiles
+
+// W = k1 columns per tile = warps per CTA (8: one CTA per SM, the default; 4: two).
+template <int W>
+struct DTile {
+  static constexpr int T = 32 * W;       // threads
+  static constexpr int RS = 2 * W + 2;   // doubles per staged row: W main | W + 1 mirror | pad
+  static constexpr int RS2 = RS / 2;     // ... in double2 (odd: 16-byte aligned, conflict-free columns)
+  static constexpr int NQ = 1024 / T;    // output slots per thread (T * NQ = 1024 per pass)
+  static constexpr size_t SMEM = sizeof(double) * DL * RS + sizeof(double2) * DL + sizeof(uint32_t) * 3 * DL;
+};
 
 struct DctParams {
   const double* A;
@@ -49,7 +54,7 @@ struct DctParams {
   int64_t N;        // rows (transform length)
   int64_t n;        // columns
   int64_t P;        // N / DL
-  int64_t tiles;    // tiles per column: P / 16 + 1
+  int64_t tiles;    // tiles per column: P / (2 W) + 1
   int64_t per;      // tiles per work item
   int64_t ranges;   // work items per column
   const uint32_t* sign_bits;
@@ -84,27 +89,28 @@ __device__ __forceinline__ double sgn(uint32_t bits, int pos, double v) {
   return ((bits >> pos) & 1u) ? v : -v;  // Rademacher bit 1 -> +1 (rng.hpp:57)
 }
 
-__global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
+template <int W>
+__global__ void __launch_bounds__(32 * W, W == 4 ? 2 : 1) srdct_tile_kernel(DctParams p) {
+  using TT = DTile<W>;
+  constexpr int DT = TT::T, RS = TT::RS, RS2 = TT::RS2, DNQ = TT::NQ;
   extern __shared__ __align__(16) double smd[];
   double* U = smd;                                        // [DL][RS]
   double2* U2 = reinterpret_cast<double2*>(U);            // [DL][RS2]
   double2* tw = U2 + DL * RS2;                            // e^{2 pi i k / DL}
-  double2* tw4 = tw + DL;                                 // e^{i pi k / (2 DL)} = omega^{P k}
-  uint32_t* SBm = reinterpret_cast<uint32_t*>(tw4 + DL);  // main sign word per row
+  uint32_t* SBm = reinterpret_cast<uint32_t*>(tw + DL);   // main sign word per row
   uint32_t* SBr = SBm + DL;                               // mirror sign words per row (2)
-  __shared__ double2 om1[DW];                             // omega^{k1} of the tile's columns
+  __shared__ double2 om1[W];                              // omega^{k1} of the tile's columns
+  __shared__ double2 r4[4];                               // e^{2 pi i r / 4 DL}
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t N = static_cast<uint64_t>(p.N);
-  const int64_t P = p.P, half_tiles = P / 16;
+  const int64_t P = p.P, half_tiles = P / (2 * W);
   const double c0 = sqrt(1.0 / static_cast<double>(p.N)), c1 = sqrt(2.0 / static_cast<double>(p.N));
   const double rs2 = 0.70710678118654752440;
 
-  for (int k = threadIdx.x; k < DL; k += DT) {
-    tw[k] = unitq(static_cast<uint64_t>(k), DL);
-    double sn, cs;
-    sincospi(static_cast<double>(k) / (2.0 * DL), &sn, &cs);
-    tw4[k] = make_double2(cs, sn);
-  }
+  for (int k = threadIdx.x; k < DL; k += DT) tw[k] = unitq(static_cast<uint64_t>(k), DL);
+  if (threadIdx.x < 4) r4[threadIdx.x] = unitq(static_cast<uint64_t>(threadIdx.x), 4 * DL);
+  // omega^{P k2} = e^{i pi k2 / 2L} = tw[k2 / 4] * r4[k2 % 4]
+  auto wp = [&](int k2) { return cmul(tw[k2 >> 2], r4[k2 & 3]); };
   auto freq_of = [&](int q) -> uint64_t {
     const int o = threadIdx.x + DT * q;
     return o < p.nslots ? static_cast<uint64_t>(__ldg(p.freq + o)) : 0;
@@ -112,6 +118,7 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
   double2 step[DNQ];
 #pragma unroll
   for (int q = 0; q < DNQ; ++q) step[q] = unitq(freq_of(q) % N, N);  // W^n
+  __syncthreads();
 
   const int64_t items = p.n * p.ranges;
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
@@ -125,32 +132,32 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
 
     for (int64_t t = t0; t < t1; ++t) {
       const bool last = t == half_tiles;  // the tile of column P/2 alone
-      const int64_t K = last ? P / 2 : 8 * t;
-      const int64_t B0 = P - 8 * t - 8;   // mirror block start (main tiles)
+      const int64_t K = last ? P / 2 : W * t;
+      const int64_t B0 = P - W * t - W;   // mirror block start (main tiles): columns B0 .. B0 + W
       __syncthreads();                    // previous tile's reads of U are done
-      // ---- stage: main 8 elements + mirror 9 elements per row, sign words
-      for (int c = threadIdx.x; c < DL * 4; c += DT) {
-        const int k2 = c >> 2, ch = c & 3;
+      // ---- stage: W main + W + 1 mirror elements per row, sign words
+      for (int c = threadIdx.x; c < DL * (W / 2); c += DT) {
+        const int k2 = c / (W / 2), ch = c % (W / 2);
         const int64_t j0 = K + P * k2 + 2 * ch;
         cp_async16(U + k2 * RS + 2 * ch, Acol + (last ? (ch == 0 ? j0 : 0) : j0), last && ch ? 0 : 16);
         if (!last) {
-          const int64_t m0 = B0 + P * (DL - 1 - k2) + 2 * ch;  // mirror row L - 1 - k2 staged at row k2
-          cp_async16(U + k2 * RS + 8 + 2 * ch, Acol + m0, 16);
+          const int64_t m0 = B0 + P * (DL - 1 - k2) + 2 * ch;  // mirror block of global row L - 1 - k2
+          cp_async16(U + k2 * RS + W + 2 * ch, Acol + m0, 16);
         }
       }
       for (int k2 = threadIdx.x; k2 < DL; k2 += DT) {
         const uint64_t jm = static_cast<uint64_t>(K + P * k2);
         cp_async4(SBm + k2, p.sign_bits + (jm >> 5), 4);
         if (!last) {
-          const uint64_t j8 = static_cast<uint64_t>(B0 + P * (DL - 1 - k2) + 8);  // 9th mirror element
-          cp_async8(U + k2 * RS + 16, Acol + (j8 < N ? j8 : 0), j8 < N ? 8 : 0);
           const uint64_t jr = static_cast<uint64_t>(B0 + P * (DL - 1 - k2));
+          const uint64_t jW = jr + W;  // the (W+1)-th mirror element
+          cp_async8(U + k2 * RS + 2 * W, Acol + (jW < N ? jW : 0), jW < N ? 8 : 0);
           cp_async4(SBr + 2 * k2, p.sign_bits + (jr >> 5), 4);
-          const uint64_t w1 = (jr + 8) >> 5;
+          const uint64_t w1 = jW >> 5;
           cp_async4(SBr + 2 * k2 + 1, p.sign_bits + (w1 < (N + 31) / 32 ? w1 : 0), 4);
         }
       }
-      if (threadIdx.x < DW) {
+      if (threadIdx.x < W) {
         double sn, cs;
         sincospi(static_cast<double>(K + threadIdx.x) / (2.0 * static_cast<double>(p.N)), &sn, &cs);
         om1[threadIdx.x] = make_double2(cs, sn);  // omega^{k1}
@@ -158,16 +165,16 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncthreads();
 
-      // ---- column 0 of tile 0 (k1 = 0, self-mirrored by k2 <-> L - k2): compute first
-      double2 e0[DL / DT];
+      // ---- column 0 of tile 0 (k1 = 0, self-mirrored by k2 <-> L - k2): computed first
+      constexpr int E0 = DL / DT;
+      double2 e0[E0];
       const bool col0 = t == 0;
       if (col0) {
 #pragma unroll
-        for (int i = 0; i < DL / DT; ++i) {
+        for (int i = 0; i < E0; ++i) {
           const int k2 = threadIdx.x + DT * i;
           double2 v = make_double2(0.0, 0.0);
-          const int sh = static_cast<int>((P * k2) & 31);
-          const double x = sgn(SBm[k2], sh, U[k2 * RS]);
+          const double x = sgn(SBm[k2], static_cast<int>((P * k2) & 31), U[k2 * RS]);
           if (k2 == 0) {
             v = make_double2(0.5 * c0 * x, 0.0);
           } else if (k2 == DL / 2) {
@@ -175,27 +182,26 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
           } else if (k2 < DL / 2) {
             const int k2m = DL - k2;  // N - P k2 = P (L - k2)
             const double xm = sgn(SBm[k2m], static_cast<int>((P * k2m) & 31), U[k2m * RS]);
-            const double2 a = make_double2(0.5 * c1 * x, -0.5 * c1 * xm);  // (X_k - i X_{N-k}) / 2
-            v = cmul(a, tw4[k2]);  // omega^{P k2}
+            v = cmul(make_double2(0.5 * c1 * x, -0.5 * c1 * xm), wp(k2));  // (X_k - i X_{N-k}) omega^k / 2
           }
           e0[i] = v;
         }
       }
       __syncthreads();
-      // ---- G in place: thread owns the row pair (k2, L - 1 - k2)
+      // ---- G in place: a thread owns the row pair (k2, L - 1 - k2)
       for (int k2 = threadIdx.x; k2 < DL / 2; k2 += DT) {
         const int k2b = DL - 1 - k2;
-        double ma[8], mb[8], ra[9], rb[9];
+        double ma[W], mb[W], ra[W + 1], rb[W + 1];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < W; ++j) {
           ma[j] = U[k2 * RS + j];
           mb[j] = U[k2b * RS + j];
         }
         if (!last) {
 #pragma unroll
-          for (int i = 0; i < 9; ++i) {
-            ra[i] = U[k2 * RS + 8 + i];   // mirror block of global row k2b: partners of main row k2
-            rb[i] = U[k2b * RS + 8 + i];  // mirror block of global row k2: partners of main row k2b
+          for (int i = 0; i <= W; ++i) {
+            ra[i] = U[k2 * RS + W + i];   // mirror block of global row k2b: partners of main row k2
+            rb[i] = U[k2b * RS + W + i];  // mirror block of global row k2: partners of main row k2b
           }
         }
         const uint32_t sma = SBm[k2], smb = SBm[k2b];
@@ -205,21 +211,20 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
         if (!last) {
           sra = static_cast<uint64_t>(SBr[2 * k2]) | (static_cast<uint64_t>(SBr[2 * k2 + 1]) << 32);
           srb = static_cast<uint64_t>(SBr[2 * k2b]) | (static_cast<uint64_t>(SBr[2 * k2b + 1]) << 32);
-          shra = static_cast<int>((B0 + P * k2b) & 31);  // staged at row k2: global row L - 1 - k2 = k2b
+          shra = static_cast<int>((B0 + P * k2b) & 31);
           shrb = static_cast<int>((B0 + P * k2) & 31);
         }
-        const double2 wa = tw4[k2], wb = tw4[k2b];
+        const double2 wa = wp(k2), wb = wp(k2b);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < W; ++j) {
           if (col0 && j == 0) continue;  // column 0 written from e0 below
           double2 ga = make_double2(0.0, 0.0), gb = make_double2(0.0, 0.0);
           if (!last) {
-            // staged row r holds the mirror block of global row L - 1 - r, i.e. the
-            // partners of main row r: element 8 - j is column P - K - j
+            // mirror element W - j of a staged row is column P - K - j (the partner of column K + j)
             const double xa = c1 * sgn(sma, sha + j, ma[j]);
-            const double xma = c1 * (((sra >> (shra + 8 - j)) & 1u) ? ra[8 - j] : -ra[8 - j]);
+            const double xma = c1 * (((sra >> (shra + W - j)) & 1u) ? ra[W - j] : -ra[W - j]);
             const double xb = c1 * sgn(smb, shb + j, mb[j]);
-            const double xmb = c1 * (((srb >> (shrb + 8 - j)) & 1u) ? rb[8 - j] : -rb[8 - j]);
+            const double xmb = c1 * (((srb >> (shrb + W - j)) & 1u) ? rb[W - j] : -rb[W - j]);
             const double2 om = om1[j];
             ga = cmul(cmul(make_double2(0.5 * xa, -0.5 * xma), om), wa);
             gb = cmul(cmul(make_double2(0.5 * xb, -0.5 * xmb), om), wb);
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
       __syncthreads();
       if (col0) {
 #pragma unroll
-        for (int i = 0; i < DL / DT; ++i) U2[(threadIdx.x + DT * i) * RS2] = e0[i];
+        for (int i = 0; i < E0; ++i) U2[(threadIdx.x + DT * i) * RS2] = e0[i];
       }
       __syncthreads();
       // ---- warp `warp`: in-place 1024-point FFT of column `warp`
@@ -267,18 +272,18 @@ __global__ void __launch_bounds__(DT, 1) srdct_tile_kernel(DctParams p) {
         double2 w = base[q];
         const int qi = static_cast<int>(f & (DL - 1));
         const double2 st = step[q];
-        double s = 0.0;
-        const int jn = last ? 1 : 8;
+        double sacc = 0.0;
+        const int jn = last ? 1 : W;
         for (int j = 0; j < jn; ++j) {
           const double2 F = U2[qi * RS2 + j];
-          s = fma(w.x, F.x, fma(-w.y, F.y, s));
+          sacc = fma(w.x, F.x, fma(-w.y, F.y, sacc));
           w = cmul(w, st);
         }
-        acc[q] += s;
-        base[q] = w;  // W^{n (K + 8)}
+        acc[q] += sacc;
+        base[q] = w;  // W^{n (K + W)}
       }
     }
-    double* part = p.part + (col * p.ranges + range) * (DNQ * DT);
+    double* part = p.part + (col * p.ranges + range) * 1024;
 #pragma unroll
     for (int q = 0; q < DNQ; ++q) part[threadIdx.x + DT * q] = acc[q];
   }
@@ -312,32 +317,37 @@ int srdct_tile_apply(const Operator& op, const RowMap& rows, int64_t n, const do
   if ((reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0) return NOTAPPLICABLE;
   const DeviceTables* tb = op.tables();
   if (!tb || !tb->sign_bits || !tb->dct_freq || !tb->dct_row) return ECUDA;
-  const int64_t P = m / DL, tiles = P / 16 + 1;
-  // work items (column, tile range): about two waves of one CTA per SM
-  const int64_t sms = sm_count();
-  int64_t ranges = (2 * sms + n - 1) / n;
+  // tile width: 8 columns, one CTA of 8 warps per SM (NSK_SRDCT_W=4: two CTAs of 4 warps,
+  // measured 1.5x slower -- the per-tile sampled stage and barriers are paid twice as often)
+  const char* we = std::getenv("NSK_SRDCT_W");
+  const int W = we && std::atoi(we) == 4 ? 4 : 8;
+  const int64_t P = m / DL, tiles = P / (2 * W) + 1;
+  const int per_sm = W == 4 ? 2 : 1;
+  // work items (column, tile range): about two waves of resident CTAs
+  const int64_t slots = sm_count() * per_sm;
+  int64_t ranges = (2 * slots + n - 1) / n;
   if (ranges > tiles) ranges = tiles;
   const int64_t per = (tiles + ranges - 1) / ranges;
   ranges = (tiles + per - 1) / per;
   const int64_t items = n * ranges;
-  const size_t smem = sizeof(double) * DL * RS + sizeof(double2) * 2 * DL + sizeof(uint32_t) * 3 * DL;
-  NSK_CUDA_OK(cudaFuncSetAttribute(srdct_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
+  const size_t smem = W == 4 ? DTile<4>::SMEM : DTile<8>::SMEM;
+  auto kern = W == 4 ? srdct_tile_kernel<4> : srdct_tile_kernel<8>;
+  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const double scale = 2.0 * std::sqrt(static_cast<double>(m) / static_cast<double>(s));
-  for (int64_t b = 0; b < s; b += DNQ * DT) {
-    const int ns = static_cast<int>((s - b) < DNQ * DT ? (s - b) : DNQ * DT);
+  for (int64_t b = 0; b < s; b += 1024) {
+    const int ns = static_cast<int>((s - b) < 1024 ? (s - b) : 1024);
     Scratch part;
-    NSK_CUDA_OK(part.alloc(sizeof(double) * items * DNQ * DT, st));
+    NSK_CUDA_OK(part.alloc(sizeof(double) * items * 1024, st));
     DctParams p{A, lda, m, n, P, tiles, per, ranges, tb->sign_bits, tb->dct_freq + b, ns, part.as<double>()};
-    const int64_t grid = items < sms ? items : sms;
+    const int64_t grid = items < slots ? items : slots;
     KernelTimer tm(st);
-    srdct_tile_kernel<<<static_cast<unsigned>(grid), DT, smem, st>>>(p);
+    kern<<<static_cast<unsigned>(grid), 32 * W, smem, st>>>(p);
     tm.stop();
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
     int64_t blocks = (n * ns + 255) / 256;
-    if (blocks > 8L * sms) blocks = 8L * sms;
-    srdct_tile_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double>(), ranges, n, ns, DNQ * DT,
+    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+    srdct_tile_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double>(), ranges, n, ns, 1024,
                                                                      tb->dct_row + b, scale, SA, ldsa);
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
