@@ -31,10 +31,10 @@ namespace {
 using namespace fft;
 
 constexpr int TL = 1024;        // FFT length
-constexpr int TW = 4;           // complex sequences per tile (one warp each)
+constexpr int TW = 8;           // complex sequences per tile (one warp each)
 constexpr int TT = 32 * TW;     // threads per CTA
 constexpr int TROW = TW + 1;    // complex slots per shared-memory row (padded: conflict-free columns)
-constexpr int TNQ = 8;          // output slots per thread (TT * TNQ = 1024 per pass)
+constexpr int TNQ = 1024 / TT;  // output slots per thread (TT * TNQ = 1024 per pass)
 constexpr int TANCHOR = 16;     // exact twiddles every TANCHOR tiles
 
 struct TileParams {
@@ -74,7 +74,7 @@ __device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t N) {
 
 // KIND 0 srft, 1 srdct; NCIN 1 real input (pairs), 2 complex input.
 template <int KIND, int NCIN>
-__global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
+__global__ void __launch_bounds__(TT, TW == 8 ? 1 : 2) srtt_tile_kernel(TileParams p) {
   extern __shared__ __align__(16) double2 sm2[];
   double2* U = sm2;                 // [TL][TROW]
   double2* tw = U + TL * TROW;      // w_1024^k, k < 1024
@@ -113,9 +113,9 @@ __global__ void __launch_bounds__(TT, 2) srtt_tile_kernel(TileParams p) {
   for (int64_t t = t0; t < t1; ++t) {
     const int64_t K = t * KT;  // first k1 of the tile
     __syncthreads();           // previous tile's reads of U are done
-    // ---- stage rows k2 < ROWS: 64 contiguous bytes each (4 x 16 B)
-    for (int c = threadIdx.x; c < ROWS * 4; c += TT) {
-      const int k2 = c >> 2, ch = c & 3;
+    // ---- stage rows k2 < ROWS: 16 TW contiguous bytes each (TW x 16 B)
+    for (int c = threadIdx.x; c < ROWS * TW; c += TT) {
+      const int k2 = c / TW, ch = c % TW;
       cp_async16(U + k2 * TROW + ch, Acol + (K + p.P * k2) * NCIN + 2 * ch);
     }
     for (int k2 = threadIdx.x; k2 < ROWS; k2 += TT)  // sign word of each row (bits K .. K + KT - 1)
