@@ -160,6 +160,71 @@ int copy_in(const void* host, int64_t rows, int64_t cols, int64_t ld, int ncomp,
   return nsk::OK;
 }
 
+cudaStream_t copy_stream() {
+  thread_local cudaStream_t cs = nullptr;
+  thread_local int dev = -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (!cs || dev != cur) {
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    dev = cur;
+  }
+  return cs;
+}
+
+// Host A (m x n, lda) -> SA (device, s x n, ld s).  Large inputs of the
+// row-sharded kinds (gaussian, srht, countsketch) are copied in row chunks on
+// a copy stream and each chunk is sketched (a row-shard apply) as soon as it
+// has landed, so the PCIe transfer overlaps the sketch; the chunk partials
+// are summed in chunk order (deterministic).  Everything else: copy, then
+// apply.  a_buf receives the device copy of A.
+int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void* A, int64_t lda, nsk::Scratch& a_buf,
+                double* SA, cudaStream_t st) {
+  const int nc_out = out_ncomp(op, nc_in);
+  const size_t elem = sizeof(double) * nc_in;
+  const int64_t align = op.kind == nsk::GAUSSIAN ? 16 : op.kind == nsk::SRHT ? 2048 : op.kind == nsk::COUNTSKETCH ? 12288 : 0;
+  constexpr int64_t CHUNKS = 8;
+  const int64_t chunk = align ? ((m + CHUNKS - 1) / CHUNKS + align - 1) / align * align : 0;
+  const bool big = static_cast<double>(m) * static_cast<double>(n) * static_cast<double>(elem) >= 256.0 * (1 << 20);
+  const bool pipelined = align && big && chunk < m && op.appended == 0 && op.zeroed.empty() &&
+                         (op.kind != nsk::SRHT || m % 2048 == 0) && !std::getenv("NSK_NO_PIPELINE");
+  double* dA = nullptr;
+  if (!pipelined) {
+    if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a_buf, st)) return rc;
+    nsk::RowMap rows{0, 1, m};
+    return dispatch_apply(op, nc_in, rows, n, dA, m, SA, op.s, st);
+  }
+  NSK_CUDA_OK(a_buf.alloc(elem * m * n, st));
+  dA = a_buf.as<double>();
+  const int64_t nchunks = (m + chunk - 1) / chunk;
+  nsk::Scratch parts;
+  const int64_t psz = op.s * n * nc_out;
+  NSK_CUDA_OK(parts.alloc(sizeof(double) * psz * nchunks, st));
+  cudaStream_t cs = copy_stream();
+  cudaEvent_t ready;
+  NSK_CUDA_OK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  NSK_CUDA_OK(cudaEventRecord(ready, st));  // the stream-ordered allocations exist before the copies
+  NSK_CUDA_OK(cudaStreamWaitEvent(cs, ready, 0));
+  cudaEventDestroy(ready);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t r0 = c * chunk, rows = m - r0 < chunk ? m - r0 : chunk;
+    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * nc_in, elem * m, static_cast<const char*>(A) + r0 * elem, elem * lda,
+                                  elem * rows, n, cudaMemcpyHostToDevice, cs));
+    cudaEvent_t landed;
+    NSK_CUDA_OK(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
+    NSK_CUDA_OK(cudaEventRecord(landed, cs));
+    NSK_CUDA_OK(cudaStreamWaitEvent(st, landed, 0));
+    cudaEventDestroy(landed);
+    nsk::RowMap shard{r0, 1, rows};
+    if (int rc = dispatch_main(op, nc_in, shard, n, dA + r0 * nc_in, m, parts.as<double>() + c * psz, op.s, st))
+      return rc;
+  }
+  NSK_CUDA_OK(cudaMemcpyAsync(SA, parts.as<double>(), sizeof(double) * psz, cudaMemcpyDeviceToDevice, st));
+  for (int64_t c = 1; c < nchunks; ++c)
+    if (int rc = nsk::accumulate(SA, op.s, nc_out, parts.as<double>() + c * psz, op.s, n, nc_out, st)) return rc;
+  return nsk::OK;
+}
+
 int copy_out(void* host, int64_t ld, const double* dev, int64_t rows, int64_t cols, int ncomp, cudaStream_t st) {
   const size_t elem = sizeof(double) * ncomp;
   if (rows > 0 && cols > 0)
@@ -385,11 +450,8 @@ int nsk_apply_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, cons
   cudaStream_t st = host_stream();
   const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc_out = out_ncomp(op, nc_in);
   nsk::Scratch a, sa;
-  double* dA = nullptr;
-  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
   NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * (n > 0 ? n : 1) * nc_out, st));
-  nsk::RowMap rows{0, 1, m};
-  if (int rc = dispatch_apply(op, nc_in, rows, n, dA, m, sa.as<double>(), op.s, st)) return rc;
+  if (int rc = host_sketch(op, nc_in, m, n, A, lda, a, sa.as<double>(), st)) return rc;
   if (int rc = copy_out(SA, ldsa, sa.as<double>(), op.s, n, nc_out, st)) return rc;
   NSK_CUDA_OK(cudaStreamSynchronize(st));
   return nsk::OK;
@@ -405,12 +467,19 @@ int nsk_solve_k_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, co
                                        ", n = " + std::to_string(n));
   cudaStream_t st = host_stream();
   const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc_out = out_ncomp(op, nc_in);
-  nsk::Scratch a, w, sg;
-  double* dA = nullptr;
-  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
+  if (n < 1) return nsk::fail(nsk::EINVAL_, "nullspace: matrix has no columns");
+  if (m != op.m_eff()) return nsk::fail(nsk::EINVAL_, "nullspace: matrix rows do not match the sketch operator");
+  if (op.s < n)
+    return nsk::fail(nsk::EINVAL_, "nullspace: sketch size s = " + std::to_string(op.s) + " is smaller than n = " +
+                                       std::to_string(n));
+  if (int rc = validate_apply(op, scalar, m, n, A, lda, reinterpret_cast<const void*>(1), op.s, false)) return rc;
+  nsk::Scratch a, sa, w, sg;
+  NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * n * nc_out, st));
+  if (int rc = host_sketch(op, nc_in, m, n, A, lda, a, sa.as<double>(), st)) return rc;
   NSK_CUDA_OK(w.alloc(sizeof(double) * n * (k > 0 ? k : 1) * nc_out, st));
   NSK_CUDA_OK(sg.alloc(sizeof(double) * n, st));
-  if (int rc = nsk_solve_k(h, scalar, m, n, dA, m, k, w.as<double>(), n, sg.as<double>(), st)) return rc;
+  if (int rc = nsk::jacobi_trailing(nc_out, op.s, n, sa.as<double>(), op.s, k, w.as<double>(), n, sg.as<double>(), st))
+    return rc;
   if (int rc = copy_out(W, ldw, w.as<double>(), n, k, nc_out, st)) return rc;
   NSK_CUDA_OK(cudaMemcpyAsync(sigma, sg.as<double>(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
   NSK_CUDA_OK(cudaStreamSynchronize(st));

@@ -462,3 +462,28 @@ def test_cfg5_loewner_complex_gaussian(nsk, oracle):
     assert np.max(np.abs(host(res.sketched_singular_values) - sref)) <= 1000 * U * sref[0]
     SA = host(nsk.apply(S, dev(L)).data)
     assert rel(SA, oracle.apply(oracle.draw("gaussian", 2 * n, m, 9000005), L)) <= SA_TOL
+
+
+@pytest.mark.parametrize("kind,s", [("gaussian", 64), ("srht", 256), ("countsketch", 4096)])
+def test_host_pipelined_sketch(nsk, oracle, kind, s):
+    """Host entry points on >= 256 MiB inputs copy A in row chunks and sketch each chunk as it
+    lands (capi.cpp host_sketch): same SA as the device path to summation-order rounding, and
+    solve_k through the host API agrees with the device API."""
+    import os
+    m, n = 1 << 21, 16
+    rng = np.random.default_rng(5)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    S = nsk.SketchOperator.draw(kind, s, m, 17)
+    got = nsk.apply(S, A).data
+    ref = host(nsk.apply(S, dev(A)).data)
+    assert rel(got, ref) <= 1e-13
+    os.environ["NSK_NO_PIPELINE"] = "1"
+    try:
+        plain = nsk.apply(S, A).data
+    finally:
+        del os.environ["NSK_NO_PIPELINE"]
+    assert np.array_equal(plain, ref)
+    r_host = nsk.solve_k(A, 1, S)
+    r_dev = nsk.solve_k(dev(A), 1, S)
+    assert np.max(np.abs(np.asarray(r_host.sketched_singular_values) - host(r_dev.sketched_singular_values))) \
+        <= 1e-12 * float(np.max(np.asarray(r_host.sketched_singular_values)))
