@@ -789,17 +789,25 @@ int nsk_tls_solve_sketched_host(const nsk_operator* h, int scalar, int64_t m, in
   if (int rc = check_op(h)) return rc;
   const Operator& op = *OP(h);
   if (lda < m || ldb < m || k < 1 || n < 1) return nsk::fail(nsk::EINVAL_, "tls: bad dimensions");
+  if (n < k) return nsk::fail(nsk::EINVAL_, "tls: need n >= k");
+  if (m < n + k) return nsk::fail(nsk::EINVAL_, "tls: need m >= n + k");
+  if (op.m_eff() != m) return nsk::fail(nsk::EINVAL_, "tls: sketch operator row count does not match [A|B]");
+  if (op.s < n + k) return nsk::fail(nsk::EINVAL_, "tls: sketch size below n + k");
+  if (int rc = validate_apply(op, scalar, m, n, A, lda, reinterpret_cast<const void*>(1), op.s, false)) return rc;
+  if (int rc = validate_apply(op, scalar, m, k, B, ldb, reinterpret_cast<const void*>(1), op.s, false)) return rc;
+  if (!info) return nsk::fail(nsk::EINVAL_, "tls: bad outputs");
   cudaStream_t st = host_stream();
   const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_ncomp(op, nc_in);
-  nsk::Scratch a, b, x, v, sg;
-  double *dA = nullptr, *dB = nullptr;
-  if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a, st)) return rc;
-  if (int rc = copy_in(B, m, k, ldb, nc_in, &dB, b, st)) return rc;
+  nsk::Scratch a, b, sa, x, v, sg;
+  // S [A | B] straight from host memory: A's H2D overlaps its sketch (host_sketch)
+  NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * (n + k) * nc, st));
+  if (int rc = host_sketch(op, nc_in, m, n, A, lda, a, sa.as<double>(), st)) return rc;
+  if (int rc = host_sketch(op, nc_in, m, k, B, ldb, b, sa.as<double>() + op.s * n * nc, st)) return rc;
   NSK_CUDA_OK(x.alloc(sizeof(double) * n * k * nc, st));
   NSK_CUDA_OK(v.alloc(sizeof(double) * (n + k) * k * nc, st));
   NSK_CUDA_OK(sg.alloc(sizeof(double) * (n + k), st));
-  const int rc = nsk_tls_solve_sketched(h, scalar, m, n, k, dA, m, dB, m, cond_limit, allow_marginal, x.p, n, v.p,
-                                        n + k, sg.as<double>(), info, st);
+  const int rc = tls_finish(nc, op.s, sa.as<double>(), op.s, n, k, cond_limit, allow_marginal, x.p, n, v.p, n + k,
+                            sg.as<double>(), info, st);
   if (rc != NSK_OK && rc != NSK_ETLS_CONDITION) return rc;
   if (rc == NSK_OK && X) {
     if (int r2 = copy_out(X, ldx, x.as<double>(), n, k, nc, st)) return r2;
