@@ -91,7 +91,14 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
   extern __shared__ double zbuf[];  // [WARPS_PER_CTA][PAD]
   __shared__ uint32_t sslot[NQ * 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x) sslot[t] = t < p.nslots ? p.slot[t] : 0u;
+  // Slots in shared memory, packed: the padded z offset r_lo + r_lo / 32
+  // (< 2^12) in the low 12 bits, r_hi (< 2^20, host-checked) above, so the
+  // gather is one AND for the offset and one AND + POPC for the parity.
+  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x) {
+    const uint32_t v = t < p.nslots ? p.slot[t] : 0u;
+    const uint32_t rlo = v & (L - 1), rhi = v >> LB;
+    sslot[t] = (rlo + (rlo >> 5)) | (rhi << 12);
+  }
   __syncthreads();
 
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * WARPS_PER_CTA + wib;
@@ -197,14 +204,12 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
     }
     __syncwarp();
     // Sampled second stage: acc += (-1)^popc(r_hi & j_hi) Z[r_lo].
-    const uint32_t jh = static_cast<uint32_t>(jhi);
+    const uint32_t jh12 = static_cast<uint32_t>(jhi) << 12;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const uint32_t v = sslot[q * 32 + lane];
-      const uint32_t rlo = v & (L - 1), rhi = v >> LB;
-      const double zz = z[rlo + (rlo >> 5)];
-      // (-1)^popc(r_hi & j_hi) applied to the sign bit (no selects)
-      const int par = static_cast<int>(__popc(rhi & jh) << 31);
+      const double zz = z[v & 0xfffu];
+      const int par = static_cast<int>(__popc(v & jh12) << 31);  // (-1)^popc(r_hi & j_hi) on the sign bit
       acc[q] += __hiloint2double(__double2hiint(zz) ^ par, __double2loint(zz));
     }
     __syncwarp();
@@ -303,7 +308,7 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
   if (!(op.m >= 2048 && mloc % 2048 == 0 && rows.row0 % 2048 == 0)) lb = 10;
   const int64_t L = int64_t(1) << lb;
   const bool blocked = op.m >= L && mloc >= L && (mloc % L) == 0 && (rows.row0 % L) == 0 &&
-                       tb->sign_mask != nullptr;
+                       tb->sign_mask != nullptr && (op.m >> lb) < (int64_t(1) << 20);  // packed slot words
   if (!blocked) {
     int64_t blocks = (s * n + 127) / 128;
     if (blocks > 16L * sm_count()) blocks = 16L * sm_count();
