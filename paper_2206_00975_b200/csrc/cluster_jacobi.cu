@@ -74,7 +74,9 @@ __device__ __forceinline__ void round_robin(int N, int r, int i, int& p, int& q)
 // Shared-memory bookkeeping of the block circle (one copy per CTA).
 struct Circle {
   int slotbuf[2];                  // block buffer of the top / bottom slot
-  int inbox[2];                    // [0] filled by the left CTA, [1] by the right CTA
+  int inbox[2];                    // [0] filled by the left CTA, [1] by the right CTA (nb = 3: [0] = free buffer)
+  int nb;                          // block buffers per CTA: 4 (two inboxes) or 3 (one free buffer, two-phase moves)
+  int sentA;                       // nb = 3: buffer sent right in phase A of the current move
   int blockid[4];                  // block held by each buffer
   int rotated;                     // any rotation in this CTA and sweep
   int sweep_rot[16];               // CTA 0: per-CTA flags of the finished sweep
@@ -82,7 +84,7 @@ struct Circle {
 };
 
 // Initial state: CTA c holds blocks 2c (top, buffer 0) and 2c + 1 (bottom, buffer 1).
-__device__ void circle_init(Circle& cc, int c, int b) {
+__device__ void circle_init(Circle& cc, int c, int b, int nb = 4) {
   const int twob = 2 * b;
   for (int e = threadIdx.x; e < (twob - 1) * b; e += blockDim.x) {
     int lp, lq;
@@ -94,7 +96,9 @@ __device__ void circle_init(Circle& cc, int c, int b) {
     cc.slotbuf[0] = 0;
     cc.slotbuf[1] = 1;
     cc.inbox[0] = 2;
-    cc.inbox[1] = 3;
+    cc.inbox[1] = nb == 4 ? 3 : -1;
+    cc.nb = nb;
+    cc.sentA = -1;
     cc.blockid[0] = 2 * c;
     cc.blockid[1] = 2 * c + 1;
     cc.blockid[2] = cc.blockid[3] = -1;
@@ -171,6 +175,52 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
       if (C == 1) continue;  // a single block pair: nothing moves
       // ---- outer move (circle method on blocks): copy the blocks crossing a CTA boundary
       cluster_wait();  // neighbours renamed after the previous move
+      if (cc.nb == 3) {
+        // Three buffers per CTA (two live blocks + one free): the move runs in
+        // two phases.  A: every CTA but the last sends its right-going block
+        // (CTA 0: bottom, others: top) into the right neighbour's free buffer.
+        // B: every CTA but the first sends its bottom block into the buffer its
+        // left neighbour emptied in phase A.
+        if (c + 1 < C) {
+          const int sb = cc.slotbuf[c == 0 ? 1 : 0];
+          Circle* rc = cluster.map_shared_rank(&cc, c + 1);
+          const int db = rc->inbox[0];
+          const double2* s2 = reinterpret_cast<const double2*>(buf + sb * blksz);
+          double2* d2 = reinterpret_cast<double2*>(cluster.map_shared_rank(buf, c + 1) + db * blksz);
+          for (int e = threadIdx.x; e < blksz / 2; e += nthr) d2[e] = s2[e];
+          if (threadIdx.x == 0) {
+            rc->blockid[db] = cc.blockid[sb];
+            cc.sentA = sb;
+          }
+        }
+        cluster_arrive();
+        cluster_wait();  // phase A landed, sentA published
+        if (c > 0) {
+          const int sb = cc.slotbuf[1];
+          Circle* lc = cluster.map_shared_rank(&cc, c - 1);
+          const int db = lc->sentA;
+          const double2* s2 = reinterpret_cast<const double2*>(buf + sb * blksz);
+          double2* d2 = reinterpret_cast<double2*>(cluster.map_shared_rank(buf, c - 1) + db * blksz);
+          for (int e = threadIdx.x; e < blksz / 2; e += nthr) d2[e] = s2[e];
+          if (threadIdx.x == 0) lc->blockid[db] = cc.blockid[sb];
+        }
+        cluster_arrive();
+        cluster_wait();  // phase B landed
+        if (threadIdx.x == 0) {
+          const int ot = cc.slotbuf[0], ob = cc.slotbuf[1], fr = cc.inbox[0];
+          if (c == 0) {
+            // bottom sent in A, refilled from the right in B (same buffer): nothing renames
+          } else if (c == C - 1) {  // top from the left (free buffer), old top -> bottom, old bottom sent
+            cc.slotbuf[0] = fr;
+            cc.slotbuf[1] = ot;
+            cc.inbox[0] = ob;
+          } else {  // top from the left (free buffer), bottom from the right (into the old top), old bottom sent
+            cc.slotbuf[0] = fr;
+            cc.slotbuf[1] = ot;
+            cc.inbox[0] = ob;
+          }
+        }
+      } else {
       if (c + 1 < C) {  // right: CTA 0 sends its bottom block (-> top[1]), the others their top block
         const int sb = cc.slotbuf[c == 0 ? 1 : 0];
         Circle* rc = cluster.map_shared_rank(&cc, c + 1);
@@ -208,6 +258,7 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
           cc.inbox[0] = ot;
           cc.inbox[1] = ob;
         }
+      }
       }
       __syncthreads();
       cluster_arrive();  // split barrier: closed by the next move's copy phase
@@ -329,11 +380,12 @@ __device__ __forceinline__ void push_candidate(cg::cluster_group& cluster, doubl
   }
 }
 
-// RPL = rows per lane of the register-resident QRCP step (n <= 32 RPL).
-template <int NC, int RPL>
+// RPL = rows per lane of the register-resident QRCP step (n <= 32 RPL);
+// NB = block buffers per CTA (4, or 3 when four do not fit: two-phase moves).
+template <int NC, int RPL, int NB>
 __global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  // b <= RPL
   cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ __align__(16) double buf[];  // [4 block buffers][b][n * NC], phys[n]
+  extern __shared__ __align__(16) double buf[];  // [NB block buffers][b][n * NC], phys[n]
   __shared__ Circle cc;
   __shared__ double cand_val[2][256];  // [step parity][CTA * b + warp]: remaining squared norm
   __shared__ int cand_idx[2][256];     //                                 and its global slot
@@ -341,13 +393,13 @@ __global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  //
   const int c = static_cast<int>(cluster.block_rank()), C = static_cast<int>(cluster.num_blocks());
   const int n = p.n, colsz = n * NC, b = p.b, twob = 2 * b, blksz = b * colsz;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
-  int* phys = reinterpret_cast<int*>(buf + 4 * blksz);
+  int* phys = reinterpret_cast<int*>(buf + NB * blksz);
   const int gbase = c * twob;  // global slot of local slot 0
   auto slot = [&](int li) { return buf + (li / b) * blksz + (li % b) * colsz; };
   auto stage = [&](int g) { return p.X + static_cast<int64_t>(g) * 2 * colsz + colsz; };  // V rows of column g
 
   stamp(p.stamps, 0);
-  circle_init(cc, c, b);
+  circle_init(cc, c, b, NB);
   for (int e = threadIdx.x; e < twob * colsz; e += nthr) {  // R columns (rows [0, n) of X)
     const int li = e / colsz, g = gbase + li;
     slot(li)[e % colsz] = g < n ? __ldcg(p.X + static_cast<int64_t>(g) * 2 * colsz + e % colsz) : 0.0;
@@ -572,31 +624,29 @@ __global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  //
   cluster.sync();  // R' complete in every CTA
   stamp(p.stamps, 1);
 
-  // ---- 2. X = R'^H into buffers 2, 3: slot li gets conj(row lg[li] of R')
+  // ---- 2. X = R'^H: R' goes out to the R rows of the global X (the V rows
+  // held the pivot staging, no longer needed), then slot li gathers conj(row
+  // lg[li] of R') from L2 into its own buffer -- no DSMEM reads, and the
+  // slot buffers are reused in place (three buffers suffice).
+  for (int e = threadIdx.x; e < twob * colsz; e += nthr) {
+    const int li = e / colsz, g = gbase + li;
+    if (g < n) p.X[static_cast<int64_t>(g) * 2 * colsz + e % colsz] = slot(li)[e % colsz];
+  }
+  cluster.sync();  // R' in global memory, visible to the whole cluster
   for (int e = threadIdx.x; e < twob * n; e += nthr) {
     const int li = e / n, r = e % n, i = lg[li];
-    double* y = buf + (2 + li / b) * blksz + (li % b) * colsz + r * NC;
     double vr = 0.0, vi = 0.0;
     if (i >= 0 && r >= i) {
-      const int g = phys[r], o = g / twob, lo = g % twob;
-      const double* src = cluster.map_shared_rank(buf, o) + (lo / b) * blksz + (lo % b) * colsz + i * NC;
-      vr = src[0];
-      if (NC == 2) vi = -src[1];
+      const double* src = p.X + static_cast<int64_t>(phys[r]) * 2 * colsz + i * NC;
+      vr = __ldcg(src);
+      if (NC == 2) vi = -__ldcg(src + 1);
     }
+    double* y = slot(li) + r * NC;
     y[0] = vr;
     if (NC == 2) y[1] = vi;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    cc.slotbuf[0] = 2;
-    cc.slotbuf[1] = 3;
-    cc.inbox[0] = 0;
-    cc.inbox[1] = 1;
-    cc.blockid[2] = 2 * c;
-    cc.blockid[3] = 2 * c + 1;
-    cc.blockid[0] = cc.blockid[1] = -1;
-  }
-  cluster.sync();  // every CTA finished reading R' before buffers 0, 1 become inboxes
+  cluster.sync();
 
   // ---- 3. one-sided Jacobi on X (no V accumulation)
   stamp(p.stamps, 2);
@@ -684,16 +734,28 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
   if (C > 16) C = 16;
   const int b = static_cast<int>((n + 2 * C - 1) / (2 * C));
   if (b > 16) return NOTAPPLICABLE;
-  const size_t smem = sizeof(double) * static_cast<size_t>(4 * b) * n * ncomp + sizeof(int) * n;
-  if (smem > 200 * 1024 || n > 512) return NOTAPPLICABLE;
+  // four block buffers when they fit, else three (two-phase block moves)
+  int nbuf = 4;
+  size_t smem = sizeof(double) * static_cast<size_t>(4 * b) * n * ncomp + sizeof(int) * n;
+  if (smem > 200 * 1024) {
+    nbuf = 3;
+    smem = sizeof(double) * static_cast<size_t>(3 * b) * n * ncomp + sizeof(int) * n;
+  }
+  if (smem > 210 * 1024 || n > 512) return NOTAPPLICABLE;
   const int threads = 32 * b;
   const bool dbg = std::getenv("NSK_SVD_DEBUG") != nullptr;
   unsigned long long* stamps = nullptr;
   if (dbg) NSK_CUDA_OK(cudaMallocAsync(&stamps, 6 * sizeof(unsigned long long), st));
   CSParams prm{X, static_cast<int>(n), b, tol, counter, degenerate, stamps};
   const int rpl = n <= 128 ? 4 : n <= 256 ? 8 : 16;
-  auto kern = ncomp == 1 ? (rpl == 4 ? cluster_svd_kernel<1, 4> : rpl == 8 ? cluster_svd_kernel<1, 8> : cluster_svd_kernel<1, 16>)
-                         : (rpl == 4 ? cluster_svd_kernel<2, 4> : rpl == 8 ? cluster_svd_kernel<2, 8> : cluster_svd_kernel<2, 16>);
+  // (three buffers are only needed for n > 256: b = 16, RPL = 16)
+  auto kern = ncomp == 1
+                  ? (rpl == 4 ? cluster_svd_kernel<1, 4, 4>
+                              : rpl == 8 ? cluster_svd_kernel<1, 8, 4>
+                                         : (nbuf == 4 ? cluster_svd_kernel<1, 16, 4> : cluster_svd_kernel<1, 16, 3>))
+                  : (rpl == 4 ? cluster_svd_kernel<2, 4, 4>
+                              : rpl == 8 ? cluster_svd_kernel<2, 8, 4>
+                                         : (nbuf == 4 ? cluster_svd_kernel<2, 16, 4> : cluster_svd_kernel<2, 16, 3>));
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   if (C > 8) NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
