@@ -286,7 +286,7 @@ def run_ours(args):
         achieved = byts / (kernel_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
-    roof.update({"kernel": {"srht": "srht_kernel", "srdct": "srtt_tile_kernel", "srft": "srtt_tile_kernel",
+    roof.update({"kernel": {"srht": "srht_kernel", "srdct": "srdct_tile_kernel", "srft": "srtt_tile_kernel",
                             "countsketch": "countsketch_owner_kernel", "gaussian": "gaussian_sketch_kernel"}[kind],
                  "kernel_ms": round(kernel_ms, 4), "algorithmic_bytes": byts, "algorithmic_flops": flops,
                  "traffic": traffic_from_profiles(kind)})

@@ -22,5 +22,5 @@ cap srht srht_kernel "--kind srht"
 cap countsketch countsketch_owner "--kind countsketch"
 cap gaussian gaussian_sketch "--kind gaussian"
 cap srft srtt_tile_kernel "--kind srft"
-cap srdct srtt_tile_kernel "--kind srdct"
+cap srdct srdct_tile_kernel "--kind srdct"
 cap svd cluster_svd_kernel "--kind srht"
