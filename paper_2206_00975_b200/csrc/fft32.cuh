@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 namespace nsk {
 namespace fft {
 
@@ -31,6 +33,27 @@ __device__ __forceinline__ double2 twmul32(double2 v, int k) {
   const double c = k < 8 ? C[k] : -C[16 - k];
   const double s = k < 8 ? C[8 - k] : C[k - 8];
   return make_double2(fma(v.x, c, -v.y * s), fma(v.x, s, v.y * c));
+}
+
+// a * b mod N for a, b < N <= 2^44 without 128-bit division: the quotient
+// from FP64 (error below 1 for these sizes), the remainder exact in wrapping
+// 64-bit arithmetic, then at most two corrections.
+__device__ __forceinline__ uint64_t mulmod_fast(uint64_t a, uint64_t b, uint64_t N, double invN) {
+  const double q = floor(static_cast<double>(a) * static_cast<double>(b) * invN);
+  int64_t r = static_cast<int64_t>(a * b - static_cast<uint64_t>(q) * N);
+  const int64_t n = static_cast<int64_t>(N);
+  if (r < 0) r += n;
+  if (r < 0) r += n;
+  if (r >= n) r -= n;
+  if (r >= n) r -= n;
+  return static_cast<uint64_t>(r);
+}
+
+// e^{2 pi i r / N} for an exact integer r in [0, N); two_over_N = 2.0 / N.
+__device__ __forceinline__ double2 unit_phase(uint64_t r, double two_over_N) {
+  double sn, cs;
+  sincospi(static_cast<double>(r) * two_over_N, &sn, &cs);
+  return make_double2(cs, sn);
 }
 
 __device__ __forceinline__ constexpr int brev5(int i) {

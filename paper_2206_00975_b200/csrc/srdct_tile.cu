@@ -82,9 +82,6 @@ __device__ __forceinline__ double2 unitq(uint64_t r, uint64_t Q) {
   sincospi(2.0 * static_cast<double>(r) / static_cast<double>(Q), &sn, &cs);
   return make_double2(cs, sn);
 }
-__device__ __forceinline__ uint64_t mulmodq(uint64_t a, uint64_t b, uint64_t Q) {
-  return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) % Q);
-}
 __device__ __forceinline__ double sgn(uint32_t bits, int pos, double v) {
   return ((bits >> pos) & 1u) ? v : -v;  // Rademacher bit 1 -> +1 (rng.hpp:57)
 }
@@ -268,7 +265,9 @@ __global__ void __launch_bounds__(32 * W, W == 4 ? 2 : 1) srdct_tile_kernel(DctP
 #pragma unroll
       for (int q = 0; q < DNQ; ++q) {
         const uint64_t f = freq_of(q);
-        if (anchor) base[q] = unitq(mulmodq(f % N, static_cast<uint64_t>(K) % N, N), N);
+        if (anchor)
+          base[q] = unit_phase(mulmod_fast(f, static_cast<uint64_t>(K), N, 1.0 / static_cast<double>(N)),
+                               2.0 / static_cast<double>(N));
         double2 w = base[q];
         const int qi = static_cast<int>(f & (DL - 1));
         const double2 st = step[q];

@@ -68,9 +68,6 @@ __device__ __forceinline__ double2 unit(uint64_t r, uint64_t N) {
   return make_double2(cs, sn);
 }
 
-__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t N) {
-  return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) % N);
-}
 
 // KIND 0 srft, 1 srdct; NCIN 1 real input (pairs), 2 complex input.
 template <int KIND, int NCIN>
@@ -169,7 +166,9 @@ __global__ void __launch_bounds__(TT, TW == 8 ? 1 : 2) srtt_tile_kernel(TilePara
 #pragma unroll
     for (int q = 0; q < TNQ; ++q) {
       const uint64_t f = freq_of(q);
-      if (anchor) base[q] = unit(mulmod((KIND == 1 ? 2 * f + 1 : f) % N, static_cast<uint64_t>(K) % N, N), N);
+      if (anchor)
+        base[q] = unit_phase(mulmod_fast(KIND == 1 ? 2 * f + 1 : f, static_cast<uint64_t>(K), N, 1.0 / static_cast<double>(N)),
+                             2.0 / static_cast<double>(N));
       double2 w = base[q];  // w_N^{g K}
       const int qi = static_cast<int>(f & (TL - 1));
       if (NCIN == 1) {

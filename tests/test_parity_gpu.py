@@ -109,6 +109,24 @@ def test_srdct_makhoul_parity(nsk, oracle, s, m, n):
     assert rel(got, other) <= SA_TOL
 
 
+@pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
+                                   (1500, 1 << 16, 9), (1024, 1 << 17, 150)])
+def test_srft_stream_parity(nsk, oracle, s, m, n):
+    """Register-streamed srft tiles (srft_stream.cu, real A, m % 16384 == 0) against numpy's
+    inverse FFT, and against the shared-memory tile path on the same operator."""
+    import os
+    A = oracle.random_real(m, n, 17)
+    got, _ = gpu_apply(nsk, "srft", s, m, 93, A)
+    ref = oracle.apply(oracle.draw("srft", s, m, 93), A)
+    assert rel(got, ref) <= SA_TOL
+    os.environ["NSK_SRFT_NOSTREAM"] = "1"
+    try:
+        other, _ = gpu_apply(nsk, "srft", s, m, 93, A)
+    finally:
+        del os.environ["NSK_SRFT_NOSTREAM"]
+    assert rel(got, other) <= SA_TOL
+
+
 def test_srft_complex_parity(nsk, oracle, golden):
     sa = golden["sa"]
     A = sa["A_srft"]
