@@ -33,6 +33,7 @@ struct DeviceTables {
   uint32_t* sign_bits = nullptr;    // srft/srdct: bit j of word j/32 = Rademacher bit of row j
   int64_t* srtt_freq = nullptr;     // srft/srdct: sample indices sorted by idx mod 1024 (tile FFT bin)
   int32_t* srtt_row = nullptr;      // output row of each sorted slot
+  uint64_t* srdct_sgn = nullptr;    // srdct (srdct_stream.cu): per tile, row class and column, main | mirror negate bits
   uint64_t* srft_sgn = nullptr;     // srft (srft_stream.cu): per tile, row class and column pair, 64 negate bits
   int64_t* dct_freq = nullptr;      // srdct (srdct_tile.cu): v index n(a) of each sample, sorted by n mod 1024
   int32_t* dct_row = nullptr;       // output row of each sorted srdct slot
@@ -59,6 +60,7 @@ bool cs_owner_eligible(int64_t s, int64_t m);
 int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out);
 int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out);
 int build_sign_bits(PhiloxKey key, int64_t m, uint32_t** out);
+int build_srdct_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out);  // null when m % 16384 != 0
 int build_srft_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out);  // null when m % 16384 != 0
 
 // A shard view: local row j of A is global row row0 + rstep * j, j < mloc.

@@ -228,6 +228,7 @@ const DeviceTables* Operator::tables() const {
   }
   if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return nullptr;
   if (kind == SRFT && build_srft_sgn(t.sign_bits, m, &t.srft_sgn) != OK) return nullptr;
+  if (kind == SRDCT && build_srdct_sgn(t.sign_bits, m, &t.srdct_sgn) != OK) return nullptr;
   if ((kind == SRFT || kind == SRDCT) && !idx.empty()) {
     // Slots sorted by FFT bin (idx mod 1024) for the tile kernel (srtt_tile.cu).
     std::vector<int32_t> order(idx.size());
@@ -314,6 +315,7 @@ Operator::~Operator() {
     if (t.srtt_freq) cudaFree(t.srtt_freq);
     if (t.srtt_row) cudaFree(t.srtt_row);
     if (t.srft_sgn) cudaFree(t.srft_sgn);
+    if (t.srdct_sgn) cudaFree(t.srdct_sgn);
     if (t.dct_freq) cudaFree(t.dct_freq);
     if (t.dct_row) cudaFree(t.dct_row);
     if (t.cs_ent) cudaFree(t.cs_ent);

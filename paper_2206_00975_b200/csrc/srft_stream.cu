@@ -59,8 +59,8 @@ struct StreamParams {
 __device__ __forceinline__ double flip(double v, uint32_t mask) {
   return __hiloint2double(__double2hiint(v) ^ static_cast<int>(mask), __double2loint(v));
 }
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;\n" ::"l"(p));
+__device__ __forceinline__ void prefetch_l2(const void* p) {  // the 128-byte line holding p
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
 
 // Negate masks: word (T, a, i) bit 2b + e = 1 iff the Rademacher bit of row
@@ -99,6 +99,7 @@ __global__ void srft_anchor_kernel(const int64_t* __restrict__ freq, int nslots,
 
 // (Issuing the next tile's loads after the sampled stage instead, behind an L2
 // prefetch, measured 1.13 ms instead of 0.88 ms at the configs[1] shape.)
+template <int PF>  // PF: L2 prefetch of the tile after the next one (NSK_STREAM_PF=0: off, 0.98 ms vs 0.88 ms)
 __global__ void __launch_bounds__(FT, 1) srft_stream_kernel(StreamParams p) {
   extern __shared__ __align__(16) double2 sm2[];
   double2* U = sm2;              // [FL][FROW]
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(FT, 1) srft_stream_kernel(StreamParams p) {
     sw = __ldg(p.sgn + (tt * 32 + a) * 8 + li);
   };
   auto prefetch = [&](int64_t c, int64_t tt) {  // L2 <- tile tt of column c (4 rows per thread)
+    if (!PF) return;
     const double* src = p.A + c * p.lda + FKT * tt;
 #pragma unroll
     for (int r = 0; r < FL / FT; ++r) prefetch_l2(src + P * (threadIdx.x + FT * r));
@@ -305,7 +307,8 @@ int srft_stream_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
   }
   const int64_t per = tiles / ranges, items = n * ranges;
   const size_t smem = sizeof(double2) * (FL * FROW + FL + 2 * FNQ * FT);
-  auto kern = srft_stream_kernel;
+  const char* pfe = std::getenv("NSK_STREAM_PF");
+  auto kern = pfe && !std::atoi(pfe) ? srft_stream_kernel<0> : srft_stream_kernel<1>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const double scale = 0.5 / std::sqrt(static_cast<double>(s));  // unnormalised DFT / sqrt(s); pairs carry 2
   for (int64_t b = 0; b < s; b += FNQ * FT) {

@@ -92,21 +92,19 @@ def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
 
 
 @pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
-                                   (1500, 1 << 16, 9)])
-def test_srdct_makhoul_parity(nsk, oracle, s, m, n):
-    """Makhoul-paired srdct tiles (srdct_tile.cu, m % 16384 == 0) against scipy's DCT-III, and
-    against the zero-padded tile path on the same operator."""
-    import os
+                                   (1500, 1 << 16, 9), (1024, 1 << 17, 150), (4096, 1 << 14, 3)])
+def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
+    """Register-streamed Makhoul tiles (srdct_stream.cu, m % 16384 == 0) against scipy's DCT-III,
+    and against the shared-memory Makhoul tiles (srdct_tile.cu) and the zero-padded tile path
+    on the same operator."""
     A = oracle.random_real(m, n, 13)
     got, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
     ref = oracle.apply(oracle.draw("srdct", s, m, 91), A)
     assert rel(got, ref) <= SA_TOL
-    os.environ["NSK_SRDCT_NOMAKHOUL"] = "1"
-    try:
+    for env in ("NSK_SRDCT_NOSTREAM", "NSK_SRDCT_NOMAKHOUL"):  # cumulative: Makhoul tiles, then padded tiles
+        monkeypatch.setenv(env, "1")
         other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
-    finally:
-        del os.environ["NSK_SRDCT_NOMAKHOUL"]
-    assert rel(got, other) <= SA_TOL
+        assert rel(got, other) <= SA_TOL, env
 
 
 @pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
