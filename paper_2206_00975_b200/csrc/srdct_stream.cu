@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
 #pragma unroll
       for (int b = 1; b < 32; ++b) x[b] = pre128(x[b], b);
     }
-    dft32(x);
+    dft32f(x);
 #pragma unroll
     for (int k = 0; k < 32; ++k) x[k] = cmul(x[k], tw[a * (4 * k + 1)]);
     __syncthreads();  // previous tile's sampled stage has read U
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
     const int sc = warp ^ (lane & 7);
 #pragma unroll
     for (int l = 0; l < 32; ++l) x[l] = U[(32 * l + lane) * SW + sc];
-    dft32(x);
+    dft32f(x);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 32; ++k) U[(lane + 32 * k) * SW + sc] = x[k];
