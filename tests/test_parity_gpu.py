@@ -92,7 +92,8 @@ def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
 
 
 @pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
-                                   (1500, 1 << 16, 9), (1024, 1 << 17, 150), (4096, 1 << 14, 3)])
+                                   (1500, 1 << 16, 9), (1024, 1 << 17, 150), (4096, 1 << 14, 3), (1, 1 << 14, 1),
+                                   (1 << 14, 1 << 14, 2), (7, 5 << 14, 149)])
 def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
     """Register-streamed Makhoul tiles (srdct_stream.cu, m % 16384 == 0) against scipy's DCT-III,
     and against the shared-memory Makhoul tiles (srdct_tile.cu) and the zero-padded tile path
@@ -108,7 +109,8 @@ def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
 
 
 @pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
-                                   (1500, 1 << 16, 9), (1024, 1 << 17, 150)])
+                                   (1500, 1 << 16, 9), (1024, 1 << 17, 150), (1, 1 << 14, 1), (1 << 14, 1 << 14, 2),
+                                   (7, 5 << 14, 149)])
 def test_srft_stream_parity(nsk, oracle, s, m, n):
     """Register-streamed srft tiles (srft_stream.cu, real A, m % 16384 == 0) against numpy's
     inverse FFT, and against the shared-memory tile path on the same operator."""
