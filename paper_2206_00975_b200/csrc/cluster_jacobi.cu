@@ -38,7 +38,7 @@ namespace cg = cooperative_groups;
 namespace nsk {
 namespace {
 
-constexpr int CJ_MAX_SWEEPS = 40;
+constexpr int CJ_MAX_SWEEPS = 80;  // == MAX_SWEEPS (jacobi_svd.cu): one counter layout
 
 struct CJParams {
   double* X;  // 2n x n (x NC), ld 2n: rows [0, n) = R part, [n, 2n) = V part

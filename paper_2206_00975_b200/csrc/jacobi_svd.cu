@@ -34,7 +34,7 @@ namespace nsk {
 namespace {
 
 constexpr int JT = 256;
-constexpr int MAX_SWEEPS = 40;
+constexpr int MAX_SWEEPS = 80;  // == CJ_MAX_SWEEPS (cluster_jacobi.cu): one counter layout
 
 template <int NC>
 __device__ __forceinline__ void block_sum4(double& a, double& b, double& c, double& d, double* red) {

@@ -339,6 +339,21 @@ def test_svd_trailing_complex(nsk, oracle):
     assert _angle(W, vh.conj().T[:, -2:]) < 1e-10
 
 
+def test_svd_complex_beyond_cluster_steep_spectrum(nsk):
+    """Complex n = 400 (> 335: the global-memory block Jacobi, no preconditioning) with sigma
+    logspaced 1 -> 1e-14: needs ~45 sweeps, above the former limit of 40."""
+    rng = np.random.default_rng(5)
+    s, n = 1200, 400
+    U, _ = np.linalg.qr(rng.standard_normal((s, n)) + 1j * rng.standard_normal((s, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    sref = np.logspace(0, -14, n)
+    X = (U * sref) @ V.conj().T
+    W, sig = nsk.svd_trailing(dev(X), 1)
+    W, sig = host(W), host(sig)
+    assert np.max(np.abs(sig - sref)) <= 1e-12
+    assert np.linalg.norm(X @ W) <= 1e-12
+
+
 def test_exact_null_space_preserved(nsk, oracle):
     # test_nullspace.cpp:21-32
     m, n, k = 200, 20, 2
