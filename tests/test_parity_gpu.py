@@ -479,6 +479,21 @@ def test_cfg2_srtt_full_size_properties(nsk, oracle, kind):
     assert rel(sa[:, cols].cpu().numpy(), ref) <= SA_TOL
 
 
+@pytest.mark.parametrize("kind", ["srdct", "srft"])
+def test_srtt_stream_large_m(nsk, oracle, kind):
+    """m = 2^24 + 2^14 (P = 16400 tile columns, not a power of two: exact-integer anchors with
+    the FP64 quotient, 1025+ tiles per column) through the stream kernels, two columns vs the oracle."""
+    import torch
+    m, n, s = (1 << 24) + (1 << 14), 3, 1000
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = torch.randn(n, m, dtype=torch.float64, device="cuda", generator=g).t()
+    S = nsk.SketchOperator.draw(kind, s, m, 9000007)
+    sa = nsk.apply(S, A).data
+    cols = [0, 2]
+    ref = oracle.apply(oracle.draw(kind, s, m, 9000007), A[:, cols].cpu().numpy())
+    assert rel(sa[:, cols].cpu().numpy(), ref) <= SA_TOL
+
+
 def test_cfg5_loewner_complex_gaussian(nsk, oracle):
     """BASELINE configs[4]: complex128 Loewner matrix (m = 99850 active rows, n = 150),
     Gaussian sketch s = 2n on complex data, k = 1 trailing vector."""
