@@ -1,0 +1,353 @@
+// srft_ws.cu -- sampled srft of a real A: warp-specialised tiles (FFT warps +
+// sampler warps) so the sampled stage of one tile overlaps the FFT of the next.
+//
+// Reference: apply(), srft branch (/root/reference/proj/src/sketch.cpp:206-217)
+// and idft_unitary_columns (transforms.cpp:17-36).  Same algebra as
+// srft_stream.cu (decimation in time, L = 1024, j = k1 + P k2, real columns
+// paired into complex sequences z = u_e + i u_o, Hermitian unpacking in the
+// sampled stage), with tiles of 8 real columns (4 sequences) and two roles in
+// one CTA of 8 warps:
+//
+//  * FFT warps 0-3: a lane (sequence i, row class a, 8 row classes per warp)
+//    reads its 32 rows of the staged tile from shared memory, flips signs,
+//    runs the first DFT32 (over b, k2 = a + 32 b) and the inter-pass twiddle,
+//    transposes in place through the same buffer (128-thread named barriers,
+//    no CTA barrier), runs the second DFT32 (warp = sequence) and writes all
+//    1024 bins to V;
+//  * sampler warps 4-7: stage tile u+1 with cp.async into the other of two
+//    tile buffers (completion tracked by that buffer's mbarrier, no thread
+//    waits on it) while the FFT warps work on tile u, then run the sampled
+//    stage of tile u from V (8 slots per thread, Horner over 4 sequences).
+//
+// Hand-offs: V_FULL / V_FREE are producer-arrive, consumer-sync named
+// barriers (256 threads; each producer's next arrival depends on the
+// consumer's previous sync, so no phase can be lapped); a tile buffer is
+// restaged only after the samplers have seen V_FULL of the tile that last
+// used it.  Shared memory: two tile buffers and V (64 KiB each, swizzled so
+// every access is 4 wavefronts per warp) and the w_1024 twiddles.
+#include "fft32.cuh"
+#include "nsk_internal.hpp"
+
+namespace nsk {
+
+namespace {
+
+using namespace fft;
+
+constexpr int XL = 1024;       // FFT length
+constexpr int XS = 4;          // sequences per tile
+constexpr int XKT = 2 * XS;    // real columns per tile
+constexpr int XT = 256;        // threads: 128 FFT + 128 sampler
+constexpr int XNQ = 8;         // output slots per sampler thread (128 x 8 = 1024)
+constexpr int XANCH = 16;      // exact twiddles every XANCH tiles
+constexpr int BAR_FFT = 1, BAR_V_FULL = 3, BAR_V_FREE = 4;
+
+struct WsParams {
+  const double* A;
+  int64_t lda;
+  int64_t m;
+  int64_t P;         // m / XL
+  int64_t tiles;     // per column: P / XKT
+  int64_t total;     // n * tiles
+  int64_t chunk;     // tiles per CTA
+  int64_t jmax;      // column pieces per CTA
+  const uint64_t* sgn;  // srft_sgn: [16-column tile][a][8] negate masks, bits 2b + e
+  const int64_t* freq;  // sample index of each slot (sorted by idx mod XL)
+  int nslots;
+  const double2* anc;   // [tile][XNQ * 128]: w_m^{f K}, K = XKT tile
+  double2* part;        // [cta][jmax][XNQ * 128]
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ double flipx(double v, uint32_t mask) {
+  return __hiloint2double(__double2hiint(v) ^ static_cast<int>(mask), __double2loint(v));
+}
+
+// U: element (row r, sequence i) at r * 4 + (i ^ ((r >> 1) & 3)); the pass-1
+// output (a, k) lives in row 32 a + (k ^ (a & 1)).  V: bin q, sequence i at
+// q * 4 + (i ^ ((q >> 1) & 3)).
+__device__ __forceinline__ int uidx(int r, int i) { return r * 4 + (i ^ ((r >> 1) & 3)); }
+
+__global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
+  extern __shared__ __align__(16) double2 smx[];
+  double2* BUF = smx;             // 2 x [XL][4]: staged tile (row k2, sequence i), then its transpose
+  double2* V = BUF + 2 * XL * XS; // [XL][4] bins
+  double2* tw = V + XL * XS;      // w_1024^k
+  double2* ST8 = tw + XL;         // [XNQ][128]: sampler slot steps w_m^{8 f} (one tile)
+  uint64_t* full = reinterpret_cast<uint64_t*>(ST8 + XNQ * 128);  // [2] per tile buffer
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t m = static_cast<uint64_t>(p.m);
+  const int64_t P = p.P;
+
+  for (int k = threadIdx.x; k < XL; k += XT) tw[k] = unit_phase(static_cast<uint64_t>(k), 2.0 / XL);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full)), "r"(128));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + 1)), "r"(128));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t u0 = blockIdx.x * p.chunk;
+  const int64_t u1 = u0 + p.chunk < p.total ? u0 + p.chunk : p.total;
+  if (u0 >= u1) return;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ FFT warps
+    const int li = lane & 3, a = 8 * warp + (lane >> 2);
+    int64_t c = u0 / p.tiles, T = u0 % p.tiles;
+    uint32_t ph = 0;  // bit j: phase of buffer j
+    double2 x[32];
+    for (int64_t u = u0; u < u1; ++u) {
+      const uint64_t sw = __ldg(p.sgn + ((T >> 1) * 32 + a) * 8 + 4 * (T & 1) + li);
+      const int bf = static_cast<int>((u - u0) & 1);
+      double2* RAW = BUF + bf * (XL * XS);
+      double2* U = RAW;  // the transpose reuses the tile's buffer
+      mbar_wait_parity(full + bf, (ph >> bf) & 1u);
+      ph ^= 1u << bf;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) x[b] = RAW[(a + 32 * b) * XS + li];
+      {
+        const uint32_t lo = static_cast<uint32_t>(sw), hi = static_cast<uint32_t>(sw >> 32);
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+          const uint32_t wd = b < 16 ? lo : hi;
+          const int sh = 2 * (b & 15);
+          x[b].x = flipx(x[b].x, (wd << (31 - sh)) & 0x80000000u);
+          x[b].y = flipx(x[b].y, (wd << (30 - sh)) & 0x80000000u);
+        }
+      }
+      dft32(x);
+#pragma unroll
+      for (int k = 1; k < 32; ++k) x[k] = cmul(x[k], tw[a * k]);
+      named_sync(BAR_FFT, 128);  // every warp has read the staged tile
+#pragma unroll
+      for (int k = 0; k < 32; ++k) U[uidx(32 * a + (k ^ (a & 1)), li)] = x[k];
+      named_sync(BAR_FFT, 128);
+#pragma unroll
+      for (int l = 0; l < 32; ++l) x[l] = U[uidx(32 * l + (lane ^ (l & 1)), warp)];
+      dft32(x);
+      if (u > u0) named_sync(BAR_V_FREE, 256);  // samplers are done with the previous tile's V
+#pragma unroll
+      for (int k = 0; k < 32; ++k) V[uidx(lane + 32 * k, warp)] = x[k];
+      named_arrive(BAR_V_FULL, 256);
+      if (++T == p.tiles) {
+        T = 0;
+        ++c;
+      }
+    }
+    named_sync(BAR_V_FREE, 256);  // pair the samplers' last arrival
+    return;
+  }
+
+  // -------------------------------------------------------------- samplers
+  const int ts = threadIdx.x - 128;
+  const double two_m = 2.0 / static_cast<double>(m);
+  double2 acc[XNQ], base[XNQ], step[XNQ];
+  int bins[XNQ];
+#pragma unroll
+  for (int q = 0; q < XNQ; ++q) {
+    const int o = ts + 128 * q;
+    const uint64_t f = o < p.nslots ? static_cast<uint64_t>(__ldg(p.freq + o)) : 0;
+    const int qi = static_cast<int>(f & (XL - 1));
+    bins[q] = qi | (((XL - qi) & (XL - 1)) << 16);
+    double2 s1 = unit_phase(f, two_m);
+    step[q] = s1;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) s1 = cmul(s1, s1);
+    ST8[128 * q + ts] = s1;  // w_m^{8 f}: one tile
+    acc[q] = make_double2(0.0, 0.0);
+    base[q] = make_double2(1.0, 0.0);
+  }
+  // stage tile (cc, TT): chunk ch = ts + 128 j is row ch / 4, sequence ch % 4
+  auto stage = [&](int64_t cc, int64_t TT, int bf) {
+    const double* src = p.A + cc * p.lda + XKT * TT;
+    double2* RAW = BUF + bf * (XL * XS);
+    uint64_t* bar = full + bf;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const int ch = ts + 128 * j, row = ch >> 2, i = ch & 3;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(RAW + row * XS + i)),
+                   "l"(src + 2 * i + P * row));
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(su32(bar)) : "memory");
+  };
+  auto prefetch = [&](int64_t cc, int64_t TT) {  // L2 <- 8 of the tile's 64-byte rows per thread
+    const double* src = p.A + cc * p.lda + XKT * TT;
+#pragma unroll
+    for (int r = 0; r < XL / 128; ++r)
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(src + P * (ts + 128 * r)));
+  };
+  int64_t c = u0 / p.tiles, T = u0 % p.tiles, piece = 0;
+  stage(c, T, 0);
+  for (int64_t u = u0; u < u1; ++u) {
+    const int64_t Tcur = T;
+    int64_t cn = c, Tn = T;
+    if (++Tn == p.tiles) {
+      Tn = 0;
+      ++cn;
+    }
+    if (u + 1 < u1) {  // tile u+1 into the buffer of tile u-1 (its V_FULL was seen: transposed and read)
+      stage(cn, Tn, static_cast<int>((u + 1 - u0) & 1));
+      if (u + 2 < u1) {
+        int64_t c2 = cn, T2 = Tn;
+        if (++T2 == p.tiles) {
+          T2 = 0;
+          ++c2;
+        }
+        prefetch(c2, T2);
+      }
+    }
+    if ((Tcur % XANCH) == 0 || u == u0) {
+#pragma unroll
+      for (int q = 0; q < XNQ; ++q) base[q] = __ldg(p.anc + Tcur * (XNQ * 128) + ts + 128 * q);
+    }
+    named_sync(BAR_V_FULL, 256);
+    // acc += w^{fK} sum_i w^{2fi} (E_i - i w^f D_i), E/D from Z[q] and conj Z[-q] by Horner
+#pragma unroll
+    for (int q = 0; q < XNQ; ++q) {
+      const double2 st = step[q];
+      const double2 st2 = cmul(st, st);
+      const int qi = bins[q] & 0xffff, qm = bins[q] >> 16;
+      double2 hq = V[uidx(qi, XS - 1)], hm = V[uidx(qm, XS - 1)];
+      hm.y = -hm.y;
+#pragma unroll
+      for (int i = XS - 2; i >= 0; --i) {
+        const double2 zq = V[uidx(qi, i)], zm = V[uidx(qm, i)];
+        hq = make_double2(fma(st2.x, hq.x, fma(-st2.y, hq.y, zq.x)), fma(st2.x, hq.y, fma(st2.y, hq.x, zq.y)));
+        hm = make_double2(fma(st2.x, hm.x, fma(-st2.y, hm.y, zm.x)), fma(st2.x, hm.y, fma(st2.y, hm.x, -zm.y)));
+      }
+      const double2 e = cadd(hq, hm), d = csub(hq, hm);
+      const double2 sd = cmul(st, d);
+      const double2 term = make_double2(e.x + sd.y, e.y - sd.x);
+      const double2 w = base[q];
+      acc[q] = make_double2(fma(w.x, term.x, fma(-w.y, term.y, acc[q].x)),
+                            fma(w.x, term.y, fma(w.y, term.x, acc[q].y)));
+      base[q] = cmul(w, ST8[128 * q + ts]);
+    }
+    named_arrive(BAR_V_FREE, 256);
+    if (u + 1 == u1 || Tn == 0) {  // column piece done
+      double2* part = p.part + (blockIdx.x * p.jmax + piece) * (XNQ * 128);
+#pragma unroll
+      for (int q = 0; q < XNQ; ++q) {
+        part[ts + 128 * q] = acc[q];
+        acc[q] = make_double2(0.0, 0.0);
+      }
+      ++piece;
+    }
+    c = cn;
+    T = Tn;
+  }
+}
+
+// anc[T][o] = w_m^{f_o K}, K = XKT T.
+__global__ void srft_ws_anchor_kernel(const int64_t* __restrict__ freq, int nslots, int64_t m, int64_t tiles,
+                                      double2* __restrict__ anc) {
+  const int64_t total = tiles * (XNQ * 128);
+  const double inv_m = 1.0 / static_cast<double>(m), two_m = 2.0 / static_cast<double>(m);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int o = static_cast<int>(e % (XNQ * 128));
+    const int64_t T = e / (XNQ * 128);
+    const uint64_t f = o < nslots ? static_cast<uint64_t>(freq[o]) : 0;
+    const uint64_t K = static_cast<uint64_t>(XKT * T) % static_cast<uint64_t>(m);
+    anc[e] = unit_phase(mulmod_fast(f, K, static_cast<uint64_t>(m), inv_m), two_m);
+  }
+}
+
+// SA(row, c) = scale * sum over the CTAs covering column c of their piece for c (fixed order).
+__global__ void srft_ws_reduce(const double2* __restrict__ part, int64_t tiles, int64_t chunk, int64_t jmax,
+                               int64_t n, int nslots, const int32_t* __restrict__ row_of_slot, double scale,
+                               double* __restrict__ SA, int64_t ldsa) {
+  const int64_t total = n * nslots;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = e / nslots;
+    const int o = static_cast<int>(e % nslots);
+    const int64_t g0 = (c * tiles) / chunk, g1 = ((c + 1) * tiles - 1) / chunk;
+    double2 v = make_double2(0.0, 0.0);
+    for (int64_t g = g0; g <= g1; ++g) {
+      const double2 x = part[(g * jmax + (c - (g * chunk) / tiles)) * (XNQ * 128) + o];
+      v.x += x.x;
+      v.y += x.y;
+    }
+    const int64_t row = row_of_slot[o];
+    SA[2 * (row + c * ldsa)] = scale * v.x;
+    SA[2 * (row + c * ldsa) + 1] = scale * v.y;
+  }
+}
+
+}  // namespace
+
+// NOTAPPLICABLE unless the whole column of a real A is applied, m is a
+// multiple of 16 * 1024 (the srft_sgn table) and A is 16-byte aligned with an
+// even lda.  NSK_SRFT_WS=0 selects the single-role stream kernel instead.
+int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                  double* SA, int64_t ldsa, cudaStream_t st) {
+  const char* e = std::getenv("NSK_SRFT_WS");
+  if (e && !std::atoi(e)) return NOTAPPLICABLE;
+  const int64_t m = op.m, s = op.s;
+  if (op.kind != SRFT || ncomp != 1 || n == 0) return NOTAPPLICABLE;
+  if (!(rows.row0 == 0 && rows.rstep == 1 && rows.mloc == m)) return NOTAPPLICABLE;
+  if (m % (XL * 16) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0) return NOTAPPLICABLE;
+  const DeviceTables* tb = op.tables();
+  if (!tb || !tb->srft_sgn || !tb->srtt_freq || !tb->srtt_row) return ECUDA;
+  const int64_t P = m / XL, tiles = P / XKT, total = n * tiles;
+  int64_t G = sm_count();
+  if (G > total) G = total;
+  const int64_t chunk = (total + G - 1) / G;
+  G = (total + chunk - 1) / chunk;
+  const int64_t jmax = chunk / tiles + 2;
+  // two tile buffers, V, twiddles, slot steps, 2 mbarriers
+  const size_t smem = sizeof(double2) * (3 * XL * XS + XL + XNQ * 128) + 16;
+  NSK_CUDA_OK(cudaFuncSetAttribute(srft_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  const double scale = 0.5 / std::sqrt(static_cast<double>(s));  // unnormalised DFT / sqrt(s); pairs carry 2
+  for (int64_t b = 0; b < s; b += XNQ * 128) {
+    const int ns = static_cast<int>((s - b) < XNQ * 128 ? (s - b) : XNQ * 128);
+    Scratch part, anc;
+    NSK_CUDA_OK(part.alloc(sizeof(double2) * G * jmax * XNQ * 128, st));
+    NSK_CUDA_OK(anc.alloc(sizeof(double2) * tiles * XNQ * 128, st));
+    {
+      int64_t blocks = (tiles * XNQ * 128 + 255) / 256;
+      if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+      srft_ws_anchor_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(tb->srtt_freq + b, ns, m, tiles,
+                                                                           anc.as<double2>());
+      count_launch();
+      NSK_CUDA_OK(cudaGetLastError());
+    }
+    WsParams p{A, lda, m, P, tiles, total, chunk, jmax, tb->srft_sgn, tb->srtt_freq + b, ns, anc.as<double2>(),
+               part.as<double2>()};
+    KernelTimer tm(st);
+    srft_ws_kernel<<<static_cast<unsigned>(G), XT, smem, st>>>(p);
+    tm.stop();
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+    int64_t blocks = (n * ns + 255) / 256;
+    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+    srft_ws_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double2>(), tiles, chunk, jmax, n, ns,
+                                                                  tb->srtt_row + b, scale, SA, ldsa);
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+  }
+  return OK;
+}
+
+}  // namespace nsk

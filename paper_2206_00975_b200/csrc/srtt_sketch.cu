@@ -21,6 +21,8 @@ int srtt_tile_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
                     double* SA, int64_t ldsa, cudaStream_t st);
 int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                     int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
+int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                  double* SA, int64_t ldsa, cudaStream_t st);
 int srft_stream_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                       double* SA, int64_t ldsa, cudaStream_t st);
 int srdct_stream_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
@@ -128,6 +130,8 @@ int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, con
     if (rd != NOTAPPLICABLE) return rd;
   }
   if (op.kind == SRFT && ncomp == 1) {
+    const int rw = srft_ws_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+    if (rw != NOTAPPLICABLE) return rw;
     const int rs = srft_stream_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
     if (rs != NOTAPPLICABLE) return rs;
   }

@@ -111,20 +111,18 @@ def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
 @pytest.mark.parametrize("s,m,n", [(256, 1 << 14, 5), (1000, 1 << 15, 3), (300, 3 << 14, 4), (2048, 1 << 18, 2),
                                    (1500, 1 << 16, 9), (1024, 1 << 17, 150), (1, 1 << 14, 1), (1 << 14, 1 << 14, 2),
                                    (7, 5 << 14, 149)])
-def test_srft_stream_parity(nsk, oracle, s, m, n):
-    """Register-streamed srft tiles (srft_stream.cu, real A, m % 16384 == 0) against numpy's
-    inverse FFT, and against the shared-memory tile path on the same operator."""
-    import os
+def test_srft_stream_parity(nsk, oracle, monkeypatch, s, m, n):
+    """Warp-specialised srft tiles (srft_ws.cu, the default for real A with m % 16384 == 0)
+    against numpy's inverse FFT, and against the register-streamed tiles (srft_stream.cu) and
+    the shared-memory tile path on the same operator."""
     A = oracle.random_real(m, n, 17)
     got, _ = gpu_apply(nsk, "srft", s, m, 93, A)
     ref = oracle.apply(oracle.draw("srft", s, m, 93), A)
     assert rel(got, ref) <= SA_TOL
-    os.environ["NSK_SRFT_NOSTREAM"] = "1"
-    try:
+    for env in ("NSK_SRFT_WS", "NSK_SRFT_NOSTREAM"):  # cumulative: stream tiles, then shared-memory tiles
+        monkeypatch.setenv(env, "0" if env == "NSK_SRFT_WS" else "1")
         other, _ = gpu_apply(nsk, "srft", s, m, 93, A)
-    finally:
-        del os.environ["NSK_SRFT_NOSTREAM"]
-    assert rel(got, other) <= SA_TOL
+        assert rel(got, other) <= SA_TOL, env
 
 
 def test_srft_complex_parity(nsk, oracle, golden):
