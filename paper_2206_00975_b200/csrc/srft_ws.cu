@@ -91,14 +91,15 @@ __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
   extern __shared__ __align__(16) double2 smx[];
   double2* BUF = smx;             // 2 x [XL][4]: staged tile (row k2, sequence i), then its transpose
   double2* V = BUF + 2 * XL * XS; // [XL][4] bins
-  double2* tw = V + XL * XS;      // w_1024^k
+  double2* tw = V + XL * XS;      // [k][a]: w_1024^{a k} (a warp's 8 row classes: one wavefront)
   double2* ST8 = tw + XL;         // [XNQ][128]: sampler slot steps w_m^{8 f} (one tile)
   uint64_t* full = reinterpret_cast<uint64_t*>(ST8 + XNQ * 128);  // [2] per tile buffer
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t m = static_cast<uint64_t>(p.m);
   const int64_t P = p.P;
 
-  for (int k = threadIdx.x; k < XL; k += XT) tw[k] = unit_phase(static_cast<uint64_t>(k), 2.0 / XL);
+  for (int e = threadIdx.x; e < XL; e += XT)
+    tw[e] = unit_phase(static_cast<uint64_t>((e >> 5) * (e & 31)), 2.0 / XL);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full)), "r"(128));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + 1)), "r"(128));
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
       }
       dft32(x);
 #pragma unroll
-      for (int k = 1; k < 32; ++k) x[k] = cmul(x[k], tw[a * k]);
+      for (int k = 1; k < 32; ++k) x[k] = cmul(x[k], tw[k * 32 + a]);
       named_sync(BAR_FFT, 128);  // every warp has read the staged tile
 #pragma unroll
       for (int k = 0; k < 32; ++k) U[uidx(32 * a + (k ^ (a & 1)), li)] = x[k];

@@ -95,13 +95,17 @@ def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
                                    (1500, 1 << 16, 9), (1024, 1 << 17, 150), (4096, 1 << 14, 3), (1, 1 << 14, 1),
                                    (1 << 14, 1 << 14, 2), (7, 5 << 14, 149)])
 def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
-    """Register-streamed Makhoul tiles (srdct_stream.cu, m % 16384 == 0) against scipy's DCT-III,
-    and against the shared-memory Makhoul tiles (srdct_tile.cu) and the zero-padded tile path
-    on the same operator."""
+    """Register-streamed Makhoul tiles (srdct_stream.cu, the default for m % 16384 == 0) against
+    scipy's DCT-III, and against the warp-specialised tiles (srdct_ws.cu, opt-in), the
+    shared-memory Makhoul tiles (srdct_tile.cu) and the zero-padded tile path."""
     A = oracle.random_real(m, n, 13)
     got, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
     ref = oracle.apply(oracle.draw("srdct", s, m, 91), A)
     assert rel(got, ref) <= SA_TOL
+    monkeypatch.setenv("NSK_SRDCT_WS", "1")  # the opt-in warp-specialised tiles
+    other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
+    assert rel(got, other) <= SA_TOL
+    monkeypatch.delenv("NSK_SRDCT_WS")
     for env in ("NSK_SRDCT_NOSTREAM", "NSK_SRDCT_NOMAKHOUL"):  # cumulative: Makhoul tiles, then padded tiles
         monkeypatch.setenv(env, "1")
         other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
