@@ -21,6 +21,6 @@ cap() {  # cap <name> <kernel regex> <bench args>
 cap srht srht_kernel "--kind srht"
 cap countsketch countsketch_owner "--kind countsketch"
 cap gaussian gaussian_sketch "--kind gaussian"
-cap srft srft_stream_kernel "--kind srft"
+cap srft srft_ws_kernel "--kind srft"
 cap srdct srdct_stream_kernel "--kind srdct"
 cap svd cluster_svd_kernel "--kind srht"
