@@ -238,6 +238,23 @@ def test_non_colmajor_and_ld_inputs(nsk, oracle):
     assert rel(host(nsk.apply(S, view).data), ref) <= 1e-15
 
 
+@pytest.mark.parametrize("kind", ["srft", "srdct", "srht", "countsketch", "gaussian"])
+def test_padded_leading_dimension_tile_kernels(nsk, oracle, kind):
+    """lda = m + 16 (even: the 16-byte staging paths stay eligible) at m = 2^14, where every kind
+    runs its tile kernel, against the oracle on the unpadded matrix."""
+    import torch
+    m, n, s = 1 << 14, 7, 256
+    A = oracle.random_real(m, n, 21)
+    big = torch.zeros((n, m + 16), dtype=torch.float64, device="cuda")
+    big[:, :m] = torch.from_numpy(A.T.copy()).cuda()
+    view = big.t()[:m]
+    assert view.stride() == (1, m + 16)
+    S = nsk.SketchOperator.draw(kind, s, m, 9000011)
+    got = host(nsk.apply(S, view).data)
+    ref = oracle.apply(oracle.draw(kind, s, m, 9000011), A)
+    assert rel(got, ref) <= SA_TOL
+
+
 def test_host_entry_point_matches_device(nsk, oracle):
     m, n = 2000, 10
     A = oracle.random_real(m, n, 8)
