@@ -238,17 +238,19 @@ def test_non_colmajor_and_ld_inputs(nsk, oracle):
     assert rel(host(nsk.apply(S, view).data), ref) <= 1e-15
 
 
+@pytest.mark.parametrize("pad,off", [(16, 0), (5, 0), (16, 1)])
 @pytest.mark.parametrize("kind", ["srft", "srdct", "srht", "countsketch", "gaussian"])
-def test_padded_leading_dimension_tile_kernels(nsk, oracle, kind):
-    """lda = m + 16 (even: the 16-byte staging paths stay eligible) at m = 2^14, where every kind
-    runs its tile kernel, against the oracle on the unpadded matrix."""
+def test_padded_leading_dimension_tile_kernels(nsk, oracle, kind, pad, off):
+    """lda = m + pad at m = 2^14 with the matrix starting `off` elements into the buffer: the
+    tile kernels (even lda, 16-byte aligned A) and their fallbacks (odd lda, 8-byte aligned A),
+    against the oracle on the unpadded matrix."""
     import torch
     m, n, s = 1 << 14, 7, 256
     A = oracle.random_real(m, n, 21)
-    big = torch.zeros((n, m + 16), dtype=torch.float64, device="cuda")
-    big[:, :m] = torch.from_numpy(A.T.copy()).cuda()
-    view = big.t()[:m]
-    assert view.stride() == (1, m + 16)
+    big = torch.zeros((n, m + pad + off), dtype=torch.float64, device="cuda")
+    big[:, off:off + m] = torch.from_numpy(A.T.copy()).cuda()
+    view = big.t()[off:off + m]
+    assert view.stride() == (1, m + pad + off)
     S = nsk.SketchOperator.draw(kind, s, m, 9000011)
     got = host(nsk.apply(S, view).data)
     ref = oracle.apply(oracle.draw(kind, s, m, 9000011), A)
