@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
     int64_t c = u0 / p.tiles, T = u0 % p.tiles;
     uint32_t ph = 0;  // bit j: phase of buffer j
     double2 x[32];
+    auto sgn_of = [&](int64_t TT) { return __ldg(p.sgn + ((TT >> 1) * 32 + a) * 8 + 4 * (TT & 1) + li); };
+    uint64_t sw_next = sgn_of(T);
     for (int64_t u = u0; u < u1; ++u) {
-      const uint64_t sw = __ldg(p.sgn + ((T >> 1) * 32 + a) * 8 + 4 * (T & 1) + li);
+      const uint64_t sw = sw_next;  // loaded one tile ahead (an L2 round trip off the critical path)
+      if (u + 1 < u1) sw_next = sgn_of(T + 1 == p.tiles ? 0 : T + 1);
       const int bf = static_cast<int>((u - u0) & 1);
       double2* RAW = BUF + bf * (XL * XS);
       double2* U = RAW;  // the transpose reuses the tile's buffer
