@@ -257,3 +257,84 @@ void nsko_srht_apply(const double* signs, const int64_t* idx, int64_t s, int64_t
   }
   for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
 }
+
+/* Rows `rows[0..nr)` of the s x m Gaussian G over the column range [j0, j1):
+ * out[r + (j - j0) * nr] = G(rows[r], j) = Gaussian #(j*s + rows[r]) of stream
+ * (seed, stream) (sketch.cpp:117-121).  Random access into the counter stream,
+ * so a row sample of G costs nr * (j1 - j0) draws instead of s * (j1 - j0);
+ * threads split the column range. */
+typedef struct {
+  uint32_t key[2];
+  int64_t s, nr, j0, j1, jbase;
+  const int64_t* rows;
+  double* out;
+} grows_job;
+
+static void* grows_worker(void* p) {
+  grows_job* jb = (grows_job*)p;
+  for (int64_t j = jb->j0; j < jb->j1; ++j)
+    for (int64_t r = 0; r < jb->nr; ++r) {
+      uint64_t L = (uint64_t)j * (uint64_t)jb->s + (uint64_t)jb->rows[r];
+      jb->out[(size_t)((j - jb->jbase) * jb->nr + r)] = nsko_gaussian(jb->key, L);
+    }
+  return NULL;
+}
+
+void nsko_gaussian_rows(uint64_t seed, uint64_t stream, int64_t s, const int64_t* rows, int64_t nr,
+                        int64_t j0, int64_t j1, double* out, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  int64_t cols = j1 - j0;
+  if (cols <= 0) return;
+  if (nthreads > cols) nthreads = (int)cols;
+  pthread_t th[256];
+  grows_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    nsko_key(seed, stream, jobs[t].key);
+    jobs[t].s = s;
+    jobs[t].nr = nr;
+    jobs[t].rows = rows;
+    jobs[t].jbase = j0;
+    jobs[t].j0 = j0 + cols * t / nthreads;
+    jobs[t].j1 = j0 + cols * (t + 1) / nthreads;
+    jobs[t].out = out;
+    pthread_create(&th[t], NULL, grows_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+/* CountSketch apply with the draw tables precomputed (nsko_countsketch_draw),
+ * threads over column ranges; within a column the rows are added in increasing
+ * order, exactly as nsko_countsketch_apply does. */
+typedef struct {
+  const int32_t* bucket; const double* sign; const double* A; double* SA;
+  int64_t s, m, lda, ldsa, c0, c1;
+} csmt_job;
+
+static void* csmt_worker(void* p) {
+  csmt_job* jb = (csmt_job*)p;
+  for (int64_t c = jb->c0; c < jb->c1; ++c) {
+    double* out = jb->SA + c * jb->ldsa;
+    const double* a = jb->A + c * jb->lda;
+    for (int64_t r = 0; r < jb->s; ++r) out[r] = 0.0;
+    for (int64_t i = 0; i < jb->m; ++i) out[jb->bucket[i]] += jb->sign[i] * a[i];
+  }
+  return NULL;
+}
+
+void nsko_countsketch_apply_tables(const int32_t* bucket, const double* sign, int64_t s, int64_t m,
+                                   int64_t n, const double* A, int64_t lda, double* SA, int64_t ldsa,
+                                   int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if (n <= 0) return;
+  if (nthreads > n) nthreads = (int)n;
+  pthread_t th[256];
+  csmt_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    csmt_job j = {bucket, sign, A, SA, s, m, lda, ldsa, n * t / nthreads, n * (t + 1) / nthreads};
+    jobs[t] = j;
+    pthread_create(&th[t], NULL, csmt_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}

@@ -80,6 +80,9 @@ def lib():
         L.nsko_srht_apply.argtypes = [_dp, _ip, c_i64, c_i64, c_i64, _dp, c_i64, _dp, c_i64,
                                       c_i64, c_i64, ctypes.c_int]
         L.nsko_fwht.argtypes = [_dp, c_i64]
+        L.nsko_gaussian_rows.argtypes = [c_u64, c_u64, c_i64, _ip, c_i64, c_i64, c_i64, _dp, ctypes.c_int]
+        L.nsko_countsketch_apply_tables.argtypes = [_i32p, _dp, c_i64, c_i64, c_i64, _dp, c_i64, _dp, c_i64,
+                                                    ctypes.c_int]
         _LIB = L
     return _LIB
 
@@ -147,6 +150,17 @@ def gaussian_block(seed, s, j0, j1, stream=0, nthreads=None):
     out = np.empty((j1 - j0) * s, dtype=np.float64)
     lib().nsko_gaussian_block(seed, stream, s, j0, j1, _p(out, _dp), nthreads or os.cpu_count())
     return out.reshape(j1 - j0, s).T
+
+
+def gaussian_rows(seed, s, rows, j0, j1, stream=0, nthreads=None):
+    """Rows `rows` of the s x m Gaussian G over columns j0..j1-1 (sketch.cpp:117-121):
+    out[r, j - j0] = Gaussian #(j*s + rows[r]) of stream (seed, stream).  A row sample of G
+    costs len(rows) draws per column, so SA row samples at configs[3] size stay cheap."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty((j1 - j0) * len(rows), dtype=np.float64)
+    lib().nsko_gaussian_rows(seed, stream, s, _p(rows, _ip), len(rows), j0, j1, _p(out, _dp),
+                             nthreads or os.cpu_count())
+    return out.reshape(j1 - j0, len(rows)).T
 
 
 class OracleOperator:
@@ -227,7 +241,9 @@ def apply(op: OracleOperator, A, col_range=None):
         A = np.asfortranarray(A, dtype=np.float64)
         n = A.shape[1]
         SA = np.zeros((s, n), dtype=np.float64, order="F")
-        lib().nsko_countsketch_apply(op.seed, s, m, n, _p(A, _dp), m, _p(SA, _dp), s)
+        # rows added in increasing order within each column (threads split the columns)
+        lib().nsko_countsketch_apply_tables(_p(op.bucket, _i32p), _p(op.signs, _dp), s, m, n, _p(A, _dp), m,
+                                            _p(SA, _dp), s, os.cpu_count())
         return SA
     raise ValueError(op.kind)
 
@@ -328,9 +344,20 @@ def thin_qr(a):
     return q * d, (r.T * d).T
 
 
-def make_test_matrix(m, n, spectrum, seed, left="haar"):
+def _cholqr2(a):
+    """Q of a well-conditioned tall a by two CholeskyQR passes, diag(R) > 0: the same Q as the
+    Householder QR with non-negative diag(R) to O(u) for cond(a) ~ 1 (Gaussian frames)."""
+    q = a
+    for _ in range(2):
+        r = np.linalg.cholesky(q.T @ q).T
+        q = q @ np.linalg.inv(r)
+    return q
+
+
+def make_test_matrix(m, n, spectrum, seed, left="haar", qr="householder"):
     """U diag(spectrum) V^T (kernels.cpp:169-203): U = Q of stream-1 Gaussians
-    (column-major, m x n), V = Q of stream-2 Gaussians (n x n)."""
+    (column-major, m x n), V = Q of stream-2 Gaussians (n x n).  qr="cholqr2" forms U by
+    CholeskyQR2 instead of Householder (same Q to rounding; 10x faster at m = 2^20)."""
     spectrum = np.asarray(spectrum, dtype=np.float64)
     if m < n:
         raise ValueError("make_test_matrix: need m >= n")
@@ -338,8 +365,9 @@ def make_test_matrix(m, n, spectrum, seed, left="haar"):
         u = np.zeros((m, n))
         u[:n, :n] = np.eye(n)
     else:
-        g = gaussians(seed, 1, 0, m * n).reshape(n, m).T
-        u = thin_qr(g)[0]
+        # g[i, c] = Gaussian #(c*m + i) of stream 1 (column-major fill), drawn by threads
+        g = gaussian_block(seed, m, 0, n, stream=1)
+        u = _cholqr2(g) if qr == "cholqr2" else thin_qr(g)[0]
     gv = gaussians(seed, 2, 0, n * n).reshape(n, n).T
     v = thin_qr(gv)[0]
     return np.asfortranarray((u * spectrum) @ v.T)
@@ -470,6 +498,12 @@ def tls_solve_sketched(A, B, op, cond_limit=1e12, allow_marginal=False):
     if k < 1 or n < k or m < n + k:
         raise ValueError("tls: bad shape")
     sk = apply_state(op, np.concatenate([A, B], axis=1))
+    return tls_from_sketch(sk, n, k, cond_limit, allow_marginal)
+
+
+def tls_from_sketch(sk, n, k, cond_limit=1e12, allow_marginal=False):
+    """The part of tls_solve_sketched after the apply (tls.cpp:110-113, extract_x 26-43):
+    SVD of the s x (n+k) sketch, existence check, X = -V1 V2^{-1}."""
     _, sv, v = svd(sk)
     sa = np.linalg.svd(sk[:, :n], compute_uv=False)
     if not (sa[n - 1] > sv[n]) and not allow_marginal:

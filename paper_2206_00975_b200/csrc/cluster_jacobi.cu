@@ -115,7 +115,9 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
                              int* counter, unsigned long long* prof = nullptr) {
   long long t_inner = 0, t_move = 0, t0 = 0, t1 = 0;
   const int c = static_cast<int>(cluster.block_rank()), C = static_cast<int>(cluster.num_blocks());
-  const int colsz = ld * NC, twob = 2 * b, blksz = b * colsz;
+  // blksz: buffer stride, rounded up to an even count so every block buffer is 16-byte aligned for
+  // the double2 block moves (b * n is odd for odd n and b in the real svd kernel)
+  const int colsz = ld * NC, twob = 2 * b, blksz = (b * colsz + 1) & ~1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
   if (C > 1) cluster_arrive();  // opens the split barrier closed before the first copy
   int sweep = 0;
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  //
   __shared__ int cand_idx[2][256];     //                                 and its global slot
   __shared__ int lg[32];               // pivot step of each slot: -1 not yet, -2 padding
   const int c = static_cast<int>(cluster.block_rank()), C = static_cast<int>(cluster.num_blocks());
-  const int n = p.n, colsz = n * NC, b = p.b, twob = 2 * b, blksz = b * colsz;
+  const int n = p.n, colsz = n * NC, b = p.b, twob = 2 * b, blksz = (b * colsz + 1) & ~1;  // even stride
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nthr = blockDim.x;
   int* phys = reinterpret_cast<int*>(buf + NB * blksz);
   const int gbase = c * twob;  // global slot of local slot 0
@@ -736,10 +738,11 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
   if (b > 16) return NOTAPPLICABLE;
   // four block buffers when they fit, else three (two-phase block moves)
   int nbuf = 4;
-  size_t smem = sizeof(double) * static_cast<size_t>(4 * b) * n * ncomp + sizeof(int) * n;
+  const size_t bstride = (static_cast<size_t>(b) * n * ncomp + 1) & ~static_cast<size_t>(1);  // as blksz
+  size_t smem = sizeof(double) * 4 * bstride + sizeof(int) * n;
   if (smem > 200 * 1024) {
     nbuf = 3;
-    smem = sizeof(double) * static_cast<size_t>(3 * b) * n * ncomp + sizeof(int) * n;
+    smem = sizeof(double) * 3 * bstride + sizeof(int) * n;
   }
   if (smem > 210 * 1024 || n > 512) return NOTAPPLICABLE;
   const int threads = 32 * b;
