@@ -242,6 +242,8 @@ int64_t nsk_kernel_launches(void);
  * duration and count since the last collect, and clears them. */
 void nsk_timing_enable(int on);
 int nsk_timing_collect(double* total_ms, int64_t* count);
+/* Name (as ncu prints it) of the kernel most recently timed on this thread. */
+const char* nsk_timing_kernel(void);
 
 #ifdef __cplusplus
 }

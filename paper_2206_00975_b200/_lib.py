@@ -25,7 +25,7 @@ EXPORTS = (
     "nsk_op_sample_indices", "nsk_op_descriptor", "nsk_op_from_descriptor", "nsk_apply",
     "nsk_apply_shard", "nsk_svd_trailing", "nsk_solve_k", "nsk_solve_tol", "nsk_residual_fro",
     "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_residual_fro_host", "nsk_kernel_launches",
-    "nsk_timing_enable", "nsk_timing_collect", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
+    "nsk_timing_enable", "nsk_timing_collect", "nsk_timing_kernel", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
     "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_tls_solve_exact", "nsk_tls_solve_exact_host", "nsk_update_row_host",
     "nsk_downdate_row_host", "nsk_update_column_host",
 )
@@ -95,6 +95,7 @@ def load():
     L.nsk_kernel_launches.restype = i64
     L.nsk_timing_enable.argtypes = [c_int]
     L.nsk_timing_enable.restype = None
+    L.nsk_timing_kernel.restype = ctypes.c_char_p
     L.nsk_timing_collect.argtypes = [dp, i64p]
     for name in EXPORTS:
         getattr(L, name)  # every declared symbol must resolve

@@ -155,21 +155,7 @@ int copy_in(const void* host, int64_t rows, int64_t cols, int64_t ld, int ncomp,
   const size_t elem = sizeof(double) * ncomp;
   NSK_CUDA_OK(s.alloc(elem * (rows > 0 ? rows : 1) * (cols > 0 ? cols : 1), st));
   *dev = s.as<double>();
-  if (rows > 0 && cols > 0)
-    NSK_CUDA_OK(cudaMemcpy2DAsync(*dev, elem * rows, host, elem * ld, elem * rows, cols, cudaMemcpyHostToDevice, st));
-  return nsk::OK;
-}
-
-cudaStream_t copy_stream() {
-  thread_local cudaStream_t cs = nullptr;
-  thread_local int dev = -1;
-  int cur = 0;
-  cudaGetDevice(&cur);
-  if (!cs || dev != cur) {
-    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    dev = cur;
-  }
-  return cs;
+  return nsk::h2d_rows(host, rows, cols, ld, elem, *dev, rows, st, nullptr);
 }
 
 // Host A (m x n, lda) -> SA (device, s x n, ld s).  Large inputs of the
@@ -200,25 +186,12 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   nsk::Scratch parts;
   const int64_t psz = op.s * n * nc_out;
   NSK_CUDA_OK(parts.alloc(sizeof(double) * psz * nchunks, st));
-  cudaStream_t cs = copy_stream();
-  cudaEvent_t ready;
-  NSK_CUDA_OK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  NSK_CUDA_OK(cudaEventRecord(ready, st));  // the stream-ordered allocations exist before the copies
-  NSK_CUDA_OK(cudaStreamWaitEvent(cs, ready, 0));
-  cudaEventDestroy(ready);
-  for (int64_t c = 0; c < nchunks; ++c) {
-    const int64_t r0 = c * chunk, rows = m - r0 < chunk ? m - r0 : chunk;
-    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * nc_in, elem * m, static_cast<const char*>(A) + r0 * elem, elem * lda,
-                                  elem * rows, n, cudaMemcpyHostToDevice, cs));
-    cudaEvent_t landed;
-    NSK_CUDA_OK(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
-    NSK_CUDA_OK(cudaEventRecord(landed, cs));
-    NSK_CUDA_OK(cudaStreamWaitEvent(st, landed, 0));
-    cudaEventDestroy(landed);
+  // each row chunk is sketched (row-shard apply into its own partial) as soon as it has landed
+  auto sketch_chunk = [&](int64_t r0, int64_t rows) {
     nsk::RowMap shard{r0, 1, rows};
-    if (int rc = dispatch_main(op, nc_in, shard, n, dA + r0 * nc_in, m, parts.as<double>() + c * psz, op.s, st))
-      return rc;
-  }
+    return dispatch_main(op, nc_in, shard, n, dA + r0 * nc_in, m, parts.as<double>() + (r0 / chunk) * psz, op.s, st);
+  };
+  if (int rc = nsk::h2d_rows(A, m, n, lda, elem, dA, chunk, st, sketch_chunk)) return rc;
   NSK_CUDA_OK(cudaMemcpyAsync(SA, parts.as<double>(), sizeof(double) * psz, cudaMemcpyDeviceToDevice, st));
   for (int64_t c = 1; c < nchunks; ++c)
     if (int rc = nsk::accumulate(SA, op.s, nc_out, parts.as<double>() + c * psz, op.s, n, nc_out, st)) return rc;

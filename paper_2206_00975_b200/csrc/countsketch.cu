@@ -507,7 +507,7 @@ int launch_cs(const CsParams& p, int64_t groups, int64_t splits, cudaStream_t st
             : MODE == STREAM   ? countsketch_stream_kernel<NC, GB>
                                : countsketch_generic_kernel<NC, GB>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  KernelTimer tm(st, timed);
+  KernelTimer tm(st, MODE == TMA_RING ? "countsketch_tma_kernel" : "countsketch_kernel", timed);
   kern<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)), THREADS, smem, st>>>(p);
   tm.stop();
   count_launch();
@@ -558,7 +558,7 @@ int launch_owner(const CsOwnerParams& p, int64_t splits, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(CS_OWNER_STAGES) * 2 * CS_T * 8;
   auto kern = countsketch_owner_kernel<BPT, CS_OWNER_STAGES>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  KernelTimer tm(st, true);
+  KernelTimer tm(st, "countsketch_owner_kernel", true);
   kern<<<dim3(static_cast<unsigned>((p.n + 1) / 2), static_cast<unsigned>(splits)), CS_THREADS, smem, st>>>(p);
   tm.stop();
   count_launch();

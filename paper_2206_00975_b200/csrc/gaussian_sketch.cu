@@ -304,7 +304,7 @@ int launch(const GaussParams& p0, int64_t n_tiles_q, int64_t s_tiles, int64_t sp
   auto kern = gaussian_sketch_kernel<BN, NCOMP, VEC16>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   dim3 grid(static_cast<unsigned>(s_tiles), static_cast<unsigned>(n_tiles_q), static_cast<unsigned>(splits));
-  KernelTimer tm(st);
+  KernelTimer tm(st, "gaussian_sketch_kernel");
   kern<<<grid, THREADS, smem, st>>>(p0);
   tm.stop();
   count_launch();

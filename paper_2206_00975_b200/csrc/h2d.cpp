@@ -1,0 +1,191 @@
+// h2d.cpp -- host -> device transfer of a caller's column-major matrix for the
+// host-buffer entry points (nsk_apply_host, nsk_solve_k_host, ...).
+//
+// The reference's callers hold ordinary (pageable) Eigen buffers
+// (matrix.hpp:32-105).  A cudaMemcpy from pageable memory is staged by the
+// driver at ~11 GB/s on the B200 hosts; registering the buffer
+// (cudaHostRegister) costs ~0.25 s per 2 GiB (tools/micro/h2d_paths.cu).  So a
+// pageable source is streamed through a ring of pinned 32 MiB slots: host
+// threads pack tiles of the matrix into free slots while the copy engine DMAs
+// the filled ones (48 GB/s measured with 8 threads, against 55.6 GB/s from a
+// pinned source).  A pinned source (cudaHostAlloc / cudaHostRegister memory) is
+// DMAed directly.  Either way the matrix moves in row chunks and the compute
+// stream waits per chunk, so the caller can sketch chunk c while chunk c + 1
+// is in flight.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "nsk_internal.hpp"
+
+namespace nsk {
+
+namespace {
+
+constexpr int RING = 8;                    // pinned slots
+constexpr size_t SLOT = size_t(32) << 20;  // bytes per slot
+
+struct Staging {
+  std::mutex mu;  // one staged transfer at a time per process
+  char* buf = nullptr;
+};
+
+Staging& staging() {
+  static Staging s;
+  return s;
+}
+
+struct Tile {
+  int64_t r0, nr, c0, nc;
+  int64_t chunk_end;  // > 0: last tile of the row chunk ending at this row
+};
+
+}  // namespace
+
+cudaStream_t copy_stream() {
+  thread_local cudaStream_t cs = nullptr;
+  thread_local int dev = -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (!cs || dev != cur) {
+    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    dev = cur;
+  }
+  return cs;
+}
+
+bool host_is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+namespace {
+
+// st waits for everything issued on cs so far.
+int join_streams(cudaStream_t cs, cudaStream_t st) {
+  cudaEvent_t e;
+  NSK_CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  NSK_CUDA_OK(cudaEventRecord(e, cs));
+  NSK_CUDA_OK(cudaStreamWaitEvent(st, e, 0));
+  cudaEventDestroy(e);
+  return OK;
+}
+
+int h2d_pinned(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, char* dA, int64_t chunk,
+               cudaStream_t cs, cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk) {
+  for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+    const int64_t rows = std::min(chunk, m - r0);
+    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * elem, elem * m, A + r0 * elem, elem * lda, elem * rows, n,
+                                  cudaMemcpyHostToDevice, cs));
+    if (int rc = join_streams(cs, st)) return rc;
+    if (on_chunk)
+      if (int rc = on_chunk(r0, rows)) return rc;
+  }
+  return OK;
+}
+
+int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, char* dA, int64_t chunk,
+               cudaStream_t cs, cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk) {
+  Staging& stg = staging();
+  std::lock_guard<std::mutex> lock(stg.mu);
+  if (!stg.buf) NSK_CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&stg.buf), SLOT * RING, cudaHostAllocPortable));
+  // tiles: row chunks, each split into slot-sized (rows x cols) pieces
+  std::vector<Tile> tiles;
+  for (int64_t r0 = 0; r0 < m; r0 += chunk) {
+    const int64_t rows = std::min(chunk, m - r0);
+    const int64_t tr = std::max<int64_t>(1, std::min<int64_t>(rows, static_cast<int64_t>(SLOT / elem)));
+    for (int64_t q0 = r0; q0 < r0 + rows; q0 += tr) {
+      const int64_t nr = std::min(tr, r0 + rows - q0);
+      const int64_t tc = std::max<int64_t>(1, static_cast<int64_t>(SLOT / (elem * nr)));
+      for (int64_t c0 = 0; c0 < n; c0 += tc) tiles.push_back({q0, nr, c0, std::min(tc, n - c0), 0});
+    }
+    tiles.back().chunk_end = r0 + rows;
+  }
+  const size_t T = tiles.size();
+  std::vector<std::atomic<int>> filled(T);
+  for (auto& f : filled) f.store(0, std::memory_order_relaxed);
+  std::atomic<size_t> owner[RING];
+  for (int s = 0; s < RING; ++s) owner[s].store(static_cast<size_t>(s), std::memory_order_relaxed);
+  std::atomic<size_t> next{0};
+  std::atomic<bool> abort{false};
+  const int nthreads = static_cast<int>(std::min<size_t>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())), T));
+  std::vector<std::thread> workers;
+  for (int w = 0; w < nthreads; ++w)
+    workers.emplace_back([&]() {
+      for (;;) {
+        const size_t t = next.fetch_add(1);
+        if (t >= T) return;
+        const int s = static_cast<int>(t % RING);
+        while (owner[s].load(std::memory_order_acquire) != t) {
+          if (abort.load(std::memory_order_relaxed)) return;
+          std::this_thread::yield();
+        }
+        const Tile& tl = tiles[t];
+        char* dst = stg.buf + s * SLOT;
+        const size_t seg = static_cast<size_t>(tl.nr) * elem;
+        for (int64_t c = 0; c < tl.nc; ++c)
+          std::memcpy(dst + c * seg, A + (tl.r0 + (tl.c0 + c) * lda) * elem, seg);
+        filled[t].store(1, std::memory_order_release);
+      }
+    });
+  cudaEvent_t ev[RING];
+  int rc = OK;
+  int made = 0;
+  for (; made < RING && rc == OK; ++made)
+    if (cudaError_t e = cudaEventCreateWithFlags(&ev[made], cudaEventDisableTiming)) rc = cuda_fail(e, "staging event");
+  for (size_t t = 0; t < T && rc == OK; ++t) {
+    const int s = static_cast<int>(t % RING);
+    while (!filled[t].load(std::memory_order_acquire)) std::this_thread::yield();
+    const Tile& tl = tiles[t];
+    cudaError_t e = cudaMemcpy2DAsync(dA + (tl.r0 + tl.c0 * m) * elem, elem * m, stg.buf + s * SLOT, elem * tl.nr,
+                                      elem * tl.nr, tl.nc, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[s], cs);
+    // the previous tile's DMA runs ahead of this one: once it is done its slot goes to the tile RING later
+    if (e == cudaSuccess && t >= 1) {
+      const int ps = static_cast<int>((t - 1) % RING);
+      e = cudaEventSynchronize(ev[ps]);
+      if (e == cudaSuccess) owner[ps].store(t - 1 + RING, std::memory_order_release);
+    }
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "staged host-to-device copy");
+      break;
+    }
+    if (tl.chunk_end > 0) {
+      rc = join_streams(cs, st);
+      const int64_t cend = tl.chunk_end, cstart = (cend - 1) / chunk * chunk;
+      if (rc == OK && on_chunk) rc = on_chunk(cstart, cend - cstart);
+    }
+  }
+  if (rc != OK) abort.store(true);
+  for (auto& w : workers) w.join();
+  // the ring is reused by the next call: its last DMAs must be done
+  if (cudaError_t e = cudaStreamSynchronize(cs); e != cudaSuccess && rc == OK) rc = cuda_fail(e, "staged copy");
+  for (int i = 0; i < made; ++i) cudaEventDestroy(ev[i]);
+  return rc;
+}
+
+}  // namespace
+
+int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void* dA, int64_t chunk,
+             cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk) {
+  if (m <= 0 || n <= 0) return OK;
+  if (chunk <= 0 || chunk > m) chunk = m;
+  cudaStream_t cs = copy_stream();
+  // the destination (stream-ordered allocation on st) exists before the copies start
+  if (int rc = join_streams(st, cs)) return rc;
+  const char* a = static_cast<const char*>(A);
+  char* d = static_cast<char*>(dA);
+  const bool small = static_cast<double>(m) * static_cast<double>(n) * static_cast<double>(elem) < 4.0 * (1 << 20);
+  if (host_is_pinned(A) || small) return h2d_pinned(a, m, n, lda, elem, d, chunk, cs, st, on_chunk);
+  return h2d_staged(a, m, n, lda, elem, d, chunk, cs, st, on_chunk);
+}
+
+}  // namespace nsk

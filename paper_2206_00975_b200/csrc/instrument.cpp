@@ -15,13 +15,15 @@ struct EvPair {
 };
 thread_local std::vector<EvPair> t_pending;
 thread_local std::vector<EvPair> t_free;
+thread_local const char* t_name = "";
 }  // namespace
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-KernelTimer::KernelTimer(cudaStream_t s, bool enabled) : st(s) {
+KernelTimer::KernelTimer(cudaStream_t s, const char* name, bool enabled) : st(s) {
   if (!enabled) return;
   if (!g_timing.load(std::memory_order_relaxed)) return;
+  t_name = name;
   EvPair p;
   if (!t_free.empty()) {
     p = t_free.back();
@@ -48,6 +50,8 @@ extern "C" {
 int64_t nsk_kernel_launches(void) { return nsk::g_launches.load(); }
 
 void nsk_timing_enable(int on) { nsk::g_timing.store(on ? 1 : 0); }
+
+const char* nsk_timing_kernel(void) { return nsk::t_name; }
 
 int nsk_timing_collect(double* total_ms, int64_t* count) {
   double tot = 0.0;

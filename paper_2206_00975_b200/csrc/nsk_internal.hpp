@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <deque>
+#include <functional>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -201,13 +202,26 @@ struct Scratch {
 
 int sm_count();
 
+// ---- host -> device (h2d.cpp) ---------------------------------------------
+// Copies host A (m x n column-major, lda, elem bytes per entry) to device dA
+// (leading dimension m) in row chunks of `chunk` rows on a per-thread copy
+// stream; st waits for each chunk before on_chunk(r0, rows) runs (may be
+// empty).  Pageable sources stream through a pinned staging ring filled by host
+// threads; pinned sources are DMAed directly.
+int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void* dA, int64_t chunk,
+             cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk);
+bool host_is_pinned(const void* p);
+cudaStream_t copy_stream();
+
 // ---- instrumentation -------------------------------------------------------
 void count_launch(int n = 1);
 // Records events around the dominant kernel of an apply when timing is enabled.
+// `name` is the kernel's name as ncu prints it (nsk_timing_kernel reports the
+// name of the most recently timed kernel).
 struct KernelTimer {
   cudaStream_t st;
   void* pair = nullptr;
-  explicit KernelTimer(cudaStream_t s, bool enabled = true);
+  KernelTimer(cudaStream_t s, const char* name, bool enabled = true);
   void stop();
 };
 

@@ -444,7 +444,7 @@ int srdct_stream_apply(const Operator& op, const RowMap& rows, int64_t n, const 
     }
     DStreamParams p{A, lda, N, P, tiles, total, chunk, jmax, tb->srdct_sgn, tb->dct_freq + b, ns,
                     anc.as<double2>(), part.as<double>()};
-    KernelTimer tm(st);
+    KernelTimer tm(st, "srdct_stream_kernel");
     kern<<<static_cast<unsigned>(G), ST, smem, st>>>(p);
     tm.stop();
     count_launch();

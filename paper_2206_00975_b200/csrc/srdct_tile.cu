@@ -339,7 +339,7 @@ int srdct_tile_apply(const Operator& op, const RowMap& rows, int64_t n, const do
     NSK_CUDA_OK(part.alloc(sizeof(double) * items * 1024, st));
     DctParams p{A, lda, m, n, P, tiles, per, ranges, tb->sign_bits, tb->dct_freq + b, ns, part.as<double>()};
     const int64_t grid = items < slots ? items : slots;
-    KernelTimer tm(st);
+    KernelTimer tm(st, "srdct_tile_kernel");
     kern<<<static_cast<unsigned>(grid), 32 * W, smem, st>>>(p);
     tm.stop();
     count_launch();

@@ -328,7 +328,7 @@ int srft_stream_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
     StreamParams p{A, lda, m, P, tiles, per, ranges, items, tb->srft_sgn, tb->srtt_freq + b, ns,
                    part.as<double2>(), anc.as<double2>(), apoints};
     const int64_t grid = items < G ? items : G;
-    KernelTimer tm(st);
+    KernelTimer tm(st, "srft_stream_kernel");
     kern<<<static_cast<unsigned>(grid), FT, smem, st>>>(p);
     tm.stop();
     count_launch();

@@ -339,7 +339,7 @@ int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, 
     }
     WsParams p{A, lda, m, P, tiles, total, chunk, jmax, tb->srft_sgn, tb->srtt_freq + b, ns, anc.as<double2>(),
                part.as<double2>()};
-    KernelTimer tm(st);
+    KernelTimer tm(st, "srft_ws_kernel");
     srft_ws_kernel<<<static_cast<unsigned>(G), XT, smem, st>>>(p);
     tm.stop();
     count_launch();

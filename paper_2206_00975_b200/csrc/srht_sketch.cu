@@ -279,7 +279,7 @@ int launch_srht_lb(SrhtParams p, int64_t warps, cudaStream_t st) {
   const size_t smem = sizeof(double) * WARPS_PER_CTA * ((1 << LB) + (1 << LB) / 32);
   auto kern = srht_kernel<NQ, LB>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  KernelTimer tm(st);
+  KernelTimer tm(st, "srht_kernel");
   kern<<<static_cast<unsigned>(ctas), WARPS_PER_CTA * 32, smem, st>>>(p);
   tm.stop();
   count_launch();

@@ -234,7 +234,7 @@ int launch_fft(const SrttParams& p, int64_t ctas, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (W * UPAD + L + 64);
   auto kern = srtt_fft_kernel<KIND, NCIN, NQ>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  KernelTimer tm(st);
+  KernelTimer tm(st, "srtt_fft_kernel");
   kern<<<static_cast<unsigned>(ctas), T, smem, st>>>(p);
   tm.stop();
   count_launch();

@@ -103,7 +103,7 @@ int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
   if (total == 0) return OK;
   int64_t blocks = (total + 127) / 128;
   if (blocks > 16L * sm_count()) blocks = 16L * sm_count();
-  KernelTimer tm(st);
+  KernelTimer tm(st, op.kind == SRDCT ? "srdct_direct" : "srft_direct");
   count_launch();
   if (op.kind == SRDCT) {
     srdct_direct<<<static_cast<unsigned>(blocks), 128, 0, st>>>(A, lda, rows, n, tb->idx, op.s, op.m, op.key0,

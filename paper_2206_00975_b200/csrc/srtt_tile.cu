@@ -234,7 +234,7 @@ int launch_tile(const TileParams& p, int64_t ctas, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (TL * TROW + TL + TL / 2) + sizeof(uint32_t) * TL;
   auto kern = srtt_tile_kernel<KIND, NCIN>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  KernelTimer tm(st);
+  KernelTimer tm(st, "srtt_tile_kernel");
   kern<<<static_cast<unsigned>(ctas), TT, smem, st>>>(p);
   tm.stop();
   count_launch();

@@ -558,3 +558,25 @@ def test_host_pipelined_sketch(nsk, oracle, kind, s):
     Wref, sref = oracle.from_sketch_svd(oref, 1)
     assert np.max(np.abs(np.asarray(r_host.sketched_singular_values) - sref)) <= 1000 * U * sref[0]
     assert _angle(np.asarray(r_host.W), Wref) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,s,m,n", [("srht", 512, 1 << 21, 40), ("countsketch", 2048, 1 << 21, 33),
+                                        ("srdct", 256, 1 << 20, 9), ("srft", 128, 3 << 18, 5)])
+def test_host_pageable_staging(nsk, oracle, kind, s, m, n):
+    """Pageable host A (the reference callers' Eigen buffers) streams through the library's pinned
+    staging ring (h2d.cpp): several slot-sized tiles per row chunk, a partial last tile, and the
+    unpipelined copy (srdct/srft); SA against the oracle, and pinned input gives the same bytes."""
+    import torch
+    rng = np.random.default_rng(9)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    S = nsk.SketchOperator.draw(kind, s, m, 23)
+    got = nsk.apply(S, A).data
+    assert rel(got, oracle.apply(oracle.draw(kind, s, m, 23), A)) <= SA_TOL
+    pinned = torch.empty((n, m), dtype=torch.float64, pin_memory=True).t()
+    pinned.copy_(torch.from_numpy(A))
+    out = np.empty_like(got, order="F")
+    from paper_2206_00975_b200 import _lib
+    import ctypes
+    _lib.check(_lib.load().nsk_apply_host(S.handle, 0, m, n, ctypes.c_void_p(pinned.data_ptr()), m,
+                                          out.ctypes.data_as(ctypes.c_void_p), s))
+    assert np.array_equal(out, got)
