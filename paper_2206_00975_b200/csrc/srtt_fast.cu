@@ -21,6 +21,8 @@
 // acc += w_m^{a (k1)} F_{k1}[a mod 1024] in registers.  Per-CTA partials
 // are reduced in fixed order.  Requires m % 4096 == 0; other sizes use the
 // direct evaluator.
+#include <cstdlib>
+
 #include "fft32.cuh"
 #include "nsk_internal.hpp"
 
@@ -28,6 +30,8 @@ namespace nsk {
 
 int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                       int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
+int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
+                       int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
 
 // ---- plain sign bitmask for srft/srdct (m/8 bytes) -------------------------
 __global__ void build_sign_bits_kernel(PhiloxKey key, int64_t m, uint32_t* __restrict__ out) {
@@ -255,7 +259,15 @@ int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
                     double* SA, int64_t ldsa, cudaStream_t st) {
   const int64_t m = op.m, s = op.s;
   const bool full = rows.row0 == 0 && rows.rstep == 1 && rows.mloc == m;
-  if (!full || m % (L * W) != 0 || n == 0) return srtt_direct_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+  if (!full || m % (L * W) != 0 || n == 0) {
+    // any other length, and the cyclic shards: the mixed-radix engine (srtt_general.cu); the direct
+    // O(s m n) evaluator only for contiguous partial shards (or NSK_SRTT_DIRECT=1)
+    if (!std::getenv("NSK_SRTT_DIRECT")) {
+      const int rg = srtt_general_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+      if (rg != NOTAPPLICABLE) return rg;
+    }
+    return srtt_direct_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+  }
   const DeviceTables* tb = op.tables();
   if (!tb || !tb->sign_bits) return ECUDA;
   const int kind = op.kind == SRFT ? 0 : 1;

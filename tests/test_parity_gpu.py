@@ -580,3 +580,43 @@ def test_host_pageable_staging(nsk, oracle, kind, s, m, n):
     _lib.check(_lib.load().nsk_apply_host(S.handle, 0, m, n, ctypes.c_void_p(pinned.data_ptr()), m,
                                           out.ctypes.data_as(ctypes.c_void_p), s))
     assert np.array_equal(out, got)
+
+
+# ----------------------------------------------------------------------------- general m and cyclic shards
+
+@pytest.mark.parametrize("kind,m,s,n,cplx", [("srft", 20000, 400, 7, False), ("srdct", 20000, 400, 7, False),
+                                             ("srft", 100000, 300, 5, True), ("srdct", 100000, 300, 5, False),
+                                             ("srft", 99850, 300, 4, True), ("srdct", 99850, 300, 4, False),
+                                             ("srft", 1009, 64, 3, False), ("srdct", 1009, 64, 3, False),
+                                             ("srdct", 840, 840, 2, False), ("srft", 3 * 7 * 5 * 64, 2500, 3, False),
+                                             ("srft", 1000000, 1000, 2, False), ("srdct", 1000000, 1000, 2, False)])
+def test_srtt_general_length(nsk, oracle, kind, m, s, n, cplx):
+    """Exact-length transforms at m not a multiple of 4096 (FFTW transforms any m with no padding,
+    transforms.cpp:17-64, sketch.hpp:34-35): the mixed-radix engine (srtt_general.cu) against
+    numpy/scipy at 1e-12 -- m = 20000, 100000 and 10^6 (the reference's AAA default, aaa.cpp:254-258),
+    99850 = 2 5^2 1997 (the Loewner row count), the prime 1009, s > 2048 (two slot chunks)."""
+    A = oracle.random_complex(m, n, 4) if cplx else oracle.random_real(m, n, 4)
+    got, _ = gpu_apply(nsk, kind, s, m, 41, A)
+    ref = oracle.apply(oracle.draw(kind, s, m, 41), A)
+    assert rel(got, ref) <= SA_TOL
+
+
+@pytest.mark.parametrize("kind,m,P", [("srft", 1 << 17, 4), ("srdct", 1 << 17, 8), ("srft", 20000, 4),
+                                      ("srdct", 20000, 8), ("srdct", 3 << 14, 2), ("srft", 99850, 2)])
+def test_cyclic_shard_partials(nsk, oracle, kind, m, P):
+    """Multi-GPU srft/srdct rows: rank g holds rows g, g+P, ...; its partial is the
+    local length-m/P transform, twiddled and gathered (decimation in time).  Every partial against
+    the oracle applied to A with the other ranks' rows zeroed, and their sum against the full apply."""
+    import torch
+    n, s = 5, 256
+    A = oracle.random_real(m, n, 8)
+    S = nsk.SketchOperator.draw(kind, s, m, 55)
+    op = oracle.draw(kind, s, m, 55)
+    acc = None
+    for g in range(P):
+        part = nsk.apply_shard(S, dev(A[g::P]), g, P)
+        Am = np.zeros_like(A)
+        Am[g::P] = A[g::P]
+        assert rel(host(part), oracle.apply(op, Am)) <= SA_TOL
+        acc = part if acc is None else acc + part
+    assert rel(host(acc), oracle.apply(op, A)) <= SA_TOL
