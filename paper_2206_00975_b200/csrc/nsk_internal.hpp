@@ -124,6 +124,18 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
 int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
 
+// srft / srdct as samples of one DFT of a local sequence (srtt_general.cu): the
+// engine's eligibility (full matrix or cyclic shard g of P with P | m), the
+// per-slot tables of shard g (frequency in [0, N), conjugation flag, shard
+// twiddle) and the fixed-order reduction of per-CTA partials into SA.
+struct Scratch;
+bool srtt_general_eligible(const Operator& op, const RowMap& rows);
+int shard_slot_tables(const Operator& op, int64_t g, int64_t N, Scratch& tab, int64_t** dfreq, double2** dpost,
+                      uint8_t** dconj, cudaStream_t st);
+int srtt_post_reduce(int kind, const double2* part, int64_t rstride, int64_t cstride, int64_t ranges, int64_t n,
+                     int ns, int base, const double2* post, const uint8_t* conj, double scale, double* SA,
+                     int64_t ldsa, cudaStream_t st);
+
 // One-sided Jacobi on [R; I] (2n x n, ld 2n) inside one thread-block cluster
 // (cluster_jacobi.cu); NOTAPPLICABLE when it does not fit one cluster.
 int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cudaStream_t st);

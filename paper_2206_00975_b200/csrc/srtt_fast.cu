@@ -85,6 +85,8 @@ struct SrttParams {
   const int64_t* freq;     // DFT frequency of each output slot (s_pass)
   int nslots;
   double* part;            // [column][range][slot] complex
+  int64_t g, rstep;        // global row of local row k: g + rstep k (cyclic shard; 0, 1 unsharded)
+  double c0, c1;           // KIND 2: orthonormal DCT-III weights of the GLOBAL length
 };
 
 __device__ __forceinline__ double row_sign(const uint32_t* bits, int64_t j) {
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(T, 2) srtt_fft_kernel(SrttParams p) {
     sincospi(static_cast<double>(k) / (L / 2), &sn, &cs);
     tw[k] = make_double2(cs, sn);
   }
-  if (KIND == 1)
+  if (KIND != 0)
     for (int k = threadIdx.x; k < 64; k += T) {
       double sn, cs;
       sincospi(k < 32 ? static_cast<double>(k) / 64.0 : static_cast<double>(k - 32) / 2048.0, &sn, &cs);
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(T, 2) srtt_fft_kernel(SrttParams p) {
     // ---- stage the W strided sequences u[k1 + P k2], k1 = K + w (w is fixed per thread)
     const int w_me = threadIdx.x % W;
     double2 ph_w = make_double2(1.0, 0.0);
-    if (KIND == 1) {  // e^{i pi (K + w) / 2m}
+    if (KIND != 0) {  // e^{i pi (K + w) / 2m}
       double sn, cs;
       sincospi(static_cast<double>(K + w_me) / (2.0 * static_cast<double>(m)), &sn, &cs);
       ph_w = make_double2(cs, sn);
@@ -148,8 +150,13 @@ __global__ void __launch_bounds__(T, 2) srtt_fft_kernel(SrttParams p) {
       const int64_t k = K + w_me + P * k2;
       double2 u;
       if (KIND == 0) {
-        const double sg = row_sign(p.sign_bits, k);
+        const double sg = row_sign(p.sign_bits, p.g + p.rstep * k);
         u = NCIN == 1 ? make_double2(sg * Acol[k], 0.0) : make_double2(sg * Acol[2 * k], sg * Acol[2 * k + 1]);
+      } else if (KIND == 2) {  // srdct of a cyclic shard: c_j d_j x_k w_{4N}^k (srtt_general.cu derivation)
+        const int64_t j = p.g + p.rstep * k;
+        const double xk = (j == 0 ? p.c0 : p.c1) * row_sign(p.sign_bits, j) * Acol[k];
+        const double2 ph = cmul(ph_w, cmul(q32[k2 >> 5], q32[32 + (k2 & 31)]));
+        u = make_double2(ph.x * xk, ph.y * xk);
       } else {
         const double xk = (k == 0 ? 2.0 * c0 : c1) * row_sign(p.sign_bits, k) * Acol[k];
         const double xm = k == 0 ? 0.0 : c1 * row_sign(p.sign_bits, m - k) * Acol[m - k];
@@ -253,12 +260,58 @@ int launch_nq(int nq, const SrttParams& p, int64_t ctas, cudaStream_t st) {
                  : launch_fft<KIND, NCIN, 8>(p, ctas, st);
 }
 
+// Cyclic shard g of P (local length N = m / P, a multiple of 4096): the same strided DFT32 x 32
+// kernel over the local rows with the signs of the global rows; srft samples W[a mod N], srdct
+// takes the complex formulation (KIND 2, srtt_general.cu header); the reduce applies the shard
+// twiddle, the conjugation and the scale.
+int srtt_fast_shard(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                    double* SA, int64_t ldsa, cudaStream_t st) {
+  const DeviceTables* tb = op.tables();
+  if (!tb || !tb->sign_bits) return ECUDA;
+  const int64_t m = op.m, s = op.s, N = rows.mloc;
+  const int kind = op.kind == SRFT ? 0 : 1;
+  Scratch tab;
+  int64_t* dfreq = nullptr;
+  double2* dpost = nullptr;
+  uint8_t* dconj = nullptr;
+  if (int rc = shard_slot_tables(op, rows.row0, N, tab, &dfreq, &dpost, &dconj, st)) return rc;
+  const int64_t P = N / L, bpc = P / W;
+  const int64_t target = 2L * sm_count();
+  int64_t ranges = (target + n - 1) / n;
+  if (ranges > bpc) ranges = bpc;
+  const int64_t per = (bpc + ranges - 1) / ranges;
+  ranges = (bpc + per - 1) / per;
+  const double scale = kind == 0 ? 1.0 / std::sqrt(static_cast<double>(s))
+                                 : std::sqrt(static_cast<double>(m) / static_cast<double>(s));
+  for (int64_t base = 0; base < s; base += 8 * T) {
+    const int ns = static_cast<int>((s - base) < 8 * T ? (s - base) : 8 * T);
+    const int nq = (ns + T - 1) / T;
+    const int NQ = nq <= 2 ? 2 : (nq <= 4 ? 4 : 8);
+    Scratch part;
+    NSK_CUDA_OK(part.alloc(sizeof(double2) * n * ranges * NQ * T, st));
+    SrttParams p{A, lda, N, n, P, bpc, ranges, per, tb->sign_bits, dfreq + base, ns, part.as<double>(),
+                 rows.row0, rows.rstep, std::sqrt(1.0 / static_cast<double>(m)), std::sqrt(2.0 / static_cast<double>(m))};
+    const int64_t ctas = n * ranges;
+    int rc = kind == 0 ? (ncomp == 1 ? launch_nq<0, 1>(NQ, p, ctas, st) : launch_nq<0, 2>(NQ, p, ctas, st))
+                       : launch_nq<2, 1>(NQ, p, ctas, st);
+    if (rc != OK) return rc;
+    // partials are [column][range][slot]
+    if (int rc2 = srtt_post_reduce(kind, reinterpret_cast<const double2*>(part.p), NQ * T, ranges * NQ * T, ranges,
+                                   n, ns, static_cast<int>(base), dpost, dconj, scale, SA, ldsa, st))
+      return rc2;
+  }
+  return OK;
+}
+
 }  // namespace
 
 int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                     double* SA, int64_t ldsa, cudaStream_t st) {
   const int64_t m = op.m, s = op.s;
   const bool full = rows.row0 == 0 && rows.rstep == 1 && rows.mloc == m;
+  if (!full && n > 0 && rows.mloc % (L * W) == 0 && srtt_general_eligible(op, rows) &&
+      !std::getenv("NSK_SRTT_DIRECT") && !(op.kind == SRDCT && ncomp != 1))
+    return srtt_fast_shard(op, ncomp, rows, n, A, lda, SA, ldsa, st);
   if (!full || m % (L * W) != 0 || n == 0) {
     // any other length, and the cyclic shards: the mixed-radix engine (srtt_general.cu); the direct
     // O(s m n) evaluator only for contiguous partial shards (or NSK_SRTT_DIRECT=1)
@@ -294,7 +347,8 @@ int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
     const int NQ = nq <= 2 ? 2 : (nq <= 4 ? 4 : 8);
     Scratch part;
     NSK_CUDA_OK(part.alloc(sizeof(double2) * n * ranges * NQ * T, st));
-    SrttParams p{A, lda, m, n, P, bpc, ranges, per, tb->sign_bits, dfreq.as<int64_t>() + base, ns, part.as<double>()};
+    SrttParams p{A, lda, m, n, P, bpc, ranges, per, tb->sign_bits, dfreq.as<int64_t>() + base, ns, part.as<double>(),
+                 0, 1, 0.0, 0.0};
     const int64_t ctas = n * ranges;
     int rc = kind == 0 ? (ncomp == 1 ? launch_nq<0, 1>(NQ, p, ctas, st) : launch_nq<0, 2>(NQ, p, ctas, st))
                        : launch_nq<1, 1>(NQ, p, ctas, st);

@@ -131,7 +131,7 @@ __device__ void stockham_pass(const double2* __restrict__ in, double2* __restric
     for (int r = 0; r < R; ++r) v[r] = src[j + r * nb];
     if (Ns > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[(r * k * tstep) % Q]);
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r * k * tstep]);  // r k tstep < Q
     }
     small_dft<R>(v);
     const int base = (j / Ns) * Ns * R + k;
@@ -156,13 +156,14 @@ __global__ void __launch_bounds__(GT) srtt_gen_kernel(GenParams p) {
   const int64_t k1lo = static_cast<int64_t>(blockIdx.x) * p.per;
   const int64_t k1hi = p.P2 < k1lo + p.per ? p.P2 : k1lo + p.per;
   const double* Acol = p.A + c * p.lda * NCIN;
-  double2 acc[NQ];
+  double2 acc[NQ], step[NQ];
   int64_t fr[NQ];
 #pragma unroll
   for (int t = 0; t < NQ; ++t) {
     acc[t] = make_double2(0.0, 0.0);
     const int i = threadIdx.x + GT * t;
     fr[t] = i < p.ns ? p.freq[i] : 0;
+    step[t] = root(fr[t], p.N);  // w_N^{f}: the outer twiddle's step from k1 to k1 + 1
   }
   __syncthreads();
   __shared__ double2 seqtw[GG];  // srdct: w_{4N}^{k1} of the batch's sequences
@@ -171,8 +172,9 @@ __global__ void __launch_bounds__(GT) srtt_gen_kernel(GenParams p) {
     if (KIND == 1 && threadIdx.x < G) seqtw[threadIdx.x] = root(kb + threadIdx.x, 4 * p.N);
     if (KIND == 1) __syncthreads();
     // ---- stage u[k1 + P2 k2] for the G sequences (G consecutive local rows per k2)
-    for (int e = threadIdx.x; e < G * Q; e += GT) {
-      const int k2 = e / G, gq = e - k2 * G;
+    for (int e = threadIdx.x; e < GG * Q; e += GT) {
+      const int k2 = e / GG, gq = e % GG;
+      if (gq >= G) continue;
       const int64_t l = kb + gq + p.P2 * k2;
       const int64_t j = p.g + p.P * l;  // global row
       const bool pos = (__ldg(p.sign_bits + (j >> 5)) >> (j & 31)) & 1u;
@@ -213,12 +215,14 @@ __global__ void __launch_bounds__(GT) srtt_gen_kernel(GenParams p) {
       const int i = threadIdx.x + GT * t;
       if (i < p.ns) {
         const int fq = static_cast<int>(fr[t] % Q);
+        // exact anchor w_N^{f kb} once per batch, then G - 1 steps (f kb < N P2 <= 2^62 for N < 2^31)
+        double2 w = root(static_cast<int64_t>((static_cast<uint64_t>(fr[t]) * static_cast<uint64_t>(kb)) %
+                                              static_cast<uint64_t>(p.N)), p.N);
         for (int gq = 0; gq < G; ++gq) {
-          const int64_t k1 = kb + gq;
-          const double2 w = root(static_cast<int64_t>((static_cast<unsigned __int128>(fr[t]) * k1) % p.N), p.N);
-          const double2 v = cmul(w, in[gq * Q + fq]);
-          acc[t].x += v.x;
-          acc[t].y += v.y;
+          const double2 f = in[gq * Q + fq];
+          acc[t].x = fma(w.x, f.x, fma(-w.y, f.y, acc[t].x));
+          acc[t].y = fma(w.x, f.y, fma(w.y, f.x, acc[t].y));
+          w = cmul(w, step[t]);
         }
       }
     }
@@ -231,9 +235,9 @@ __global__ void __launch_bounds__(GT) srtt_gen_kernel(GenParams p) {
 
 // SA[i, c] = scale * post_i * (conj_i ? conj : id)(sum over ranges) -- srft complex, srdct real part.
 template <int KIND>
-__global__ void srtt_gen_reduce(const double2* __restrict__ part, int64_t ranges, int64_t n, int ns, int stride,
-                                int base, const double2* __restrict__ post, const uint8_t* __restrict__ conj,
-                                double scale, double* __restrict__ SA, int64_t ldsa) {
+__global__ void srtt_gen_reduce(const double2* __restrict__ part, int64_t rstride, int64_t cstride, int64_t ranges,
+                                int64_t n, int ns, int base, const double2* __restrict__ post,
+                                const uint8_t* __restrict__ conj, double scale, double* __restrict__ SA, int64_t ldsa) {
   const int64_t total = n * ns;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -241,7 +245,7 @@ __global__ void srtt_gen_reduce(const double2* __restrict__ part, int64_t ranges
     const int i = static_cast<int>(e - c * ns);
     double2 z = make_double2(0.0, 0.0);
     for (int64_t r = 0; r < ranges; ++r) {
-      const double2 v = part[(r * n + c) * stride + i];
+      const double2 v = part[r * rstride + c * cstride + i];
       z.x += v.x;
       z.y += v.y;
     }
@@ -298,26 +302,31 @@ int launch_gen(int nq, const GenParams& p, dim3 grid, size_t smem, cudaStream_t 
 
 }  // namespace
 
-// Whether the engine takes this row map: the full matrix, or a cyclic shard
-// (row0 = g < P = rstep, P divides m, mloc = m / P).
-bool srtt_general_eligible(const Operator& op, const RowMap& rows) {
-  if (rows.rstep < 1 || rows.row0 < 0 || rows.row0 >= rows.rstep) return false;
-  if (op.m % rows.rstep != 0 || rows.mloc != op.m / rows.rstep) return false;
-  return true;
+// Partial layout part[r * rstride + c * cstride + i] (ranges r, columns c, slots i < ns of the chunk at
+// `base`): SA[base + i, c] = scale * Re / complex (post_i * conj_i(sum_r)).  kind 0 srft (complex SA), 1 srdct.
+int srtt_post_reduce(int kind, const double2* part, int64_t rstride, int64_t cstride, int64_t ranges, int64_t n,
+                     int ns, int base, const double2* post, const uint8_t* conj, double scale, double* SA,
+                     int64_t ldsa, cudaStream_t st) {
+  int64_t blocks = (n * ns + 255) / 256;
+  if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+  if (blocks < 1) return OK;
+  if (kind == 0)
+    srtt_gen_reduce<0><<<static_cast<unsigned>(blocks), 256, 0, st>>>(part, rstride, cstride, ranges, n, ns, base,
+                                                                     post, conj, scale, SA, ldsa);
+  else
+    srtt_gen_reduce<1><<<static_cast<unsigned>(blocks), 256, 0, st>>>(part, rstride, cstride, ranges, n, ns, base,
+                                                                     post, conj, scale, SA, ldsa);
+  count_launch();
+  NSK_CUDA_OK(cudaGetLastError());
+  return OK;
 }
 
-int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
-                       double* SA, int64_t ldsa, cudaStream_t st) {
-  if (!srtt_general_eligible(op, rows) || n == 0) return NOTAPPLICABLE;
+// Slot tables of a cyclic shard (first global row g, local length N = m / P; g = 0, N = m unsharded):
+// DFT frequency in [0, N), conjugation flag and shard twiddle per output row (header comment).
+int shard_slot_tables(const Operator& op, int64_t g, int64_t N, Scratch& tab, int64_t** dfreq, double2** dpost,
+                      uint8_t** dconj, cudaStream_t st) {
   const int kind = op.kind == SRFT ? 0 : 1;
-  if (kind == 1 && ncomp != 1) return NOTAPPLICABLE;
-  const DeviceTables* tb = op.tables();
-  if (!tb || !tb->sign_bits) return ECUDA;
-  const int64_t m = op.m, s = op.s, P = rows.rstep, g = rows.row0, N = rows.mloc;
-  std::vector<int> radix;
-  const int64_t Q = plan_q(N, radix);
-  if (static_cast<int>(radix.size()) > MAXPASS) return NOTAPPLICABLE;
-  const int64_t P2 = N / Q;
+  const int64_t m = op.m, s = op.s;
   // slot tables: frequency, conjugation, shard twiddle
   std::vector<int64_t> freq(static_cast<size_t>(s));
   std::vector<uint8_t> conj(static_cast<size_t>(s), 0);
@@ -344,15 +353,42 @@ int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_
     const double ang = 2.0 * M_PI * static_cast<double>(e) / static_cast<double>(K);
     post[i] = make_double2(std::cos(ang), std::sin(ang));
   }
-  Scratch dtab;
   const size_t bytes = sizeof(int64_t) * s + sizeof(double2) * s + s;
-  NSK_CUDA_OK(dtab.alloc(bytes, st));
-  int64_t* dfreq = dtab.as<int64_t>();
-  double2* dpost = reinterpret_cast<double2*>(dfreq + s);
-  uint8_t* dconj = reinterpret_cast<uint8_t*>(dpost + s);
-  NSK_CUDA_OK(cudaMemcpyAsync(dfreq, freq.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, st));
-  NSK_CUDA_OK(cudaMemcpyAsync(dpost, post.data(), sizeof(double2) * s, cudaMemcpyHostToDevice, st));
-  NSK_CUDA_OK(cudaMemcpyAsync(dconj, conj.data(), s, cudaMemcpyHostToDevice, st));
+  NSK_CUDA_OK(tab.alloc(bytes, st));
+  *dpost = tab.as<double2>();  // 16-byte entries first: every table stays aligned for any s
+  *dfreq = reinterpret_cast<int64_t*>(*dpost + s);
+  *dconj = reinterpret_cast<uint8_t*>(*dfreq + s);
+  NSK_CUDA_OK(cudaMemcpyAsync(*dfreq, freq.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice, st));
+  NSK_CUDA_OK(cudaMemcpyAsync(*dpost, post.data(), sizeof(double2) * s, cudaMemcpyHostToDevice, st));
+  NSK_CUDA_OK(cudaMemcpyAsync(*dconj, conj.data(), s, cudaMemcpyHostToDevice, st));
+  return OK;
+}
+
+// Whether the engine takes this row map: the full matrix, or a cyclic shard
+// (row0 = g < P = rstep, P divides m, mloc = m / P).
+bool srtt_general_eligible(const Operator& op, const RowMap& rows) {
+  if (rows.rstep < 1 || rows.row0 < 0 || rows.row0 >= rows.rstep) return false;
+  if (op.m % rows.rstep != 0 || rows.mloc != op.m / rows.rstep) return false;
+  return true;
+}
+
+int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                       double* SA, int64_t ldsa, cudaStream_t st) {
+  if (!srtt_general_eligible(op, rows) || n == 0 || rows.mloc >= (int64_t(1) << 31)) return NOTAPPLICABLE;
+  const int kind = op.kind == SRFT ? 0 : 1;
+  if (kind == 1 && ncomp != 1) return NOTAPPLICABLE;
+  const DeviceTables* tb = op.tables();
+  if (!tb || !tb->sign_bits) return ECUDA;
+  const int64_t m = op.m, s = op.s, P = rows.rstep, g = rows.row0, N = rows.mloc;
+  std::vector<int> radix;
+  const int64_t Q = plan_q(N, radix);
+  if (static_cast<int>(radix.size()) > MAXPASS) return NOTAPPLICABLE;
+  const int64_t P2 = N / Q;
+  Scratch dtab;
+  int64_t* dfreq = nullptr;
+  double2* dpost = nullptr;
+  uint8_t* dconj = nullptr;
+  if (int rc = shard_slot_tables(op, g, N, dtab, &dfreq, &dpost, &dconj, st)) return rc;
   // CTA ranges of k1: about two CTAs per SM over all columns, each range a multiple of G
   const int64_t target = 2L * sm_count();
   int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((target + n - 1) / n, (P2 + GG - 1) / GG));
@@ -392,18 +428,9 @@ int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_
     int rc = kind == 0 ? (ncomp == 1 ? launch_gen<0, 1>(nq, p, grid, smem, st) : launch_gen<0, 2>(nq, p, grid, smem, st))
                        : launch_gen<1, 1>(nq, p, grid, smem, st);
     if (rc != OK) return rc;
-    int64_t blocks = (n * ns + 255) / 256;
-    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-    if (kind == 0)
-      srtt_gen_reduce<0><<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double2>(), ranges, n, ns, NQ * GT,
-                                                                       static_cast<int>(base), dpost, dconj, scale,
-                                                                       SA, ldsa);
-    else
-      srtt_gen_reduce<1><<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double2>(), ranges, n, ns, NQ * GT,
-                                                                       static_cast<int>(base), dpost, dconj, scale,
-                                                                       SA, ldsa);
-    count_launch();
-    NSK_CUDA_OK(cudaGetLastError());
+    if (int rc2 = srtt_post_reduce(kind, part.as<double2>(), n * NQ * GT, NQ * GT, ranges, n, ns, static_cast<int>(base),
+                                   dpost, dconj, scale, SA, ldsa, st))
+      return rc2;
   }
   return OK;
 }
