@@ -182,6 +182,7 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   }
   NSK_CUDA_OK(a_buf.alloc(elem * m * n, st));
   dA = a_buf.as<double>();
+  if (!op.tables(0, m)) return nsk::ECUDA;  // one table window for all chunks (CountSketch)
   const int64_t nchunks = (m + chunk - 1) / chunk;
   nsk::Scratch parts;
   const int64_t psz = op.s * n * nc_out;

@@ -61,14 +61,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
 
 // Row table entry: bits 0-15 bucket, bit 16 sign(+1), bit 17 leader,
 // bits 18-26 offset of the next same-bucket row in the 512-row tile (0 = none).
-__global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, uint32_t* __restrict__ out) {
+// Rows [base, base + rows) (base a multiple of CT), entry of global row i at out[i - base].
+__global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, int64_t base, int64_t rows,
+                                      uint32_t* __restrict__ out) {
   __shared__ uint32_t bucket[CT];
-  const int64_t ntiles = (m + CT - 1) / CT;
+  const int64_t ntiles = (rows + CT - 1) / CT, end = base + rows;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     for (int r = threadIdx.x; r < CT; r += blockDim.x) {
-      const int64_t i = tile * CT + r;
+      const int64_t i = base + tile * CT + r;
       uint32_t b = 0xFFFFFFFFu;
-      if (i < m) {
+      if (i < end) {
         const uint64_t w = static_cast<uint64_t>(m) + 2u * static_cast<uint64_t>(i);
         const uint64_t u = (static_cast<uint64_t>(stream_word(key, w + 1)) << 32) | stream_word(key, w);
         b = static_cast<uint32_t>(mulhi64(u, static_cast<uint64_t>(s)));
@@ -77,8 +79,8 @@ __global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, uint3
     }
     __syncthreads();
     for (int r = threadIdx.x; r < CT; r += blockDim.x) {
-      const int64_t i = tile * CT + r;
-      if (i >= m) continue;
+      const int64_t i = base + tile * CT + r;
+      if (i >= end) continue;
       const uint32_t b = bucket[r];
       bool leader = true;
       for (int q = 0; q < r; ++q)
@@ -93,18 +95,19 @@ __global__ void build_cs_table_kernel(PhiloxKey key, int64_t m, int64_t s, uint3
           break;
         }
       const uint32_t sg = stream_word(key, static_cast<uint64_t>(i)) & 1u;
-      out[i] = (b & 0xFFFFu) | (sg << 16) | (static_cast<uint32_t>(leader) << 17) | (next << 18);
+      out[i - base] = (b & 0xFFFFu) | (sg << 16) | (static_cast<uint32_t>(leader) << 17) | (next << 18);
     }
     __syncthreads();
   }
 }
 
-int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out) {
+int build_cs_table(PhiloxKey key, int64_t m, int64_t s, int64_t base, int64_t rows, uint32_t** out) {
   *out = nullptr;
-  NSK_CUDA_OK(cudaMalloc(out, sizeof(uint32_t) * m));
-  const int64_t ntiles = (m + CT - 1) / CT;
+  if (rows <= 0) return OK;
+  NSK_CUDA_OK(cudaMalloc(out, sizeof(uint32_t) * rows));
+  const int64_t ntiles = (rows + CT - 1) / CT;
   int64_t blocks = ntiles < 16L * sm_count() ? ntiles : 16L * sm_count();
-  build_cs_table_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, m, s, *out);
+  build_cs_table_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, m, s, base, rows, *out);
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
   NSK_CUDA_OK(cudaDeviceSynchronize());
@@ -124,7 +127,7 @@ struct CsParams {
   int64_t n;
   int64_t s;
   const uint32_t* table;  // indexed by global row
-  int64_t row0;           // global row of local row 0 (multiple of CT)
+  int64_t row0;           // table row (window-relative) of local row 0 (multiple of CT)
   int64_t t0;             // first tile (local) handled by split 0
   int64_t ntiles;         // tiles handled by this launch
   int64_t per;            // tiles per split
@@ -581,12 +584,13 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   if (rows.rstep != 1 || rows.row0 % CT != 0)
     return fail(EINVAL_, "countsketch shard: rows must be contiguous and start at a multiple of 512");
   if (s > 65536) return fail(EINVAL_, "countsketch: this build supports s <= 65536");
-  const DeviceTables* tb = op.tables();
-  if (!tb || !tb->cs_table) return ECUDA;
   if (mloc == 0) {
     for (int64_t c = 0; c < n; ++c) NSK_CUDA_OK(cudaMemsetAsync(SA + c * ldsa, 0, sizeof(double) * s, st));
     return OK;
   }
+  const DeviceTables* tb = op.tables(rows.row0, rows.row0 + mloc);  // this shard's row window
+  if (!tb || !tb->cs_table) return ECUDA;
+  const int64_t wrow0 = rows.row0 - tb->cs_base;  // local row 0 inside the window
   // Columns per CTA: up to 32 KiB of shared-memory bins (3+ CTAs per SM keep
   // enough independent tiles in flight to cover the per-tile barrier).
   int NC = static_cast<int>(32768 / (s * 8));
@@ -598,8 +602,8 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   // Owner kernel over the leading T-row tiles that have a schedule.
   const int T = CS_T;
   int64_t own_tiles = 0, splits_o = 0, per_o = 0;
-  if (aligned && tb->cs_ent && rows.row0 % T == 0) {
-    const int64_t g0 = rows.row0 / T;
+  if (aligned && tb->cs_ent && wrow0 % T == 0) {
+    const int64_t g0 = wrow0 / T;
     own_tiles = mloc / T;
     if (own_tiles > tb->cs_ntiles - g0) own_tiles = tb->cs_ntiles - g0 > 0 ? tb->cs_ntiles - g0 : 0;
   }
@@ -647,7 +651,7 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   if (gb && splits_f + splits_r > 0)
     NSK_CUDA_OK(gbins.alloc(sizeof(double) * (splits_f + splits_r) * groups * NC * s, st));
   if (own_tiles > 0) {
-    CsOwnerParams p{A, lda, n, s, tb->cs_ent, tb->cs_cnt, rows.row0 / T, own_tiles, per_o, 0, part.as<double>()};
+    CsOwnerParams p{A, lda, n, s, tb->cs_ent, tb->cs_cnt, wrow0 / T, own_tiles, per_o, 0, part.as<double>()};
     const int bpt = static_cast<int>((s + CS_THREADS - 1) / CS_THREADS);
     const int rc = bpt == 1 ? launch_owner<1>(p, splits_o, st)
                  : bpt == 2 ? launch_owner<2>(p, splits_o, st)
@@ -655,7 +659,7 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
     if (rc) return rc;
   }
   if (full > 0) {
-    CsParams p{Ar, lda, n, s, tb->cs_table, rest_map.row0, 0, full, per_f, CT, splits_o, part.as<double>(),
+    CsParams p{Ar, lda, n, s, tb->cs_table, rest_map.row0 - tb->cs_base, 0, full, per_f, CT, splits_o, part.as<double>(),
                gb ? gbins.as<double>() : nullptr};
     const bool timed = own_tiles == 0;  // one timed (dominant) kernel per apply
     const int rc = use_tma_ring() ? launch_nc<TMA_RING>(NC, gb, p, groups, splits_f, st, timed)
@@ -664,7 +668,8 @@ int countsketch_apply(const Operator& op, const RowMap& rows, int64_t n, const d
   }
   if (rest_tiles > 0) {
     const int64_t last_rows = rest_rows - (rest_tiles - 1) * CT;
-    CsParams p{Ar, lda, n, s, tb->cs_table, rest_map.row0, full, rest_tiles, per_r, last_rows, splits_o + splits_f,
+    CsParams p{Ar, lda, n, s, tb->cs_table, rest_map.row0 - tb->cs_base, full, rest_tiles, per_r, last_rows,
+               splits_o + splits_f,
                part.as<double>(),
                gb ? gbins.as<double>() + splits_f * groups * NC * s : nullptr};
     if (int rc = launch_nc<GENERIC>(NC, gb, p, groups, splits_r, st, full == 0 && own_tiles == 0)) return rc;

@@ -41,7 +41,10 @@ struct DeviceTables {
   // CountSketch owner schedule (cs_schedule.cpp) over CS_T-row tiles.
   uint64_t* cs_ent = nullptr;       // [tile][warp][CS_GMAX][32] packed entries
   uint8_t* cs_cnt = nullptr;        // [tile][warp] iterations
-  int64_t cs_ntiles = 0;            // full tiles covered (global tiles 0 .. cs_ntiles-1)
+  int64_t cs_ntiles = 0;            // full tiles covered (window tiles 0 .. cs_ntiles-1)
+  // CountSketch row window: cs_table / the schedule cover global rows [cs_base, cs_base + cs_rows)
+  // (cs_base a multiple of CS_T), so a rank of the multi-GPU path holds tables for its shard only.
+  int64_t cs_base = 0, cs_rows = 0;
 };
 
 // CountSketch owner kernel geometry (countsketch.cu / cs_schedule.cpp).
@@ -59,7 +62,7 @@ bool cs_owner_eligible(int64_t s, int64_t m);
 
 // Device-side table builders (run once per operator and device).
 int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out);
-int build_cs_table(PhiloxKey key, int64_t m, int64_t s, uint32_t** out);
+int build_cs_table(PhiloxKey key, int64_t m, int64_t s, int64_t base, int64_t rows, uint32_t** out);
 int build_sign_bits(PhiloxKey key, int64_t m, uint32_t** out);
 int build_srdct_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out);  // null when m % 16384 != 0
 int build_srft_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out);  // null when m % 16384 != 0
@@ -92,7 +95,10 @@ struct Operator {
 
   mutable std::mutex mu;
   mutable std::deque<DeviceTables> dev;  // one entry per device used (stable addresses)
-  const DeviceTables* tables() const;      // uploads on first use on the current device
+  // Uploads on first use on the current device.  CountSketch tables cover a row window: the first
+  // call that needs rows [row_lo, row_hi) not covered yet builds one for them (tile-aligned);
+  // row_hi < 0 means m, row_hi <= row_lo means no CountSketch rows are needed.
+  const DeviceTables* tables(int64_t row_lo = 0, int64_t row_hi = -1) const;
   // Device bitmask of the zeroed rows (m_eff bits) on the current device, or
   // nullptr when no row is zeroed.  Re-uploaded after every downdate.
   const uint32_t* zero_mask() const;

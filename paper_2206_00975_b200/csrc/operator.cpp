@@ -181,14 +181,20 @@ int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out)
   return OK;
 }
 
-const DeviceTables* Operator::tables() const {
+const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
   int devno = 0;
   if (cudaGetDevice(&devno) != cudaSuccess) return nullptr;
+  if (row_hi < 0) row_hi = m;
+  const bool window = kind == COUNTSKETCH && row_hi > row_lo;
   std::lock_guard<std::mutex> lock(mu);
   for (auto& t : dev)
-    if (t.device == devno) return &t;
+    if (t.device == devno && (!window || (t.cs_base <= row_lo && row_hi <= t.cs_base + t.cs_rows))) return &t;
   DeviceTables t;
   t.device = devno;
+  if (window) {  // tile-aligned window around the requested rows
+    t.cs_base = row_lo / CS_T * CS_T;
+    t.cs_rows = std::min<int64_t>(m, (row_hi + CS_T - 1) / CS_T * CS_T) - t.cs_base;
+  }
   auto up = [](void** dst, const void* src, size_t bytes) {
     if (bytes == 0) return cudaSuccess;
     cudaError_t e = cudaMalloc(dst, bytes);
@@ -206,10 +212,11 @@ const DeviceTables* Operator::tables() const {
     return nullptr;
   }
   if (kind == SRHT && m >= 1024 && build_sign_mask(key0, m, &t.sign_mask) != OK) return nullptr;
-  if (kind == COUNTSKETCH && s <= 65536 && build_cs_table(key0, m, s, &t.cs_table) != OK) return nullptr;
-  if (kind == COUNTSKETCH && cs_owner_eligible(s, m)) {
-    // Owner schedule over the full CS_T-row tiles, from the device row table.
-    const int64_t ntiles = m / CS_T;
+  if (kind == COUNTSKETCH && s <= 65536 && build_cs_table(key0, m, s, t.cs_base, t.cs_rows, &t.cs_table) != OK)
+    return nullptr;
+  if (kind == COUNTSKETCH && t.cs_rows > 0 && cs_owner_eligible(s, m)) {
+    // Owner schedule over the window's full CS_T-row tiles, from the device row table.
+    const int64_t ntiles = t.cs_rows / CS_T;
     std::vector<uint32_t> tab(static_cast<size_t>(ntiles * CS_T));
     std::vector<uint64_t> ent;
     std::vector<uint8_t> cnt;

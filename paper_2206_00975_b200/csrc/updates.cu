@@ -114,7 +114,7 @@ unsigned grid_for(int64_t work) {
 }  // namespace
 
 int sketch_column(const Operator& op, int64_t j, double* out, int ncomp_out, cudaStream_t st) {
-  const DeviceTables* tb = op.tables();
+  const DeviceTables* tb = op.tables(0, 0);  // the sample indices only (no CountSketch row window)
   if (!tb) return ECUDA;
   ColParams p{op.kind, op.s, op.m, j, op.key0, op.key1, tb->idx, 0u, 1.0};
   if (op.kind == COUNTSKETCH && j < op.m) {  // h(j) = below(s) of words m+2j, m+2j+1; sigma(j) = word j

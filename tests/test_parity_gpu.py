@@ -620,3 +620,25 @@ def test_cyclic_shard_partials(nsk, oracle, kind, m, P):
         assert rel(host(part), oracle.apply(op, Am)) <= SA_TOL
         acc = part if acc is None else acc + part
     assert rel(host(acc), oracle.apply(op, A)) <= SA_TOL
+
+
+@pytest.mark.parametrize("splits", [[0, 12288 * 3, 12288 * 7, 100000], [0, 512 * 5, 4096 * 9, 4096 * 9 + 512, 100000]])
+def test_countsketch_shard_windows(nsk, oracle, splits):
+    """CountSketch shards build tables for their own rows only (a tile-aligned window, operator.cpp
+    tables(lo, hi)): each shard's partial against the oracle on A with the other rows zeroed, fresh
+    operators per shard order (first use builds the window), and the sum against the full apply."""
+    m, n, s = 100000, 6, 2048
+    A = oracle.random_real(m, n, 12)
+    op = oracle.draw("countsketch", s, m, 77)
+    for order in (list(range(len(splits) - 1)), list(reversed(range(len(splits) - 1)))):
+        S = nsk.SketchOperator.draw("countsketch", s, m, 77)
+        acc = np.zeros((s, n))
+        for i in order:
+            a, b = splits[i], splits[i + 1]
+            part = host(nsk.apply_shard(S, dev(A[a:b]), a))
+            Am = np.zeros_like(A)
+            Am[a:b] = A[a:b]
+            assert rel(part, oracle.apply(op, Am)) <= SA_TOL
+            acc += part
+        assert rel(acc, oracle.apply(op, A)) <= SA_TOL
+        assert rel(host(nsk.apply(S, dev(A)).data), oracle.apply(op, A)) <= SA_TOL
