@@ -347,13 +347,20 @@ def run_ours(args):
     S = nsk.SketchOperator.draw(kind, s, m_glob, 9000002)
     A = make_input(key, mloc, n, k, 1234 + rank, dev)
     stream = torch.cuda.current_stream()
+    comm = shard = None
+    # N > 1 (or NSK_BENCH_SHARDED=1 on one GPU, to exercise it): the library's own NCCL path
+    # (nsk_apply_allreduce: partial + ncclAllReduce in one call)
+    sharded = world > 1 or os.environ.get("NSK_BENCH_SHARDED") == "1"
+    if sharded:
+        from paper_2206_00975_b200.distributed import NcclComm, RowShard, sharded_apply_nccl
+        comm = NcclComm()
+        # srft / srdct: cyclic shards (decimation in time); the others: contiguous row blocks
+        shard = RowShard(rank, world, mloc) if kind in ("srft", "srdct") else RowShard(rank * mloc, 1, mloc)
 
     def step():
-        if world == 1:
+        if not sharded:
             return nsk.apply(S, A).data
-        part = nsk.apply_shard(S, A, rank * mloc)
-        dist.all_reduce(part)
-        return part
+        return sharded_apply_nccl(S, A, shard, comm)
 
     for _ in range(args.warmup):
         step()
@@ -424,7 +431,7 @@ def run_ours(args):
     svd_ms = t0.elapsed_time(t1)
 
     # ---- e2e through the C ABI with host buffers (rank-local shard on N > 1).
-    e2e = e2e_measure(nsk, cfg, A, args, world, rank, mloc)
+    e2e = e2e_measure(nsk, cfg, A, args, world, rank, mloc, comm)
     del A
     torch.cuda.empty_cache()
 
@@ -449,13 +456,15 @@ def run_ours(args):
             "breakdown": {"apply_ms": round(ms_per_step, 4), "svd_ms": round(svd_ms, 3),
                           "hbm_gbs_step": round(byts / (ms_per_step / 1e3) / 1e9, 1)},
         }
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
 
 
-def e2e_measure(nsk, cfg, A, args, world, rank, mloc):
+def e2e_measure(nsk, cfg, A, args, world, rank, mloc, comm=None):
     """The user's call per step: nsk_op_draw + nsk_solve_k_host + nsk_op_destroy, A in host memory
     (pageable, the reference callers' Eigen buffers; and pinned), W and sigma back in host memory."""
     import numpy as np
@@ -467,8 +476,8 @@ def e2e_measure(nsk, cfg, A, args, world, rank, mloc):
     dt = torch.complex128 if cfg["cplx"] else torch.float64
     Ah_pin = torch.empty((n, mloc), dtype=dt, pin_memory=True).t()
     Ah_pin.copy_(A)
-    if world > 1:
-        return e2e_sharded(nsk, cfg, Ah_pin, steps, rank, mloc)
+    if comm is not None:
+        return e2e_sharded(nsk, cfg, Ah_pin, steps, rank, mloc, comm)
     Ah_page = np.asfortranarray(Ah_pin.numpy().copy())  # ordinary malloc'd host memory
     cplx_out = kind == "srft" or cfg["cplx"]
     W = np.empty((n, k), dtype=np.complex128 if cplx_out else np.float64, order="F")
@@ -504,27 +513,28 @@ def e2e_measure(nsk, cfg, A, args, world, rank, mloc):
                        "api": "same call with A in pinned (cudaHostAlloc) memory"}}
 
 
-def e2e_sharded(nsk, cfg, Ah, steps, rank, mloc):
-    """N > 1: every rank draws the operator, copies its pinned host shard in, sketches it, the partials
-    are all-reduced, rank 0 runs the SVD and W / sigma are broadcast and copied out
-    (paper_2206_00975_b200.distributed.sharded_solve_k); device time, max over ranks."""
+def e2e_sharded(nsk, cfg, Ah, steps, rank, mloc, comm):
+    """N > 1: every rank draws the operator, copies its pinned host shard in, and calls
+    nsk_solve_k_sharded (partial sketch, ncclAllReduce, SVD on every rank), then W / sigma come
+    back to the host; device time, max over ranks."""
     import torch
     import torch.distributed as dist
-    from paper_2206_00975_b200.distributed import RowShard, sharded_solve_k
+    from paper_2206_00975_b200.distributed import RowShard, sharded_solve_k_nccl
     dev = torch.device("cuda", torch.cuda.current_device())
     n, k = cfg["n"], cfg["k"]
     Ad = torch.empty((n, mloc), dtype=Ah.dtype, device=dev).t()
-    world = dist.get_world_size()
-    shard = RowShard(rank * mloc, 1, mloc)
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    shard = RowShard(rank, world, mloc) if cfg["kind"] in ("srft", "srdct") else RowShard(rank * mloc, 1, mloc)
 
     def one():
         S = nsk.SketchOperator.draw(cfg["kind"], cfg["s"], world * mloc, 9000002)
         Ad.copy_(Ah, non_blocking=True)
-        W, sig = sharded_solve_k(S, Ad, k, shard)
+        W, sig = sharded_solve_k_nccl(S, Ad, k, shard, comm)
         return W.cpu(), sig.cpu()
 
     one()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -533,11 +543,12 @@ def e2e_sharded(nsk, cfg, Ah, steps, rank, mloc):
     e1.record()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / steps], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = t.item() / 1e3
     return {"value": world * mloc / dt, "unit": "rows/s", "ms": round(dt * 1e3, 3), "steps": steps,
-            "api": "draw + distributed.sharded_solve_k (pinned H2D of each shard, apply_shard, NCCL all-reduce, "
-                   "Jacobi SVD on rank 0, broadcast, D2H of W and sigma)",
+            "api": "draw + nsk_solve_k_sharded (pinned H2D of each shard, partial sketch, ncclAllReduce, "
+                   "Jacobi SVD on every rank, D2H of W and sigma)",
             "h2d_bytes_per_step": world * mloc * n * Ah.element_size(),
             "d2h_bytes_per_step": int(W.numel() * W.element_size() + sig.numel() * 8)}
 

@@ -231,6 +231,29 @@ int nsk_tls_solve_exact_host(int scalar, int64_t m, int64_t n, int64_t k, const 
                              const void* B, int64_t ldb, double cond_limit, int allow_marginal, void* X,
                              int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info);
 
+/* ---- multi-GPU: row shards + NCCL (one process per GPU) ------------------
+ * SA = sum_g S[:, rows_g] A_g.  Rank g holds local rows j of
+ * A_local = global rows row0 + rstep * j (contiguous shards: rstep = 1; srft /
+ * srdct cyclic shards: row0 = g, rstep = P, P | m).  The operator regenerates S
+ * for the global rows; one ncclAllReduce (sum, FP64) of the s x n partials on
+ * `nccl_comm` (an ncclComm_t) leaves the same SA on every rank.  Callers of the
+ * reference API this replaces: solve_k (nullspace.hpp:24, nullspace.cpp:23-32)
+ * and apply (sketch.hpp:89) with A row-sharded across GPUs.  NCCL is loaded at
+ * run time (libnccl.so.2, or NSK_NCCL_LIB); NSK_ECUDA if it is absent. */
+#define NSK_NCCL_UNIQUE_ID_BYTES 128
+/* ncclGetUniqueId / ncclCommInitRank / ncclCommDestroy for callers without a communicator. */
+int nsk_nccl_unique_id(char* id_out /* NSK_NCCL_UNIQUE_ID_BYTES */);
+int nsk_nccl_comm_init(int nranks, const char* id, int rank, void** comm_out);
+int nsk_nccl_comm_destroy(void* comm);
+/* SA (device, s x n, ldsa) = the full sketch, on every rank. */
+int nsk_apply_allreduce(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep, int64_t mloc, int64_t n,
+                        const void* A_local, int64_t lda, void* SA, int64_t ldsa, void* nccl_comm, void* stream);
+/* solve_k on row shards: the all-reduced SA, then the on-device SVD on every rank (bitwise-identical SA
+ * gives identical W and sigma everywhere).  W (device, n x k, ldw), sigma (device, n). */
+int nsk_solve_k_sharded(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep, int64_t mloc, int64_t n,
+                        const void* A_local, int64_t lda, int64_t k, void* W, int64_t ldw, double* sigma,
+                        void* nccl_comm, void* stream);
+
 /* ---- instrumentation (bench.py; no effect on results) ------------------- */
 
 /* Number of CUDA kernels this library has launched in this process. */

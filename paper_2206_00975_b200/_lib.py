@@ -27,7 +27,8 @@ EXPORTS = (
     "nsk_apply_host", "nsk_solve_k_host", "nsk_solve_tol_host", "nsk_residual_fro_host", "nsk_kernel_launches",
     "nsk_timing_enable", "nsk_timing_collect", "nsk_timing_kernel", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
     "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_tls_solve_exact", "nsk_tls_solve_exact_host", "nsk_update_row_host",
-    "nsk_downdate_row_host", "nsk_update_column_host",
+    "nsk_downdate_row_host", "nsk_update_column_host", "nsk_nccl_unique_id", "nsk_nccl_comm_init",
+    "nsk_nccl_comm_destroy", "nsk_apply_allreduce", "nsk_solve_k_sharded",
 )
 
 
@@ -92,6 +93,11 @@ def load():
                                       i64, vp, dp, vp]
     L.nsk_tls_solve_exact_host.argtypes = [c_int, i64, i64, i64, vp, i64, vp, i64, ctypes.c_double, c_int, vp, i64,
                                            vp, i64, vp, dp]
+    L.nsk_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.nsk_nccl_comm_init.argtypes = [c_int, ctypes.c_char_p, c_int, ctypes.POINTER(vp)]
+    L.nsk_nccl_comm_destroy.argtypes = [vp]
+    L.nsk_apply_allreduce.argtypes = [vp, c_int, i64, i64, i64, i64, vp, i64, vp, i64, vp, vp]
+    L.nsk_solve_k_sharded.argtypes = [vp, c_int, i64, i64, i64, i64, vp, i64, i64, vp, i64, vp, vp, vp]
     L.nsk_kernel_launches.restype = i64
     L.nsk_timing_enable.argtypes = [c_int]
     L.nsk_timing_enable.restype = None

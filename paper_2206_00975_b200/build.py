@@ -22,7 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 SOURCES = ["operator.cpp", "capi.cpp", "gaussian_sketch.cu", "srht_sketch.cu", "countsketch.cu",
            "srtt_sketch.cu", "srtt_fast.cu", "srtt_general.cu", "jacobi_svd.cu", "residual.cu", "instrument.cpp", "updates.cu",
-           "cs_schedule.cpp", "h2d.cpp", "cluster_jacobi.cu", "srtt_tile.cu", "tall_qr.cu", "srdct_tile.cu", "srft_stream.cu", "srdct_stream.cu", "srft_ws.cu", "srdct_ws.cu"]
+           "cs_schedule.cpp", "h2d.cpp", "nccl_shard.cpp", "cluster_jacobi.cu", "srtt_tile.cu", "tall_qr.cu", "srdct_tile.cu", "srft_stream.cu", "srdct_stream.cu", "srft_ws.cu", "srdct_ws.cu"]
 
 
 def _deps():
@@ -30,10 +30,24 @@ def _deps():
         os.path.join(HERE, "..", "include", "nullsketch_b200.h")]
 
 
+def _nccl_dirs():
+    """nccl.h (types only; the library is dlopened at run time) from the torch-bundled NCCL wheel."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+    except Exception:
+        base = "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"
+    return os.path.join(base, "include"), os.path.join(base, "lib", "libnccl.so.2")
+
+
 def _compile(src):
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
     lang = ["-x", "cu"] if src.endswith(".cpp") else []
-    cmd = [NVCC, *ARCH, *FLAGS, *lang, "-c", os.path.join(CSRC, src), "-o", obj]
+    extra = []
+    if src == "nccl_shard.cpp":
+        inc, lib = _nccl_dirs()
+        extra = ["-I", inc, f'-DNSK_NCCL_PATH="{lib}"']
+    cmd = [NVCC, *ARCH, *FLAGS, *lang, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -56,7 +70,7 @@ def build(force=False, verbose=False):
     for obj, err in results:
         if verbose and err.strip():
             print(err, file=sys.stderr)
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *[o for o, _ in results], "-lcublas"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *[o for o, _ in results], "-lcublas", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

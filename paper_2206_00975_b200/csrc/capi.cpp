@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
+#include <chrono>
+#include <future>
 
 #include "../../include/nullsketch_b200.h"
 #include "nsk_internal.hpp"
@@ -182,17 +184,49 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   }
   NSK_CUDA_OK(a_buf.alloc(elem * m * n, st));
   dA = a_buf.as<double>();
-  if (!op.tables(0, m)) return nsk::ECUDA;  // one table window for all chunks (CountSketch)
   const int64_t nchunks = (m + chunk - 1) / chunk;
   nsk::Scratch parts;
   const int64_t psz = op.s * n * nc_out;
   NSK_CUDA_OK(parts.alloc(sizeof(double) * psz * nchunks, st));
-  // each row chunk is sketched (row-shard apply into its own partial) as soon as it has landed
-  auto sketch_chunk = [&](int64_t r0, int64_t rows) {
+  // The operator's device tables (one window for all chunks; CountSketch's owner schedule takes
+  // ~0.2 s of host work at m = 2^24) are built on a helper thread while the copy engine moves A.
+  int devno = 0;
+  NSK_CUDA_OK(cudaGetDevice(&devno));
+  std::future<const nsk::DeviceTables*> tab = std::async(std::launch::async, [&op, m, devno]() {
+    cudaSetDevice(devno);
+    return op.tables(0, m);
+  });
+  bool have_tables = false;
+  std::vector<std::pair<int64_t, int64_t>> pending;  // chunks that landed before the tables existed
+  auto run_chunk = [&](int64_t r0, int64_t rows) {
     nsk::RowMap shard{r0, 1, rows};
     return dispatch_main(op, nc_in, shard, n, dA + r0 * nc_in, m, parts.as<double>() + (r0 / chunk) * psz, op.s, st);
   };
-  if (int rc = nsk::h2d_rows(A, m, n, lda, elem, dA, chunk, st, sketch_chunk)) return rc;
+  auto flush = [&]() {
+    have_tables = true;
+    if (!tab.get()) return static_cast<int>(nsk::ECUDA);
+    for (auto& c : pending)
+      if (int rc = run_chunk(c.first, c.second)) return rc;
+    pending.clear();
+    return static_cast<int>(nsk::OK);
+  };
+  // each row chunk is sketched (row-shard apply into its own partial) as soon as it has landed
+  auto sketch_chunk = [&](int64_t r0, int64_t rows) {
+    if (!have_tables) {
+      if (tab.wait_for(std::chrono::seconds(0)) != std::future_status::ready) {
+        pending.emplace_back(r0, rows);
+        return static_cast<int>(nsk::OK);
+      }
+      if (int rc = flush()) return rc;
+    }
+    return run_chunk(r0, rows);
+  };
+  int rc = nsk::h2d_rows(A, m, n, lda, elem, dA, chunk, st, sketch_chunk);
+  if (!have_tables) {
+    const int rf = flush();  // also joins the helper thread on the error path
+    if (rc == nsk::OK) rc = rf;
+  }
+  if (rc) return rc;
   NSK_CUDA_OK(cudaMemcpyAsync(SA, parts.as<double>(), sizeof(double) * psz, cudaMemcpyDeviceToDevice, st));
   for (int64_t c = 1; c < nchunks; ++c)
     if (int rc = nsk::accumulate(SA, op.s, nc_out, parts.as<double>() + c * psz, op.s, n, nc_out, st)) return rc;
@@ -207,6 +241,14 @@ int copy_out(void* host, int64_t ld, const double* dev, int64_t rows, int64_t co
 }
 
 }  // namespace
+
+namespace nsk {
+// dispatch_apply for the multi-GPU entry points (nccl_shard.cpp)
+int dispatch_apply_c(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                     double* SA, int64_t ldsa, cudaStream_t st) {
+  return dispatch_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+}
+}  // namespace nsk
 
 extern "C" {
 

@@ -110,7 +110,7 @@ int build_cs_table(PhiloxKey key, int64_t m, int64_t s, int64_t base, int64_t ro
   build_cs_table_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, m, s, base, rows, *out);
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
-  NSK_CUDA_OK(cudaDeviceSynchronize());
+  NSK_CUDA_OK(cudaStreamSynchronize(0));  // the table kernels ran on the legacy stream (copies on other streams continue)
   return OK;
 }
 

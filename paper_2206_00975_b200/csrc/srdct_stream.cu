@@ -403,7 +403,7 @@ int build_srdct_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out) {
   build_srdct_sgn_kernel<<<static_cast<unsigned>(blocks), 256>>>(sign_bits, m, P, words, *out);
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
-  NSK_CUDA_OK(cudaDeviceSynchronize());
+  NSK_CUDA_OK(cudaStreamSynchronize(0));  // the table kernels ran on the legacy stream (copies on other streams continue)
   return OK;
 }
 

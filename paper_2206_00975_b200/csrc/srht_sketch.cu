@@ -53,7 +53,7 @@ int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out) {
   build_sign_mask_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, nblocks, *out);
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
-  NSK_CUDA_OK(cudaDeviceSynchronize());
+  NSK_CUDA_OK(cudaStreamSynchronize(0));  // the table kernels ran on the legacy stream (copies on other streams continue)
   return OK;
 }
 

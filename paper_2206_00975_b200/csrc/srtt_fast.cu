@@ -58,7 +58,7 @@ int build_sign_bits(PhiloxKey key, int64_t m, uint32_t** out) {
   build_sign_bits_kernel<<<static_cast<unsigned>(blocks), 256>>>(key, m, *out);
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
-  NSK_CUDA_OK(cudaDeviceSynchronize());
+  NSK_CUDA_OK(cudaStreamSynchronize(0));  // the table kernels ran on the legacy stream (copies on other streams continue)
   return OK;
 }
 

@@ -7,12 +7,19 @@ s x n partials -- 2 MiB at BASELINE configs[1] -- produces SA on every rank.
 The SVD of the small SA then runs on the root rank (or every rank).
 
 Row maps:
-  gaussian, countsketch, srht   contiguous shards (srht: multiples of 1024
+  gaussian, countsketch, srht   contiguous shards (srht: multiples of 2048
                                 rows so the Hadamard split stays block-aligned;
-                                countsketch: multiples of 12288 rows, or 512 for short matrices)
+                                countsketch: multiples of 12288 rows, or 512 for short matrices;
+                                each rank builds CountSketch tables for its own rows only)
   srft, srdct                   cyclic shards: rank g holds rows g, g+P, ...
-                                (decimation in time keeps every local
-                                transform a plain strided DFT)
+                                (decimation in time: one local length-m/P
+                                transform, a twiddle and the sampled gather)
+
+Two reduce paths: sharded_apply / sharded_solve_k all-reduce with
+torch.distributed (any backend; the gloo tests use it), and NcclComm +
+sharded_apply_nccl / sharded_solve_k_nccl go through the library's C ABI
+(nsk_apply_allreduce / nsk_solve_k_sharded), which own the NCCL all-reduce
+themselves -- the path a C++ caller of the reference API uses.
 """
 from __future__ import annotations
 
@@ -99,4 +106,77 @@ def sharded_solve_k(S, A_local, k: int, shard: RowShard, group=None, root: int =
     if multi:
         dist.broadcast(W, src=root, group=group)
         dist.broadcast(sig, src=root, group=group)
+    return W, sig
+
+
+class NcclComm:
+    """An NCCL communicator owned by the library (nsk_nccl_comm_init); the unique id is
+    distributed over torch.distributed (any backend).  world/rank default to the process group's."""
+
+    def __init__(self, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+        L = _lib.load()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(L.nsk_nccl_unique_id(uid))
+        if self.world > 1:
+            box = [uid.raw]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        h = ctypes.c_void_p()
+        _lib.check(L.nsk_nccl_comm_init(self.world, uid, self.rank, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        from . import _lib
+        if self.handle is not None and self.handle.value:
+            _lib.check(_lib.load().nsk_nccl_comm_destroy(self.handle))
+        self.handle = None
+
+
+def sharded_apply_nccl(S, A_local, shard: RowShard, comm: NcclComm):
+    """SA on every rank through the C ABI: nsk_apply_allreduce (partial + ncclAllReduce)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .sketch import _colmajor, _empty_colmajor, _out_dtype_is_complex, _scalar_of, _stream_ptr
+    L = _lib.load()
+    scalar = _scalar_of(A_local)
+    A_local, lda = _colmajor(A_local)
+    mloc, n = A_local.shape
+    dt = torch.complex128 if _out_dtype_is_complex(S, scalar) else torch.float64
+    SA = _empty_colmajor(S.s, n, dt, A_local.device)
+    _lib.check(L.nsk_apply_allreduce(S.handle, scalar, shard.row0, shard.rstep, mloc, n,
+                                     ctypes.c_void_p(A_local.data_ptr()), lda, ctypes.c_void_p(SA.data_ptr()), S.s,
+                                     comm.handle, _stream_ptr()))
+    return SA
+
+
+def sharded_solve_k_nccl(S, A_local, k: int, shard: RowShard, comm: NcclComm):
+    """(W, sigma) on every rank through the C ABI: nsk_solve_k_sharded."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .sketch import _colmajor, _empty_colmajor, _out_dtype_is_complex, _scalar_of, _stream_ptr
+    L = _lib.load()
+    scalar = _scalar_of(A_local)
+    A_local, lda = _colmajor(A_local)
+    mloc, n = A_local.shape
+    dt = torch.complex128 if _out_dtype_is_complex(S, scalar) else torch.float64
+    W = _empty_colmajor(n, max(k, 0), dt, A_local.device)
+    sig = torch.empty(n, dtype=torch.float64, device=A_local.device)
+    _lib.check(L.nsk_solve_k_sharded(S.handle, scalar, shard.row0, shard.rstep, mloc, n,
+                                     ctypes.c_void_p(A_local.data_ptr()), lda, int(k), ctypes.c_void_p(W.data_ptr()),
+                                     max(n, 1), ctypes.c_void_p(sig.data_ptr()), comm.handle, _stream_ptr()))
     return W, sig

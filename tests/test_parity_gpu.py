@@ -642,3 +642,29 @@ def test_countsketch_shard_windows(nsk, oracle, splits):
             acc += part
         assert rel(acc, oracle.apply(op, A)) <= SA_TOL
         assert rel(host(nsk.apply(S, dev(A)).data), oracle.apply(op, A)) <= SA_TOL
+
+
+@pytest.mark.parametrize("kind,cyclic", [("srht", False), ("countsketch", False), ("gaussian", False),
+                                         ("srdct", True), ("srft", True)])
+def test_nccl_entry_points_single_rank(nsk, oracle, kind, cyclic):
+    """The multi-GPU C ABI (nsk_apply_allreduce / nsk_solve_k_sharded, nccl_shard.cpp) on a
+    one-rank NCCL communicator made by the library (nsk_nccl_unique_id / nsk_nccl_comm_init):
+    NCCL is dlopened, the partial is all-reduced in place, the SVD runs; results against the
+    oracle.  (One GPU per process: the world-size > 1 reduce is the same call.)"""
+    from paper_2206_00975_b200.distributed import NcclComm, RowShard, sharded_apply_nccl, sharded_solve_k_nccl
+    m = 1 << 16
+    n, s = 8, (4096 if kind == "countsketch" else 64)
+    A = oracle.random_real(m, n, 21)
+    S = nsk.SketchOperator.draw(kind, s, m, 61)
+    comm = NcclComm()
+    try:
+        shard = RowShard(0, 1, m)
+        SA = host(sharded_apply_nccl(S, dev(A), shard, comm))
+        ref = oracle.apply(oracle.draw(kind, s, m, 61), A)
+        assert rel(SA, ref) <= SA_TOL
+        W, sig = sharded_solve_k_nccl(S, dev(A), 2, shard, comm)
+        Wref, sref = oracle.from_sketch_svd(ref, 2)
+        assert np.max(np.abs(host(sig) - sref)) <= 1000 * U * sref[0]
+        assert _angle(host(W), Wref) <= 1e-8
+    finally:
+        comm.close()
