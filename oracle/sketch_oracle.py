@@ -248,6 +248,42 @@ def apply(op: OracleOperator, A, col_range=None):
     raise ValueError(op.kind)
 
 
+def srtt_shard_partial(op: OracleOperator, A_local, g, P):
+    """Partial sketch of cyclic shard g of P (global rows g, g+P, ...; P | m) by decimation in time
+    (SURVEY.md 8e): one length-N = m/P inverse DFT of the local rows, the shard twiddle, the gather.
+      srft : (1/sqrt s) w_m^{a g} W[a mod N],                    W = DFT_N(d x)
+      srdct: sqrt(m/s) Re(w_{4m}^{(2a+1) g} Z_a),                W = DFT_N(c d x w_{4N}^l),
+             Z_a = W[b/2] (b even) or conj(W[(-(b-1)/2 - 1) mod N]) (b odd), b = ((2a+1) mod 4N - 1)/2
+    (w_K = e^{+2 pi i/K}); summed over g it equals apply(op, A) (sketch.cpp:206-229)."""
+    m, s = op.m, op.s
+    if m % P:
+        raise ValueError("cyclic shards need P | m")
+    N = m // P
+    A_local = np.asarray(A_local)
+    if A_local.ndim == 1:
+        A_local = A_local[:, None]
+    rows = g + P * np.arange(N)
+    d = op.signs[rows][:, None]
+    a = op.idx.astype(np.int64)
+    if op.kind == "srft":
+        W = np.fft.ifft(d * A_local.astype(np.complex128), axis=0) * N
+        post = np.exp(2j * np.pi * ((a * g) % m) / m)
+        return post[:, None] * W[a % N] / math.sqrt(s)
+    if op.kind != "srdct":
+        raise ValueError("srtt_shard_partial: srft / srdct only")
+    cj = np.where(rows == 0, math.sqrt(1.0 / m), math.sqrt(2.0 / m))[:, None]
+    lw = np.exp(2j * np.pi * np.arange(N) / (4 * N))[:, None]
+    W = np.fft.ifft(d * cj * A_local * lw, axis=0) * N
+    q = (2 * a + 1) % (4 * N)
+    b = (q - 1) // 2
+    odd = b % 2 == 1
+    f = np.where(odd, (-(b - 1) // 2 - 1) % N, b // 2)
+    Z = W[f]
+    Z[odd] = np.conj(Z[odd])
+    post = np.exp(2j * np.pi * (((2 * a + 1) * g) % (4 * m)) / (4 * m))
+    return math.sqrt(m / s) * np.real(post[:, None] * Z)
+
+
 # ----------------------------------------------------------------------------- solve
 
 def svd(a):

@@ -95,3 +95,47 @@ def test_row_partition_covers_rows_once(kind, world):
             assert all(sh.row0 % 2048 == 0 and sh.mloc % 2048 == 0 for sh in shards)
         if kind == "countsketch" and m >= 512 * world:
             assert all(sh.row0 % 512 == 0 for sh in shards)
+
+
+def _dit_worker(rank, world, port, kind, s, m, n, seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import sketch_oracle as O
+        A = O.random_real(m, n, 3)
+        shard = row_partition(m, world, kind)[rank]
+        assert (shard.row0, shard.rstep) == (rank, world)  # cyclic map
+        op = O.draw(kind, s, m, seed)
+
+        def fn(S, A_local, row0, rstep):  # the decimation-in-time local transform, not a zero-filled apply
+            part = O.srtt_shard_partial(op, A_local.numpy(), row0, rstep)
+            return torch.from_numpy(np.ascontiguousarray(part))
+        A_loc = torch.from_numpy(np.ascontiguousarray(local_rows(A, shard)))
+        SA = sharded_apply(None, A_loc, shard, partial_fn=fn)
+        q.put((rank, SA.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,m,world", [("srft", 1000, 2), ("srdct", 1000, 2), ("srft", 4096, 4), ("srdct", 840, 4)])
+def test_cyclic_shards_decimation_in_time(kind, m, world):
+    """srft / srdct across ranks: each rank's partial is its local length-m/P transform, twiddled
+    and gathered (oracle.srtt_shard_partial, the algorithm srtt_general.cu / srtt_fast.cu run on the
+    GPU); the gloo all-reduce of the partials equals the single-process apply."""
+    from oracle import sketch_oracle as O
+    O.build()
+    s, n, seed = 40, 5, 23
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dit_worker, args=(r, world, port, kind, s, m, n, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = O.apply(O.draw(kind, s, m, seed), O.random_real(m, n, 3))
+    for rank, SA in out:
+        assert np.linalg.norm(SA - ref) <= 1e-12 * np.linalg.norm(ref)
