@@ -98,6 +98,27 @@ int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64
   return nsk::accumulate(SA, ldsa, nc_out, t.as<double>(), op.s, n, ncomp, st);
 }
 
+// S [A | B] into adjacent column blocks of SA (B: kb columns).  Gaussian: one pass, every G tile
+// generated once for all n + kb columns (gaussian_apply_key2); the per-column kinds regenerate
+// nothing across columns, so they run the two blocks one after the other.
+int dispatch_main2(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
+                   int64_t kb, const double* B, int64_t ldb, double* SA, int64_t ldsa, cudaStream_t st) {
+  if (kb > 0 && op.kind == nsk::GAUSSIAN)
+    return nsk::gaussian_apply_key2(op.key0, op.s, op.zero_mask(), 0, ncomp, rows, n, A, lda, kb, B, ldb, SA, ldsa,
+                                    st);
+  if (int rc = dispatch_main(op, ncomp, rows, n, A, lda, SA, ldsa, st)) return rc;
+  if (kb == 0) return nsk::OK;
+  return dispatch_main(op, ncomp, rows, kb, B, ldb, SA + ldsa * n * out_ncomp(op, ncomp), ldsa, st);
+}
+
+int dispatch_apply2(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
+                    int64_t kb, const double* B, int64_t ldb, double* SA, int64_t ldsa, cudaStream_t st) {
+  if (op.appended == 0) return dispatch_main2(op, ncomp, rows, n, A, lda, kb, B, ldb, SA, ldsa, st);
+  if (int rc = dispatch_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st)) return rc;
+  if (kb == 0) return nsk::OK;
+  return dispatch_apply(op, ncomp, rows, kb, B, ldb, SA + ldsa * n * out_ncomp(op, ncomp), ldsa, st);
+}
+
 // Minimal JSON field readers for the descriptor (flat object, known keys).
 bool json_find(const std::string& js, const std::string& key, size_t& pos) {
   const std::string pat = "\"" + key + "\"";
@@ -167,9 +188,16 @@ int copy_in(const void* host, int64_t rows, int64_t cols, int64_t ld, int ncomp,
 // are summed in chunk order (deterministic).  Everything else: copy, then
 // apply.  a_buf receives the device copy of A.
 int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void* A, int64_t lda, nsk::Scratch& a_buf,
-                double* SA, cudaStream_t st) {
+                double* SA, cudaStream_t st, int64_t kb = 0, const void* B = nullptr, int64_t ldb = 0,
+                nsk::Scratch* b_buf = nullptr) {
   const int nc_out = out_ncomp(op, nc_in);
   const size_t elem = sizeof(double) * nc_in;
+  // [A | B] (sketched TLS): B (a few columns) is copied whole first, then A streams in chunks and
+  // every chunk is sketched together with the same rows of B (dispatch_main2)
+  double* dB = nullptr;
+  if (kb > 0)
+    if (int rc = copy_in(B, m, kb, ldb, nc_in, &dB, *b_buf, st)) return rc;
+  const int64_t ntot = n + kb;
   const int64_t align = op.kind == nsk::GAUSSIAN ? 16 : op.kind == nsk::SRHT ? 2048 : op.kind == nsk::COUNTSKETCH ? 12288 : 0;
   constexpr int64_t CHUNKS = 8;
   const int64_t chunk = align ? ((m + CHUNKS - 1) / CHUNKS + align - 1) / align * align : 0;
@@ -180,13 +208,13 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   if (!pipelined) {
     if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a_buf, st)) return rc;
     nsk::RowMap rows{0, 1, m};
-    return dispatch_apply(op, nc_in, rows, n, dA, m, SA, op.s, st);
+    return dispatch_apply2(op, nc_in, rows, n, dA, m, kb, dB, m, SA, op.s, st);
   }
   NSK_CUDA_OK(a_buf.alloc(elem * m * n, st));
   dA = a_buf.as<double>();
   const int64_t nchunks = (m + chunk - 1) / chunk;
   nsk::Scratch parts;
-  const int64_t psz = op.s * n * nc_out;
+  const int64_t psz = op.s * ntot * nc_out;
   NSK_CUDA_OK(parts.alloc(sizeof(double) * psz * nchunks, st));
   // The operator's device tables (one window for all chunks; CountSketch's owner schedule takes
   // ~0.2 s of host work at m = 2^24) are built on a helper thread while the copy engine moves A.
@@ -200,7 +228,8 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   std::vector<std::pair<int64_t, int64_t>> pending;  // chunks that landed before the tables existed
   auto run_chunk = [&](int64_t r0, int64_t rows) {
     nsk::RowMap shard{r0, 1, rows};
-    return dispatch_main(op, nc_in, shard, n, dA + r0 * nc_in, m, parts.as<double>() + (r0 / chunk) * psz, op.s, st);
+    return dispatch_main2(op, nc_in, shard, n, dA + r0 * nc_in, m, kb, dB ? dB + r0 * nc_in : nullptr, m,
+                          parts.as<double>() + (r0 / chunk) * psz, op.s, st);
   };
   auto flush = [&]() {
     have_tables = true;
@@ -229,7 +258,7 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   if (rc) return rc;
   NSK_CUDA_OK(cudaMemcpyAsync(SA, parts.as<double>(), sizeof(double) * psz, cudaMemcpyDeviceToDevice, st));
   for (int64_t c = 1; c < nchunks; ++c)
-    if (int rc = nsk::accumulate(SA, op.s, nc_out, parts.as<double>() + c * psz, op.s, n, nc_out, st)) return rc;
+    if (int rc = nsk::accumulate(SA, op.s, nc_out, parts.as<double>() + c * psz, op.s, ntot, nc_out, st)) return rc;
   return nsk::OK;
 }
 
@@ -688,8 +717,11 @@ static int tls_finish(int nc, int64_t rows, const double* M, int64_t ldm, int64_
   NSK_CUDA_OK(siga.alloc(sizeof(double) * n, st));
   NSK_CUDA_OK(v2s.alloc(sizeof(double) * k, st));
   NSK_CUDA_OK(v2w.alloc(sizeof(double) * k * k * nc, st));
-  if (int rc = nsk::jacobi_trailing(nc, rows, nk, M, ldm, k, static_cast<double*>(Vk), ldv, sigma, st)) return rc;
-  if (int rc = nsk::jacobi_trailing(nc, rows, n, M, ldm, 0, nullptr, 1, siga.as<double>(), st)) return rc;
+  // The two SVDs of tls.cpp:110-111 share one QR (R of the leading n columns is the leading block of
+  // R) and their Jacobi stages run concurrently (jacobi_trailing_pair).
+  if (int rc = nsk::jacobi_trailing_pair(nc, rows, nk, M, ldm, k, static_cast<double*>(Vk), ldv, sigma, n,
+                                         siga.as<double>(), st))
+    return rc;
   std::vector<double> s_aug(static_cast<size_t>(nk)), s_a(static_cast<size_t>(n));
   NSK_CUDA_OK(cudaMemcpyAsync(s_aug.data(), sigma, sizeof(double) * nk, cudaMemcpyDeviceToHost, st));
   NSK_CUDA_OK(cudaMemcpyAsync(s_a.data(), siga.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -739,11 +771,9 @@ int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t
   nsk::Scratch sa;
   NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * nk * nc, st));
   nsk::RowMap rows{0, 1, m};
-  // S [A | B] without forming [A | B] (tls.cpp:108-109): two applies into adjacent columns.
-  if (int rc = dispatch_apply(op, nc_in, rows, n, static_cast<const double*>(A), lda, sa.as<double>(), op.s, st))
-    return rc;
-  if (int rc = dispatch_apply(op, nc_in, rows, k, static_cast<const double*>(B), ldb, sa.as<double>() + op.s * n * nc,
-                              op.s, st))
+  // S [A | B] without forming [A | B] (tls.cpp:108-109): one pass over both blocks.
+  if (int rc = dispatch_apply2(op, nc_in, rows, n, static_cast<const double*>(A), lda, k,
+                               static_cast<const double*>(B), ldb, sa.as<double>(), op.s, st))
     return rc;
   return tls_finish(nc, op.s, sa.as<double>(), op.s, n, k, cond_limit, allow_marginal, X, ldx, Vk, ldv, sigma, info,
                     st);
@@ -817,8 +847,7 @@ int nsk_tls_solve_sketched_host(const nsk_operator* h, int scalar, int64_t m, in
   nsk::Scratch a, b, sa, x, v, sg;
   // S [A | B] straight from host memory: A's H2D overlaps its sketch (host_sketch)
   NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * (n + k) * nc, st));
-  if (int rc = host_sketch(op, nc_in, m, n, A, lda, a, sa.as<double>(), st)) return rc;
-  if (int rc = host_sketch(op, nc_in, m, k, B, ldb, b, sa.as<double>() + op.s * n * nc, st)) return rc;
+  if (int rc = host_sketch(op, nc_in, m, n, A, lda, a, sa.as<double>(), st, k, B, ldb, &b)) return rc;
   NSK_CUDA_OK(x.alloc(sizeof(double) * n * k * nc, st));
   NSK_CUDA_OK(v.alloc(sizeof(double) * (n + k) * k * nc, st));
   NSK_CUDA_OK(sg.alloc(sizeof(double) * (n + k), st));

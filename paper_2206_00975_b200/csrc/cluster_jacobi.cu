@@ -31,6 +31,9 @@
 #include <cstdlib>
 
 #include "jacobi_pair.cuh"
+#include <map>
+#include <mutex>
+#include <tuple>
 #include "nsk_internal.hpp"
 
 namespace cg = cooperative_groups;
@@ -683,6 +686,48 @@ __global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  //
 
 }  // namespace
 
+// Function attributes once per (kernel, device) at the largest shared memory seen: re-setting them
+// while another launch of the same kernel runs (the concurrent stages of jacobi_trailing_pair) is
+// avoided.
+template <class K>
+int set_attrs_once(K kern, size_t smem, bool nonportable) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[std::make_pair(reinterpret_cast<const void*>(kern), dev)];
+  if (have >= smem && have > 0) return OK;
+  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (nonportable) NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  have = smem;
+  return OK;
+}
+
+// cudaOccupancyMaxActiveClusters once per (kernel, device, shared memory, cluster size): the query
+// is not needed per call, and the concurrent SVD stages (jacobi_trailing_pair) must not wait on it.
+template <class K>
+int max_clusters_cached(K kern, const cudaLaunchConfig_t& cfg) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, unsigned>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), dev, cfg.dynamicSmemBytes, cfg.gridDim.x);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    ncl = 0;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = ncl;
+  return ncl;
+}
+
 // Returns OK after running, or NOTAPPLICABLE when [R; I] does not fit one
 // cluster (the caller then uses the global-memory block kernel).
 int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cudaStream_t st) {
@@ -702,8 +747,7 @@ int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cu
                                                                               : cluster_jacobi_kernel<1, 16>)
                          : (rpl == 4 ? cluster_jacobi_kernel<2, 4> : rpl == 8 ? cluster_jacobi_kernel<2, 8>
                                                                               : cluster_jacobi_kernel<2, 16>);
-  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  if (C > 8) NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (int rc = set_attrs_once(kern, smem, C > 8)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(C));
   cfg.blockDim = dim3(static_cast<unsigned>(threads));
@@ -716,11 +760,8 @@ int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cu
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
-    cudaGetLastError();
-    return NOTAPPLICABLE;
-  }
+  const int ncl = max_clusters_cached(kern, cfg);
+  if (ncl < 1) return NOTAPPLICABLE;
   NSK_CUDA_OK(cudaLaunchKernelEx(&cfg, kern, prm));
   count_launch();
   return OK;
@@ -759,8 +800,7 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
                   : (rpl == 4 ? cluster_svd_kernel<2, 4, 4>
                               : rpl == 8 ? cluster_svd_kernel<2, 8, 4>
                                          : (nbuf == 4 ? cluster_svd_kernel<2, 16, 4> : cluster_svd_kernel<2, 16, 3>));
-  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  if (C > 8) NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  if (int rc = set_attrs_once(kern, smem, C > 8)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(C));
   cfg.blockDim = dim3(static_cast<unsigned>(threads));
@@ -773,11 +813,8 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  int ncl = 0;
-  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
-    cudaGetLastError();
-    return NOTAPPLICABLE;
-  }
+  const int ncl = max_clusters_cached(kern, cfg);
+  if (ncl < 1) return NOTAPPLICABLE;
   NSK_CUDA_OK(cudaLaunchKernelEx(&cfg, kern, prm));
   count_launch();
   if (dbg) {
@@ -785,10 +822,10 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
     NSK_CUDA_OK(cudaMemcpyAsync(h, stamps, sizeof(h), cudaMemcpyDeviceToHost, st));
     NSK_CUDA_OK(cudaStreamSynchronize(st));
     std::fprintf(stderr,
-                 "nsk svd_rt: n=%lld C=%d b=%d qrcp %.3f ms transpose %.3f ms sweeps %.3f ms (cycles inner %llu move "
-                 "%llu)\n",
-                 static_cast<long long>(n), C, b, (h[1] - h[0]) * 1e-6, (h[2] - h[1]) * 1e-6, (h[3] - h[2]) * 1e-6,
-                 h[4], h[5]);
+                 "nsk svd_rt: n=%lld C=%d b=%d max clusters %d qrcp %.3f ms transpose %.3f ms sweeps %.3f ms "
+                 "(cycles inner %llu move %llu; globaltimer %llu .. %llu us)\n",
+                 static_cast<long long>(n), C, b, ncl, (h[1] - h[0]) * 1e-6, (h[2] - h[1]) * 1e-6,
+                 (h[3] - h[2]) * 1e-6, h[4], h[5], h[0] / 1000 % 100000000ull, h[3] / 1000 % 100000000ull);
     NSK_CUDA_OK(cudaFreeAsync(stamps, st));
   }
   return OK;

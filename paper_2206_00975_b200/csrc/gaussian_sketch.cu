@@ -81,6 +81,9 @@ __device__ __forceinline__ void named_arrive(int id, int count) {
 struct GaussParams {
   const double* A;
   int64_t lda;      // in scalars (complex elements for ncomp = 2)
+  const double* B;  // [A | B] in one pass (sketched TLS, tls.cpp:108-109): logical columns q >= nqa
+  int64_t ldb;      //   come from B (column (q - nqa) / ncomp); B = A, nqa = nq without a second block
+  int64_t nqa;
   int64_t mloc;     // local rows
   int64_t row0;     // global row of local row 0
   int64_t s;
@@ -91,6 +94,14 @@ struct GaussParams {
   const uint32_t* zmask;  // zeroed rows (bit zoff + global row), or nullptr
   int64_t zoff;
 };
+
+// Address of [A | B](row, logical column q).
+template <int NCOMP>
+__device__ __forceinline__ const double* a_elem(const GaussParams& p, int64_t row, int64_t q) {
+  if (q < p.nqa) return NCOMP == 1 ? p.A + row + q * p.lda : p.A + 2 * (row + (q >> 1) * p.lda) + (q & 1);
+  const int64_t qb = q - p.nqa;
+  return NCOMP == 1 ? p.B + row + qb * p.ldb : p.B + 2 * (row + (qb >> 1) * p.ldb) + (qb & 1);
+}
 
 // Producer: A rows [k0, k0 + BK) x logical columns [q0, q0 + BN) -> sb[col][row].
 template <int BN, int NCOMP, bool VEC16>
@@ -106,7 +117,7 @@ __device__ __forceinline__ void load_a_tile(const GaussParams& p, double* sb, in
       const double* src = p.A;
       if (q < p.nq && row < p.mloc) {
         bytes = (row + 1 < p.mloc) ? 16 : 8;
-        src = p.A + row + q * p.lda;
+        src = a_elem<1>(p, row, q);
       }
       cp_async16(sb + k4(col, r2, BN), src, bytes);
     }
@@ -120,7 +131,7 @@ __device__ __forceinline__ void load_a_tile(const GaussParams& p, double* sb, in
       const double* src = p.A;
       if (q < p.nq && row < p.mloc) {
         bytes = 8;
-        src = NCOMP == 1 ? p.A + row + q * p.lda : p.A + 2 * (row + (q >> 1) * p.lda) + (q & 1);
+        src = a_elem<NCOMP>(p, row, q);
       }
       cp_async8(sb + k4(col, r, BN), src, bytes);
     }
@@ -184,17 +195,21 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     // every chunk up to the row offset k0, so their source offsets and k4
     // destinations are computed once (the producers' register budget is the
     // consumers'): a full chunk then costs ~3 instructions per 16-byte copy.
+    // Slot i of this thread is column colx0 + i * CSTEP at row offset r2 (PRODUCERS is a multiple of
+    // BK / 2), so its k4 destination is soff0 + i * 4 * CSTEP; only the source addresses are kept
+    // (the column may sit in A or in B).
     constexpr int PER = (BN * (T::BK / 2)) / PRODUCERS;
-    int64_t aoff[PER];
-    uint32_t soff[PER];
+    constexpr int CSTEP = PRODUCERS / (T::BK / 2);
+    static_assert(PRODUCERS % (T::BK / 2) == 0, "slot columns form a progression");
+    const double* abase[PER];  // row-0 address of the slot's column ([A | B]), + r2
     uint32_t okmask = 0;
+    const uint32_t soff0 = static_cast<uint32_t>(k4(pt / (T::BK / 2), (pt % (T::BK / 2)) * 2, BN));
     if (NCOMP == 1 && VEC16) {
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int cc = pt + PRODUCERS * i, colx = cc / (T::BK / 2), r2 = (cc % (T::BK / 2)) * 2;
         const int64_t q = q0 + colx;
-        aoff[i] = q < p.nq ? r2 + q * p.lda : 0;
-        soff[i] = static_cast<uint32_t>(k4(colx, r2, BN));
+        abase[i] = q < p.nq ? a_elem<1>(p, r2, q) : p.A;
         okmask |= (q < p.nq ? 1u : 0u) << i;
       }
     }
@@ -206,11 +221,10 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         double* sb = sa + T::BM * T::BK;
         const int64_t k0 = kbeg + c * T::BK;
         if (NCOMP == 1 && VEC16 && k0 + T::BK <= p.mloc) {
-          const double* a0 = p.A + k0;
 #pragma unroll
           for (int i = 0; i < PER; ++i) {
             const bool ok = (okmask >> i) & 1u;
-            cp_async16(sb + soff[i], ok ? a0 + aoff[i] : p.A, ok ? 16 : 0);
+            cp_async16(sb + soff0 + i * 4 * CSTEP, ok ? abase[i] + k0 : p.A, ok ? 16 : 0);
           }
         } else {
           load_a_tile<BN, NCOMP, VEC16>(p, sb, k0, q0, pt);
@@ -327,9 +341,19 @@ int gaussian_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n,
 }
 
 int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t zoff, int ncomp, const RowMap& rows,
-                       int64_t n, const double* A, int64_t lda,
-                   double* SA, int64_t ldsa, cudaStream_t st) {
+                       int64_t n, const double* A, int64_t lda, double* SA, int64_t ldsa, cudaStream_t st) {
+  return gaussian_apply_key2(key, s, zmask, zoff, ncomp, rows, n, A, lda, 0, nullptr, 0, SA, ldsa, st);
+}
+
+// S [A | B] in one pass: every G tile is generated once for the n + k columns (the reference forms the
+// m x (n+k) copy hcat(A, B) first, tls.cpp:108); SA columns n .. n+k-1 hold S B.
+int gaussian_apply_key2(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t zoff, int ncomp, const RowMap& rows,
+                        int64_t n, const double* A, int64_t lda, int64_t kb, const double* B, int64_t ldb,
+                        double* SA, int64_t ldsa, cudaStream_t st) {
   if (rows.rstep != 1) return fail(EINVAL_, "gaussian shard: rows must be contiguous (rstep 1)");
+  if (kb == 0) B = nullptr;
+  const int64_t nqa = n * ncomp;
+  n += kb;
   const int64_t nq = n * ncomp, mloc = rows.mloc;
   const double scale = 1.0 / std::sqrt(static_cast<double>(s));
   if (nq == 0) return OK;
@@ -365,8 +389,10 @@ int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t 
 
   Scratch part;
   NSK_CUDA_OK(part.alloc(sizeof(double) * splits * nq * s, st));
-  GaussParams p{A, lda, mloc, rows.row0, s, nq, part.as<double>(), per, key, zmask, zoff};
-  const bool vec16 = ncomp == 1 && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  GaussParams p{A, lda, B ? B : A, B ? ldb : lda, B ? nqa : nq, mloc, rows.row0, s, nq, part.as<double>(), per, key,
+                zmask, zoff};
+  const bool vec16 = ncomp == 1 && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                     (!B || ((ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0)));
   int rc = ncomp == 2 ? launch_bn<2, false>(BN, p, q_tiles, s_tiles, splits, st)
          : vec16     ? launch_bn<1, true>(BN, p, q_tiles, s_tiles, splits, st)
                      : launch_bn<1, false>(BN, p, q_tiles, s_tiles, splits, st);

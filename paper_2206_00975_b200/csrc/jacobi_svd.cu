@@ -26,6 +26,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <future>
+#include <string>
+
 #include "nsk_internal.hpp"
 
 namespace cg = cooperative_groups;
@@ -581,35 +584,40 @@ int coop_launch(K kern, int64_t want, size_t smem, void** args, cudaStream_t st,
   return OK;
 }
 
+// Per-SVD device buffers of the Jacobi stage (X = [R; I] or [R'; V] workspace and its counters).
+struct SvdBufs {
+  double* X;
+  double* norms;
+  int* counter;  // [MAX_SWEEPS + 1]
+  int* bad;
+  int* version;  // [n]: Jacobi column versions / degenerate flag; zero on entry
+};
+
+size_t svd_bufs_bytes(int64_t n, int nc) {
+  return sizeof(double) * (2 * n * n * nc + n) + sizeof(int) * (MAX_SWEEPS + 2 + n) + 64;
+}
+
+SvdBufs svd_bufs_at(void* base, int64_t n, int nc) {
+  SvdBufs b;
+  b.X = static_cast<double*>(base);
+  b.norms = b.X + 2 * n * n * nc;
+  b.counter = reinterpret_cast<int*>(b.norms + n);
+  b.bad = b.counter + MAX_SWEEPS + 1;
+  b.version = b.bad + 1;
+  return b;
+}
+
+// Trailing k right singular vectors and all n singular values of the leading s x n block of the
+// QR'd matrix (R in the upper triangle of A, ld s, diagonal in rdiag): the Jacobi stage.
 template <int NC>
-int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W, int64_t ldw, double* sigma,
-        cudaStream_t st) {
-  Scratch ws;
-  const size_t apad = (s * n * NC + 1) & ~static_cast<int64_t>(1);  // X 16-byte aligned (double2 staging)
-  const size_t abytes = sizeof(double) * apad, xbytes = sizeof(double) * 2 * n * n * NC;
-  const size_t extra = sizeof(double) * (n + n * NC + n) + sizeof(int) * (MAX_SWEEPS + 2 + 2 * n) + 64;
-  NSK_CUDA_OK(ws.alloc(abytes + xbytes + extra, st));
-  double* A = ws.as<double>();
-  double* X = A + apad;
-  double* tau = X + 2 * n * n * NC;
-  double* rdiag = tau + n;
-  double* norms = rdiag + n * NC;
-  int* counter = reinterpret_cast<int*>(norms + n);
-  int* bad = counter + MAX_SWEEPS + 1;
-  int* ready = bad + 1;       // QR reflector flags
-  int* version = ready + n;   // Jacobi column versions
-  NSK_CUDA_OK(cudaMemsetAsync(ready, 0, sizeof(int) * 2 * n, st));
+int svd_stage(const double* A, const double* rdiag, int64_t s, int64_t n, int64_t k, double* W, int64_t ldw,
+              double* sigma, SvdBufs B, cudaStream_t st) {
+  double* X = B.X;
+  double* norms = B.norms;
+  int* counter = B.counter;
+  int* bad = B.bad;
+  int* version = B.version;
   {
-    int64_t blocks = (s * n * NC + 255) / 256;
-    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-    copy_in_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(SA, ldsa, s, n, NC, A, counter);
-    count_launch();
-    NSK_CUDA_OK(cudaGetLastError());
-  }
-  {  // 1. Householder QR
-    QrParams Q{A, tau, rdiag, s, n};
-    void* args[] = {&Q, &ready};
-    if (int rc = coop_launch(qr_kernel<NC>, n, 0, args, st)) return rc;
     int64_t blocks = (2 * n * n * NC + 255) / 256;
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
     build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, X);
@@ -682,6 +690,7 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   if (int rc = solve(true, host)) return rc;
   if (host[2] < 0) {  // exactly singular R: What undefined, rerun on [R; I]
     NSK_CUDA_OK(cudaMemsetAsync(version, 0, sizeof(int) * n, st));
+    NSK_CUDA_OK(cudaMemsetAsync(counter, 0, sizeof(int) * (MAX_SWEEPS + 1), st));
     int64_t blocks = (2 * n * n * NC + 255) / 256;
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
     build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, X);
@@ -697,12 +706,83 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   return OK;
 }
 
+// Householder QR of the s x n copy of SA (R above the diagonal of A, diagonal in rdiag), then the
+// Jacobi stage on R; with n2 > 0 also the singular values of the leading n2 columns (the
+// existence check of sketched TLS, tls.cpp:110-111): their R is the leading block of the same
+// factor, so that second Jacobi stage needs no QR of its own and runs concurrently on a helper
+// thread and stream (each stage fills one 16-CTA cluster).
+template <int NC>
+int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W, int64_t ldw, double* sigma,
+        int64_t n2, double* sigma2, cudaStream_t st) {
+  Scratch ws;
+  const size_t apad = (s * n * NC + 1) & ~static_cast<int64_t>(1);  // X 16-byte aligned (double2 staging)
+  const size_t abytes = sizeof(double) * apad;
+  const size_t qbytes = (sizeof(double) * (n + n * NC) + sizeof(int) * n + 15) / 16 * 16;
+  const size_t b1 = (svd_bufs_bytes(n, NC) + 15) / 16 * 16, b2 = n2 > 0 ? svd_bufs_bytes(n2, NC) : 0;
+  NSK_CUDA_OK(ws.alloc(abytes + qbytes + b1 + b2, st));
+  char* base = ws.as<char>();
+  double* A = reinterpret_cast<double*>(base);
+  double* tau = reinterpret_cast<double*>(base + abytes);
+  double* rdiag = tau + n;
+  int* ready = reinterpret_cast<int*>(rdiag + n * NC);  // QR reflector flags
+  const SvdBufs B1 = svd_bufs_at(base + abytes + qbytes, n, NC);
+  const SvdBufs B2 = n2 > 0 ? svd_bufs_at(base + abytes + qbytes + b1, n2, NC) : SvdBufs{};
+  NSK_CUDA_OK(cudaMemsetAsync(ready, 0, sizeof(int) * n, st));
+  NSK_CUDA_OK(cudaMemsetAsync(B1.version, 0, sizeof(int) * n, st));
+  if (n2 > 0) {
+    NSK_CUDA_OK(cudaMemsetAsync(B2.version, 0, sizeof(int) * n2, st));
+    NSK_CUDA_OK(cudaMemsetAsync(B2.counter, 0, sizeof(int) * (MAX_SWEEPS + 1), st));
+  }
+  {
+    int64_t blocks = (s * n * NC + 255) / 256;
+    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+    copy_in_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(SA, ldsa, s, n, NC, A, B1.counter);
+    count_launch();
+    NSK_CUDA_OK(cudaGetLastError());
+  }
+  {  // 1. Householder QR
+    QrParams Q{A, tau, rdiag, s, n};
+    void* args[] = {&Q, &ready};
+    if (int rc = coop_launch(qr_kernel<NC>, n, 0, args, st)) return rc;
+  }
+  if (n2 <= 0) return svd_stage<NC>(A, rdiag, s, n, k, W, ldw, sigma, B1, st);
+  int devno = 0;
+  NSK_CUDA_OK(cudaGetDevice(&devno));
+  cudaEvent_t qr_done;
+  NSK_CUDA_OK(cudaEventCreateWithFlags(&qr_done, cudaEventDisableTiming));
+  NSK_CUDA_OK(cudaEventRecord(qr_done, st));
+  std::string side_err;  // the helper's error text (last_error is per thread)
+  std::future<int> side = std::async(std::launch::async, [&]() -> int {
+    cudaSetDevice(devno);
+    cudaStream_t aux = copy_stream();  // the helper thread's own non-blocking stream
+    int rc = OK;
+    if (cudaError_t e = cudaStreamWaitEvent(aux, qr_done, 0)) rc = cuda_fail(e, "svd: stream fork");
+    if (rc == OK) rc = svd_stage<NC>(A, rdiag, s, n2, 0, nullptr, 1, sigma2, B2, aux);
+    if (rc != OK) side_err = last_error();
+    return rc;
+  });
+  const int rc1 = svd_stage<NC>(A, rdiag, s, n, k, W, ldw, sigma, B1, st);
+  const int rc2 = side.get();
+  cudaEventDestroy(qr_done);
+  if (rc1 != OK) return rc1;
+  if (rc2 != OK) return fail(rc2, side_err);
+  return OK;
+}
+
 }  // namespace
 
 int jacobi_trailing(int ncomp, int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W,
                     int64_t ldw, double* sigma, cudaStream_t st) {
   if (s < 1 || n < 1) return fail(EINVAL_, "svd: matrix is empty");
-  return ncomp == 1 ? run<1>(s, n, SA, ldsa, k, W, ldw, sigma, st) : run<2>(s, n, SA, ldsa, k, W, ldw, sigma, st);
+  return ncomp == 1 ? run<1>(s, n, SA, ldsa, k, W, ldw, sigma, 0, nullptr, st)
+                    : run<2>(s, n, SA, ldsa, k, W, ldw, sigma, 0, nullptr, st);
+}
+
+int jacobi_trailing_pair(int ncomp, int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W,
+                         int64_t ldw, double* sigma, int64_t n2, double* sigma2, cudaStream_t st) {
+  if (s < 1 || n < 1 || n2 < 1 || n2 > n) return fail(EINVAL_, "svd: bad shapes");
+  return ncomp == 1 ? run<1>(s, n, SA, ldsa, k, W, ldw, sigma, n2, sigma2, st)
+                    : run<2>(s, n, SA, ldsa, k, W, ldw, sigma, n2, sigma2, st);
 }
 
 }  // namespace nsk

@@ -20,6 +20,7 @@ enum Status { OK = 0, EINVAL_ = 1, ERANGE_ = 2, ENOCONV = 3, ECUDA = 4, ENOMEM_ 
 constexpr int NOTAPPLICABLE = -100;  // internal: a specialised path declines, the caller falls back
 
 int fail(int code, const std::string& msg);
+const char* last_error();  // this thread's message of the last failure
 int cuda_fail(cudaError_t e, const char* what);
 const char* kind_name(int kind);
 
@@ -114,6 +115,11 @@ int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t 
                        const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
                        int64_t ldsa, cudaStream_t st);
 
+// The same for [A | B] (B: kb columns, ldb) in one pass, SA columns n .. n+kb-1 = S B.
+int gaussian_apply_key2(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t zoff, int ncomp,
+                        const RowMap& rows, int64_t n, const double* A, int64_t lda, int64_t kb, const double* B,
+                        int64_t ldb, double* SA, int64_t ldsa, cudaStream_t st);
+
 int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out);
 
 // Sampled Fisher-Yates with an O(s) map (bit-identical to rng.hpp:108-121).
@@ -154,6 +160,10 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
 // (device, non-increasing).  Returns ENOCONV if the sweep limit is hit.
 int jacobi_trailing(int ncomp, int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k,
                     double* W, int64_t ldw, double* sigma, cudaStream_t st);
+// The same plus all n2 singular values of the leading s x n2 block (one shared QR; the two Jacobi
+// stages run concurrently).
+int jacobi_trailing_pair(int ncomp, int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W,
+                         int64_t ldw, double* sigma, int64_t n2, double* sigma2, cudaStream_t st);
 
 // R factor (N x N upper, ld N, N = n + k) of the thin QR of [A | B] (m x N),
 // shifted CholeskyQR3 (tall_qr.cu).  B may be null when k = 0.
