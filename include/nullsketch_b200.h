@@ -106,8 +106,9 @@ int nsk_op_sample_indices(const nsk_operator* op, int64_t* idx_host);
  * the terminating NUL; *len receives the length without NUL. */
 int nsk_op_descriptor(const nsk_operator* op, char* buf, size_t cap, size_t* len);
 
-/* SketchOperator::from_descriptor (sketch.cpp:315-337).  Only appended = 0
- * and no zeroed rows are accepted by this build. */
+/* SketchOperator::from_descriptor (sketch.cpp:315-337): replays the draw, then
+ * the appended Gaussian columns (stream (seed, 1)) and the zeroed rows, so the
+ * operator applies exactly as the one that wrote the descriptor. */
 int nsk_op_from_descriptor(const char* json, nsk_operator** out);
 
 /* ---- apply (sketch.hpp:89) ---------------------------------------------- */
@@ -121,7 +122,10 @@ int nsk_apply(const nsk_operator* op, int scalar, int64_t m, int64_t n, const vo
  * j = 0..mloc-1 of A, which are global rows row0 + rstep*j.  Writes the
  * partial SA_g = S[:, rows] A_g; the sum of the partials over a partition of
  * the rows is apply(S, A).  gaussian/countsketch/srht need rstep == 1
- * (contiguous shards); srft/srdct accept any rstep (cyclic shards). */
+ * (contiguous shards; countsketch: row0 a multiple of 512, and each shard
+ * builds its tables for its own rows only); srft/srdct take cyclic shards
+ * (row0 = g < rstep = P, P | m: the local length-m/P transform, decimation in
+ * time) and, less efficiently, any other row map. */
 int nsk_apply_shard(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep,
                     int64_t mloc, int64_t n, const void* A, int64_t lda, void* SA,
                     int64_t ldsa, void* stream);
@@ -253,6 +257,14 @@ int nsk_apply_allreduce(const nsk_operator* op, int scalar, int64_t row0, int64_
 int nsk_solve_k_sharded(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep, int64_t mloc, int64_t n,
                         const void* A_local, int64_t lda, int64_t k, void* W, int64_t ldw, double* sigma,
                         void* nccl_comm, void* stream);
+
+/* ---- memory --------------------------------------------------------------
+ * Scratch (device copies of host inputs, partial sketches, SVD workspaces)
+ * comes from a library-private stream-ordered pool per device, so it never
+ * holds on to the default pool other libraries (PyTorch) allocate from.  Freed
+ * blocks stay mapped for the next call; this returns them to the device
+ * (synchronises the current device first). */
+int nsk_release_scratch(void);
 
 /* ---- instrumentation (bench.py; no effect on results) ------------------- */
 

@@ -28,7 +28,7 @@ EXPORTS = (
     "nsk_timing_enable", "nsk_timing_collect", "nsk_timing_kernel", "nsk_op_state", "nsk_update_row", "nsk_downdate_row",
     "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_tls_solve_exact", "nsk_tls_solve_exact_host", "nsk_update_row_host",
     "nsk_downdate_row_host", "nsk_update_column_host", "nsk_nccl_unique_id", "nsk_nccl_comm_init",
-    "nsk_nccl_comm_destroy", "nsk_apply_allreduce", "nsk_solve_k_sharded",
+    "nsk_nccl_comm_destroy", "nsk_apply_allreduce", "nsk_solve_k_sharded", "nsk_release_scratch",
 )
 
 

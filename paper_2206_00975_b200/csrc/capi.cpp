@@ -92,7 +92,9 @@ int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64
   nsk::Scratch t;
   NSK_CUDA_OK(t.alloc(sizeof(double) * op.s * (n > 0 ? n : 1) * ncomp, st));
   nsk::RowMap app{0, 1, op.appended};
-  if (int rc = nsk::gaussian_apply_key(op.key1, op.s, op.zero_mask(), op.m, ncomp, app, n, A + op.m * ncomp, lda,
+  const uint32_t* zmask = nullptr;
+  if (int rc = op.zero_mask(&zmask)) return rc;
+  if (int rc = nsk::gaussian_apply_key(op.key1, op.s, zmask, op.m, ncomp, app, n, A + op.m * ncomp, lda,
                                        t.as<double>(), op.s, st))
     return rc;
   return nsk::accumulate(SA, ldsa, nc_out, t.as<double>(), op.s, n, ncomp, st);
@@ -103,9 +105,11 @@ int dispatch_apply(const Operator& op, int ncomp, const nsk::RowMap& rows, int64
 // nothing across columns, so they run the two blocks one after the other.
 int dispatch_main2(const Operator& op, int ncomp, const nsk::RowMap& rows, int64_t n, const double* A, int64_t lda,
                    int64_t kb, const double* B, int64_t ldb, double* SA, int64_t ldsa, cudaStream_t st) {
-  if (kb > 0 && op.kind == nsk::GAUSSIAN)
-    return nsk::gaussian_apply_key2(op.key0, op.s, op.zero_mask(), 0, ncomp, rows, n, A, lda, kb, B, ldb, SA, ldsa,
-                                    st);
+  if (kb > 0 && op.kind == nsk::GAUSSIAN) {
+    const uint32_t* zmask = nullptr;
+    if (int rc = op.zero_mask(&zmask)) return rc;
+    return nsk::gaussian_apply_key2(op.key0, op.s, zmask, 0, ncomp, rows, n, A, lda, kb, B, ldb, SA, ldsa, st);
+  }
   if (int rc = dispatch_main(op, ncomp, rows, n, A, lda, SA, ldsa, st)) return rc;
   if (kb == 0) return nsk::OK;
   return dispatch_main(op, ncomp, rows, kb, B, ldb, SA + ldsa * n * out_ncomp(op, ncomp), ldsa, st);
@@ -755,6 +759,7 @@ static int tls_finish(int nc, int64_t rows, const double* M, int64_t ldm, int64_
 int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,
                            int64_t lda, const void* B, int64_t ldb, double cond_limit, int allow_marginal, void* X,
                            int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info, void* stream) {
+  if (k > 64) return nsk::fail(nsk::EINVAL_, "tls: this build supports at most 64 right-hand sides");
   if (int rc = check_op(h)) return rc;
   const Operator& op = *OP(h);
   if (k < 1) return nsk::fail(nsk::EINVAL_, "tls: B must have at least one column");
@@ -785,6 +790,7 @@ int nsk_tls_solve_sketched(const nsk_operator* h, int scalar, int64_t m, int64_t
 int nsk_tls_solve_exact(int scalar, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
                         int64_t ldb, double cond_limit, int allow_marginal, void* X, int64_t ldx, void* Vk,
                         int64_t ldv, double* sigma, double* info, void* stream) {
+  if (k > 64) return nsk::fail(nsk::EINVAL_, "tls: this build supports at most 64 right-hand sides");
   if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "tls: bad scalar kind");
   if (k < 1) return nsk::fail(nsk::EINVAL_, "tls: B must have at least one column");
   if (n < k) return nsk::fail(nsk::EINVAL_, "tls: need n >= k");
@@ -805,6 +811,7 @@ int nsk_tls_solve_exact(int scalar, int64_t m, int64_t n, int64_t k, const void*
 int nsk_tls_solve_exact_host(int scalar, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
                              int64_t ldb, double cond_limit, int allow_marginal, void* X, int64_t ldx, void* Vk,
                              int64_t ldv, double* sigma, double* info) {
+  if (k > 64) return nsk::fail(nsk::EINVAL_, "tls: this build supports at most 64 right-hand sides");
   if (lda < m || ldb < m || k < 1 || n < 1) return nsk::fail(nsk::EINVAL_, "tls: bad dimensions");
   cudaStream_t st = host_stream();
   const int nc = scalar == NSK_COMPLEX ? 2 : 1;
@@ -832,6 +839,7 @@ int nsk_tls_solve_exact_host(int scalar, int64_t m, int64_t n, int64_t k, const 
 int nsk_tls_solve_sketched_host(const nsk_operator* h, int scalar, int64_t m, int64_t n, int64_t k, const void* A,
                                 int64_t lda, const void* B, int64_t ldb, double cond_limit, int allow_marginal,
                                 void* X, int64_t ldx, void* Vk, int64_t ldv, double* sigma, double* info) {
+  if (k > 64) return nsk::fail(nsk::EINVAL_, "tls: this build supports at most 64 right-hand sides");
   if (int rc = check_op(h)) return rc;
   const Operator& op = *OP(h);
   if (lda < m || ldb < m || k < 1 || n < 1) return nsk::fail(nsk::EINVAL_, "tls: bad dimensions");

@@ -337,7 +337,9 @@ int launch_bn(int BN, const GaussParams& p, int64_t q_tiles, int64_t s_tiles, in
 
 int gaussian_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                    double* SA, int64_t ldsa, cudaStream_t st) {
-  return gaussian_apply_key(op.key0, op.s, op.zero_mask(), 0, ncomp, rows, n, A, lda, SA, ldsa, st);
+  const uint32_t* zmask = nullptr;
+  if (int rc = op.zero_mask(&zmask)) return rc;
+  return gaussian_apply_key(op.key0, op.s, zmask, 0, ncomp, rows, n, A, lda, SA, ldsa, st);
 }
 
 int gaussian_apply_key(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t zoff, int ncomp, const RowMap& rows,

@@ -100,9 +100,11 @@ struct Operator {
   // call that needs rows [row_lo, row_hi) not covered yet builds one for them (tile-aligned);
   // row_hi < 0 means m, row_hi <= row_lo means no CountSketch rows are needed.
   const DeviceTables* tables(int64_t row_lo = 0, int64_t row_hi = -1) const;
-  // Device bitmask of the zeroed rows (m_eff bits) on the current device, or
-  // nullptr when no row is zeroed.  Re-uploaded after every downdate.
-  const uint32_t* zero_mask() const;
+  // Device bitmask of the zeroed rows (m_eff bits) on the current device in
+  // *out, nullptr when no row is zeroed.  Re-uploaded after every downdate.
+  // Returns ECUDA (with the message set) when the upload fails -- never a
+  // silent "no zeroed rows".
+  int zero_mask(const uint32_t** out) const;
   mutable std::vector<std::pair<int, uint32_t*>> zmask_dev;  // (device, mask)
   mutable uint64_t zmask_version = 0, state_version = 0;
   ~Operator();
@@ -190,7 +192,14 @@ int mask_zeroed(const Operator& op, double* col, int ncomp, cudaStream_t st);
 int tls_corner(int ncomp, const double* Vk, int64_t ldv, int64_t n, int64_t k, double* X, int64_t ldx,
                cudaStream_t st);
 
-// Stream-ordered scratch allocation (cudaMallocAsync from the device pool).
+// The library's own stream-ordered memory pool on the current device (created
+// on first use).  Freed scratch stays mapped in it -- repeated calls with
+// gigabyte-sized scratch (host staging, the exact solver's Q) would otherwise
+// re-map HBM every call -- without touching the device's default pool that
+// PyTorch and other libraries use; nsk_release_scratch() trims it.
+cudaMemPool_t scratch_pool();
+
+// Stream-ordered scratch allocation from scratch_pool().
 struct Scratch {
   void* p = nullptr;
   cudaStream_t st = nullptr;
@@ -202,25 +211,9 @@ struct Scratch {
   }
   cudaError_t alloc(size_t bytes, cudaStream_t s) {
     st = s;
-    keep_pool();
-    return cudaMallocAsync(&p, bytes ? bytes : 8, s);
-  }
-  // Keep freed blocks in the device's default pool instead of unmapping them
-  // at every synchronisation (once per device): repeated calls with
-  // gigabyte-sized scratch (host staging, the exact solver's Q) would
-  // otherwise re-map HBM on every call.
-  static void keep_pool() {
-    static std::atomic<uint64_t> done{0};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
-    const uint64_t bit = uint64_t(1) << dev;
-    if (done.load(std::memory_order_relaxed) & bit) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    done.fetch_or(bit, std::memory_order_relaxed);
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool) return cudaErrorMemoryAllocation;
+    return cudaMallocFromPoolAsync(&p, bytes ? bytes : 8, pool, s);
   }
   template <class T>
   T* as() const {

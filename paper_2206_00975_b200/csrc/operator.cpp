@@ -191,6 +191,14 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     if (t.device == devno && (!window || (t.cs_base <= row_lo && row_hi <= t.cs_base + t.cs_rows))) return &t;
   DeviceTables t;
   t.device = devno;
+  // a failed build frees what it allocated (the next call retries from scratch)
+  auto bail = [&t]() -> const DeviceTables* {
+    void* ptrs[] = {t.idx, t.srht_slot, t.srht_row, t.sign_mask, t.cs_table, t.sign_bits, t.srtt_freq, t.srtt_row,
+                    t.srdct_sgn, t.srft_sgn, t.dct_freq, t.dct_row, t.cs_ent, t.cs_cnt};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    return nullptr;
+  };
   if (window) {  // tile-aligned window around the requested rows
     t.cs_base = row_lo / CS_T * CS_T;
     t.cs_rows = std::min<int64_t>(m, (row_hi + CS_T - 1) / CS_T * CS_T) - t.cs_base;
@@ -209,11 +217,11 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     e = up(reinterpret_cast<void**>(&t.srht_row), srht_row.data(), srht_row.size() * 4);
   if (e != cudaSuccess) {
     cuda_fail(e, "operator table upload");
-    return nullptr;
+    return bail();
   }
-  if (kind == SRHT && m >= 1024 && build_sign_mask(key0, m, &t.sign_mask) != OK) return nullptr;
+  if (kind == SRHT && m >= 1024 && build_sign_mask(key0, m, &t.sign_mask) != OK) return bail();
   if (kind == COUNTSKETCH && s <= 65536 && build_cs_table(key0, m, s, t.cs_base, t.cs_rows, &t.cs_table) != OK)
-    return nullptr;
+    return bail();
   if (kind == COUNTSKETCH && t.cs_rows > 0 && cs_owner_eligible(s, m)) {
     // Owner schedule over the window's full CS_T-row tiles, from the device row table.
     const int64_t ntiles = t.cs_rows / CS_T;
@@ -222,20 +230,20 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     std::vector<uint8_t> cnt;
     if (cudaMemcpy(tab.data(), t.cs_table, tab.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
       cuda_fail(cudaGetLastError(), "countsketch table readback");
-      return nullptr;
+      return bail();
     }
     if (ntiles > 0 && build_cs_schedule(tab.data(), ntiles, CS_T, s, ent, cnt) == OK) {
       if (up(reinterpret_cast<void**>(&t.cs_ent), ent.data(), ent.size() * 8) != cudaSuccess ||
           up(reinterpret_cast<void**>(&t.cs_cnt), cnt.data(), cnt.size()) != cudaSuccess) {
         cuda_fail(cudaGetLastError(), "countsketch schedule upload");
-        return nullptr;
+        return bail();
       }
       t.cs_ntiles = ntiles;
     }  // else: the streaming kernel covers every tile
   }
-  if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return nullptr;
-  if (kind == SRFT && build_srft_sgn(t.sign_bits, m, &t.srft_sgn) != OK) return nullptr;
-  if (kind == SRDCT && build_srdct_sgn(t.sign_bits, m, &t.srdct_sgn) != OK) return nullptr;
+  if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return bail();
+  if (kind == SRFT && build_srft_sgn(t.sign_bits, m, &t.srft_sgn) != OK) return bail();
+  if (kind == SRDCT && build_srdct_sgn(t.sign_bits, m, &t.srdct_sgn) != OK) return bail();
   if ((kind == SRFT || kind == SRDCT) && !idx.empty()) {
     // Slots sorted by FFT bin (idx mod 1024) for the tile kernel (srtt_tile.cu).
     std::vector<int32_t> order(idx.size());
@@ -248,7 +256,7 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     if (up(reinterpret_cast<void**>(&t.srtt_freq), freq.data(), freq.size() * 8) != cudaSuccess ||
         up(reinterpret_cast<void**>(&t.srtt_row), order.data(), order.size() * 4) != cudaSuccess) {
       cuda_fail(cudaGetLastError(), "srtt slot table upload");
-      return nullptr;
+      return bail();
     }
   }
   if (kind == SRDCT && !idx.empty()) {
@@ -268,7 +276,7 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     if (up(reinterpret_cast<void**>(&t.dct_freq), freq.data(), freq.size() * 8) != cudaSuccess ||
         up(reinterpret_cast<void**>(&t.dct_row), order.data(), order.size() * 4) != cudaSuccess) {
       cuda_fail(cudaGetLastError(), "srdct slot table upload");
-      return nullptr;
+      return bail();
     }
   }
   dev.push_back(t);
@@ -277,10 +285,11 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
 
 bool Operator::is_zeroed(int64_t j) const { return std::binary_search(zeroed.begin(), zeroed.end(), j); }
 
-const uint32_t* Operator::zero_mask() const {
-  if (zeroed.empty()) return nullptr;
+int Operator::zero_mask(const uint32_t** out) const {
+  *out = nullptr;
+  if (zeroed.empty()) return OK;
   int devno = 0;
-  if (cudaGetDevice(&devno) != cudaSuccess) return nullptr;
+  NSK_CUDA_OK(cudaGetDevice(&devno));
   std::lock_guard<std::mutex> lock(mu);
   if (zmask_version != state_version) {  // operator changed: drop every device copy
     if (!zmask_dev.empty()) cudaDeviceSynchronize();  // earlier applies may still read them
@@ -293,15 +302,22 @@ const uint32_t* Operator::zero_mask() const {
     zmask_version = state_version;
   }
   for (auto& d : zmask_dev)
-    if (d.first == devno) return d.second;
+    if (d.first == devno) {
+      *out = d.second;
+      return OK;
+    }
   const int64_t words = (m_eff() + 31) / 32;
   std::vector<uint32_t> bits(static_cast<size_t>(words), 0u);
   for (int64_t j : zeroed) bits[static_cast<size_t>(j >> 5)] |= 1u << (j & 31);
   uint32_t* d = nullptr;
-  if (cudaMalloc(&d, sizeof(uint32_t) * words) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, bits.data(), sizeof(uint32_t) * words, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  NSK_CUDA_OK(cudaMalloc(&d, sizeof(uint32_t) * words));
+  if (cudaError_t e = cudaMemcpy(d, bits.data(), sizeof(uint32_t) * words, cudaMemcpyHostToDevice)) {
+    cudaFree(d);
+    return cuda_fail(e, "zeroed-row mask upload");
+  }
   zmask_dev.emplace_back(devno, d);
-  return d;
+  *out = d;
+  return OK;
 }
 
 Operator::~Operator() {

@@ -25,8 +25,6 @@ int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, 
                   double* SA, int64_t ldsa, cudaStream_t st);
 int srft_stream_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                       double* SA, int64_t ldsa, cudaStream_t st);
-int srdct_ws_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
-                   int64_t ldsa, cudaStream_t st);
 int srdct_stream_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
                        int64_t ldsa, cudaStream_t st);
 int srdct_tile_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
@@ -126,8 +124,6 @@ int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, con
   // FFT (srtt_tile.cu) when the shape allows, else the strided FFT
   // (srtt_fast.cu), else the direct evaluator.
   if (op.kind == SRDCT && ncomp == 1) {
-    const int rw = srdct_ws_apply(op, rows, n, A, lda, SA, ldsa, st);
-    if (rw != NOTAPPLICABLE) return rw;
     const int rsd = srdct_stream_apply(op, rows, n, A, lda, SA, ldsa, st);
     if (rsd != NOTAPPLICABLE) return rsd;
     const int rd = srdct_tile_apply(op, rows, n, A, lda, SA, ldsa, st);

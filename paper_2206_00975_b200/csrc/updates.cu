@@ -278,10 +278,15 @@ int tls_corner(int ncomp, const double* Vk, int64_t ldv, int64_t n, int64_t k, d
   NSK_CUDA_OK(flag.alloc(sizeof(int), st));
   NSK_CUDA_OK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
   const size_t smem = sizeof(double) * k * k * ncomp;
-  if (ncomp == 1)
+  if (ncomp == 1) {
+    NSK_CUDA_OK(cudaFuncSetAttribute(tls_corner_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
     tls_corner_kernel<1><<<1, 128, smem, st>>>(Vk, ldv, n, k, X, ldx, flag.as<int>());
-  else
+  } else {
+    NSK_CUDA_OK(cudaFuncSetAttribute(tls_corner_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));  // complex k = 64: 64 KiB
     tls_corner_kernel<2><<<1, 128, smem, st>>>(Vk, ldv, n, k, X, ldx, flag.as<int>());
+  }
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
   int host = 0;

@@ -96,16 +96,12 @@ def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
                                    (1 << 14, 1 << 14, 2), (7, 5 << 14, 149)])
 def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
     """Register-streamed Makhoul tiles (srdct_stream.cu, the default for m % 16384 == 0) against
-    scipy's DCT-III, and against the warp-specialised tiles (srdct_ws.cu, opt-in), the
-    shared-memory Makhoul tiles (srdct_tile.cu) and the zero-padded tile path."""
+    scipy's DCT-III, and against the shared-memory Makhoul tiles (srdct_tile.cu) and the
+    zero-padded tile path."""
     A = oracle.random_real(m, n, 13)
     got, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
     ref = oracle.apply(oracle.draw("srdct", s, m, 91), A)
     assert rel(got, ref) <= SA_TOL
-    monkeypatch.setenv("NSK_SRDCT_WS", "1")  # the opt-in warp-specialised tiles
-    other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
-    assert rel(got, other) <= SA_TOL
-    monkeypatch.delenv("NSK_SRDCT_WS")
     for env in ("NSK_SRDCT_NOSTREAM", "NSK_SRDCT_NOMAKHOUL"):  # cumulative: Makhoul tiles, then padded tiles
         monkeypatch.setenv(env, "1")
         other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
@@ -668,3 +664,23 @@ def test_nccl_entry_points_single_rank(nsk, oracle, kind, cyclic):
         assert _angle(host(W), Wref) <= 1e-8
     finally:
         comm.close()
+
+
+def test_tls_complex_many_rhs_and_release(nsk, oracle):
+    """Complex sketched TLS with k = 60 right-hand sides (the corner solve needs 57.6 KiB of
+    dynamic shared memory, above the 48 KiB default) against the oracle, k = 65 rejected before
+    any work, and nsk_release_scratch trims the library's private pool."""
+    from paper_2206_00975_b200 import _lib
+    rng = np.random.default_rng(3)
+    m, n, k, s = 600, 64, 60, 300
+    A = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    X0 = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    B = A @ X0 + 1e-6 * (rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k)))
+    S = nsk.SketchOperator.draw("gaussian", s, m, 5)
+    sol = nsk.tls_solve_sketched(dev(A), dev(B), S, allow_marginal=True)
+    Xr, Vr, sr, _, _ = oracle.tls_solve_sketched(A, B, oracle.draw("gaussian", s, m, 5), allow_marginal=True)
+    assert np.max(np.abs(host(sol.augmented_singular_values) - sr)) <= 1000 * U * sr[0]
+    assert rel(host(sol.X), Xr) <= 1e-8
+    with pytest.raises(ValueError):
+        nsk.tls_solve_sketched(dev(np.hstack([A, A[:, :1]])), dev(np.hstack([B, B[:, :5]])), S)
+    _lib.check(_lib.load().nsk_release_scratch())
