@@ -229,30 +229,47 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
     return op.tables(0, m);
   });
   bool have_tables = false;
-  std::vector<std::pair<int64_t, int64_t>> pending;  // chunks that landed before the tables existed
-  auto run_chunk = [&](int64_t r0, int64_t rows) {
-    nsk::RowMap shard{r0, 1, rows};
-    return dispatch_main2(op, nc_in, shard, n, dA + r0 * nc_in, m, kb, dB ? dB + r0 * nc_in : nullptr, m,
-                          parts.as<double>() + (r0 / chunk) * psz, op.s, st);
+  struct Pending {
+    int64_t r0, rows;
+    cudaEvent_t landed;
+  };
+  std::vector<Pending> pending;  // chunks that landed before the tables existed
+  // chunk apply: st waits for exactly this chunk's copy, then the row-shard apply into its own partial
+  auto run_chunk = [&](const Pending& c) {
+    cudaError_t e = cudaStreamWaitEvent(st, c.landed, 0);
+    cudaEventDestroy(c.landed);
+    if (e != cudaSuccess) return nsk::cuda_fail(e, "chunk wait");
+    nsk::RowMap shard{c.r0, 1, c.rows};  // chunk-major device copy: this chunk's block, ld = its rows
+    return dispatch_main2(op, nc_in, shard, n, dA + c.r0 * n * nc_in, c.rows, kb, dB ? dB + c.r0 * nc_in : nullptr, m,
+                          parts.as<double>() + (c.r0 / chunk) * psz, op.s, st);
   };
   auto flush = [&]() {
     have_tables = true;
-    if (!tab.get()) return static_cast<int>(nsk::ECUDA);
-    for (auto& c : pending)
-      if (int rc = run_chunk(c.first, c.second)) return rc;
+    int rc = tab.get() ? static_cast<int>(nsk::OK) : static_cast<int>(nsk::ECUDA);
+    for (auto& c : pending) {
+      if (rc == nsk::OK)
+        rc = run_chunk(c);
+      else
+        cudaEventDestroy(c.landed);
+    }
     pending.clear();
-    return static_cast<int>(nsk::OK);
+    return rc;
   };
-  // each row chunk is sketched (row-shard apply into its own partial) as soon as it has landed
-  auto sketch_chunk = [&](int64_t r0, int64_t rows) {
+  // each row chunk is sketched as soon as it has landed (or, while the tables are still being built,
+  // right after they exist -- each apply waits on its own chunk's event either way)
+  auto sketch_chunk = [&](int64_t r0, int64_t rows, cudaEvent_t landed) {
+    const Pending c{r0, rows, landed};
     if (!have_tables) {
       if (tab.wait_for(std::chrono::seconds(0)) != std::future_status::ready) {
-        pending.emplace_back(r0, rows);
+        pending.push_back(c);
         return static_cast<int>(nsk::OK);
       }
-      if (int rc = flush()) return rc;
+      if (int rc = flush()) {
+        cudaEventDestroy(landed);
+        return rc;
+      }
     }
-    return run_chunk(r0, rows);
+    return run_chunk(c);
   };
   int rc = nsk::h2d_rows(A, m, n, lda, elem, dA, chunk, st, sketch_chunk);
   if (!have_tables) {

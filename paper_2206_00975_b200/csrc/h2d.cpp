@@ -11,9 +11,13 @@
 // pinned source).  A pinned source (cudaHostAlloc / cudaHostRegister memory) is
 // DMAed directly.  Either way the matrix moves in row chunks and the compute
 // stream waits per chunk, so the caller can sketch chunk c while chunk c + 1
-// is in flight.
+// is in flight.  On the device the chunks are laid out chunk-major: chunk c
+// (rows [c chunk, c chunk + rows)) is a rows x n column-major block with
+// leading dimension rows at element offset c chunk n -- with one chunk, plain
+// column-major with ld m -- so the staged DMAs are contiguous runs.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -33,6 +37,16 @@ struct Staging {
   std::mutex mu;  // one staged transfer at a time per process
   char* buf = nullptr;
 };
+
+// Host threads packing the ring (NSK_STAGE_THREADS overrides; default 8, measured best of 4/8/16).
+int stage_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("NSK_STAGE_THREADS");
+    const int v = e ? std::atoi(e) : 8;
+    return v >= 1 && v <= 64 ? v : 8;
+  }();
+  return t;
+}
 
 Staging& staging() {
   static Staging s;
@@ -79,21 +93,33 @@ int join_streams(cudaStream_t cs, cudaStream_t st) {
   return OK;
 }
 
+// The chunk ending now on cs: its landing event goes to on_chunk (which owns it and makes its own
+// stream wait on it), or st waits for it here when there is no callback.
+int chunk_landed(int64_t r0, int64_t rows, cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
+  if (!on_chunk) return join_streams(cs, st);
+  cudaEvent_t e;
+  NSK_CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (cudaError_t err = cudaEventRecord(e, cs)) {
+    cudaEventDestroy(e);
+    return cuda_fail(err, "chunk event");
+  }
+  return on_chunk(r0, rows, e);
+}
+
 int h2d_pinned(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, char* dA, int64_t chunk,
-               cudaStream_t cs, cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk) {
+               cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t rows = std::min(chunk, m - r0);
-    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * elem, elem * m, A + r0 * elem, elem * lda, elem * rows, n,
+    // chunk-major destination: chunk c is its own rows x n column-major block (ld = rows) at row offset r0 * n
+    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * n * elem, elem * rows, A + r0 * elem, elem * lda, elem * rows, n,
                                   cudaMemcpyHostToDevice, cs));
-    if (int rc = join_streams(cs, st)) return rc;
-    if (on_chunk)
-      if (int rc = on_chunk(r0, rows)) return rc;
+    if (int rc = chunk_landed(r0, rows, cs, st, on_chunk)) return rc;
   }
   return OK;
 }
 
 int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, char* dA, int64_t chunk,
-               cudaStream_t cs, cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk) {
+               cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
   Staging& stg = staging();
   std::lock_guard<std::mutex> lock(stg.mu);
   if (!stg.buf) NSK_CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&stg.buf), SLOT * RING, cudaHostAllocPortable));
@@ -116,7 +142,8 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
   for (int s = 0; s < RING; ++s) owner[s].store(static_cast<size_t>(s), std::memory_order_relaxed);
   std::atomic<size_t> next{0};
   std::atomic<bool> abort{false};
-  const int nthreads = static_cast<int>(std::min<size_t>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())), T));
+  const int nthreads = static_cast<int>(std::min<size_t>(
+      std::min<unsigned>(static_cast<unsigned>(stage_threads()), std::max(1u, std::thread::hardware_concurrency())), T));
   std::vector<std::thread> workers;
   for (int w = 0; w < nthreads; ++w)
     workers.emplace_back([&]() {
@@ -145,8 +172,13 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
     const int s = static_cast<int>(t % RING);
     while (!filled[t].load(std::memory_order_acquire)) std::this_thread::yield();
     const Tile& tl = tiles[t];
-    cudaError_t e = cudaMemcpy2DAsync(dA + (tl.r0 + tl.c0 * m) * elem, elem * m, stg.buf + s * SLOT, elem * tl.nr,
-                                      elem * tl.nr, tl.nc, cudaMemcpyHostToDevice, cs);
+    // chunk-major destination (see h2d_pinned): a tile spanning the chunk's rows is one contiguous run
+    const int64_t cr0 = tl.r0 / chunk * chunk, crows = std::min(chunk, m - cr0);
+    char* dst = dA + (cr0 * n + (tl.r0 - cr0) + tl.c0 * crows) * elem;
+    cudaError_t e = tl.nr == crows
+                        ? cudaMemcpyAsync(dst, stg.buf + s * SLOT, elem * tl.nr * tl.nc, cudaMemcpyHostToDevice, cs)
+                        : cudaMemcpy2DAsync(dst, elem * crows, stg.buf + s * SLOT, elem * tl.nr, elem * tl.nr, tl.nc,
+                                            cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaEventRecord(ev[s], cs);
     // the previous tile's DMA runs ahead of this one: once it is done its slot goes to the tile RING later
     if (e == cudaSuccess && t >= 1) {
@@ -159,9 +191,8 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
       break;
     }
     if (tl.chunk_end > 0) {
-      rc = join_streams(cs, st);
       const int64_t cend = tl.chunk_end, cstart = (cend - 1) / chunk * chunk;
-      if (rc == OK && on_chunk) rc = on_chunk(cstart, cend - cstart);
+      rc = chunk_landed(cstart, cend - cstart, cs, st, on_chunk);
     }
   }
   if (rc != OK) abort.store(true);
@@ -175,7 +206,7 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
 }  // namespace
 
 int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void* dA, int64_t chunk,
-             cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk) {
+             cudaStream_t st, const ChunkFn& on_chunk) {
   if (m <= 0 || n <= 0) return OK;
   if (chunk <= 0 || chunk > m) chunk = m;
   cudaStream_t cs = copy_stream();

@@ -225,12 +225,16 @@ int sm_count();
 
 // ---- host -> device (h2d.cpp) ---------------------------------------------
 // Copies host A (m x n column-major, lda, elem bytes per entry) to device dA
-// (leading dimension m) in row chunks of `chunk` rows on a per-thread copy
-// stream; st waits for each chunk before on_chunk(r0, rows) runs (may be
-// empty).  Pageable sources stream through a pinned staging ring filled by host
+// in row chunks of `chunk` rows on a per-thread copy stream, chunk-major: chunk
+// c is a rows_c x n column-major block (ld rows_c) at element offset c chunk n
+// (one chunk = plain column-major, ld m).  Each landed chunk is handed to on_chunk(r0, rows, landed): the
+// callback owns the event (its work must wait on it, then destroy it) and may
+// defer that work; without a callback st simply waits for every chunk.
+// Pageable sources stream through a pinned staging ring filled by host
 // threads; pinned sources are DMAed directly.
+using ChunkFn = std::function<int(int64_t, int64_t, cudaEvent_t)>;
 int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void* dA, int64_t chunk,
-             cudaStream_t st, const std::function<int(int64_t, int64_t)>& on_chunk);
+             cudaStream_t st, const ChunkFn& on_chunk);
 bool host_is_pinned(const void* p);
 cudaStream_t copy_stream();
 

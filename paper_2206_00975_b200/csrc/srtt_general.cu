@@ -34,6 +34,7 @@
 // Q and a long outer sum (N = 99850: Q = 50, P2 = 1997); still s N / Q, not s N.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "nsk_internal.hpp"
@@ -97,14 +98,26 @@ __device__ __forceinline__ void small_dft(double2 (&v)[R]) {
     v[1] = make_double2(d0.x - d1.y, d0.y + d1.x);  // d0 + i d1
     v[3] = make_double2(d0.x + d1.y, d0.y - d1.x);  // d0 - i d1
   } else {
+    // cos / sin (2 pi t / R), t < R, as literals (R = 3, 5, 7)
+    constexpr double C3[3] = {1.0, -0.5, -0.5};
+    constexpr double S3[3] = {0.0, 0.86602540378443864676, -0.86602540378443864676};
+    constexpr double C5[5] = {1.0, 0.30901699437494742410, -0.80901699437494742410, -0.80901699437494742410,
+                              0.30901699437494742410};
+    constexpr double S5[5] = {0.0, 0.95105651629515357212, 0.58778525229247312917, -0.58778525229247312917,
+                              -0.95105651629515357212};
+    constexpr double C7[7] = {1.0, 0.62348980185873353053, -0.22252093395631440429, -0.90096886790241912624,
+                              -0.90096886790241912624, -0.22252093395631440429, 0.62348980185873353053};
+    constexpr double S7[7] = {0.0, 0.78183148246802980871, 0.97492791218182360702, 0.43388373911755812048,
+                              -0.43388373911755812048, -0.97492791218182360702, -0.78183148246802980871};
     double2 out[R];
 #pragma unroll
     for (int p = 0; p < R; ++p) {
       double2 acc = v[0];
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double sn, cs;
-        sincospi(2.0 * static_cast<double>((r * p) % R) / R, &sn, &cs);  // constant-folded
+        const int t = (r * p) % R;
+        const double cs = R == 3 ? C3[t] : R == 5 ? C5[t] : C7[t];
+        const double sn = R == 3 ? S3[t] : R == 5 ? S5[t] : S7[t];
         acc.x = fma(v[r].x, cs, fma(-v[r].y, sn, acc.x));
         acc.y = fma(v[r].x, sn, fma(v[r].y, cs, acc.y));
       }
@@ -263,11 +276,16 @@ __global__ void srtt_gen_reduce(const double2* __restrict__ part, int64_t rstrid
 
 // Largest 2,3,5,7-smooth divisor of N not above QMAX, and its radix sequence (4s first).
 int64_t plan_q(int64_t N, std::vector<int>& radix) {
+  int64_t qmax = QMAX;  // NSK_GEN_QMAX (<= 1024): smaller Q = less shared memory, more CTAs per SM
+  if (const char* e = std::getenv("NSK_GEN_QMAX")) {
+    const int64_t v = std::atoll(e);
+    if (v >= 2 && v <= QMAX) qmax = v;
+  }
   int64_t best = 1;
-  for (int64_t a = 1; a <= QMAX; a *= 2)
-    for (int64_t b = a; b <= QMAX; b *= 3)
-      for (int64_t c5 = b; c5 <= QMAX; c5 *= 5)
-        for (int64_t d = c5; d <= QMAX; d *= 7)
+  for (int64_t a = 1; a <= qmax; a *= 2)
+    for (int64_t b = a; b <= qmax; b *= 3)
+      for (int64_t c5 = b; c5 <= qmax; c5 *= 5)
+        for (int64_t d = c5; d <= qmax; d *= 7)
           if (N % d == 0 && d > best) best = d;
   radix.clear();
   int64_t t = best;

@@ -238,6 +238,8 @@ __global__ void tls_corner_kernel(const double* __restrict__ Vk, int64_t ldv, in
     double b[64][NC];
     for (int64_t c = 0; c < k; ++c)
       for (int q = 0; q < NC; ++q) b[c][q] = -Vk[(i + c * ldv) * NC + q];
+    // The factor stores L with every later row interchange applied (whole rows are swapped, as
+    // LAPACK's getrf does), so P b is formed completely before the forward substitution.
     for (int64_t j = 0; j < k; ++j) {
       const int p = piv[j];
       if (p != j)
@@ -246,6 +248,8 @@ __global__ void tls_corner_kernel(const double* __restrict__ Vk, int64_t ldv, in
           b[j][q] = b[p][q];
           b[p][q] = t;
         }
+    }
+    for (int64_t j = 0; j < k; ++j) {
       for (int64_t r = j + 1; r < k; ++r) {
         const double lr = lu[(r + j * k) * NC], li = NC == 2 ? lu[(r + j * k) * NC + 1] : 0.0;
         b[r][0] -= lr * b[j][0] - (NC == 2 ? li * b[j][NC - 1] : 0.0);

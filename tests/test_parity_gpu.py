@@ -684,3 +684,18 @@ def test_tls_complex_many_rhs_and_release(nsk, oracle):
     with pytest.raises(ValueError):
         nsk.tls_solve_sketched(dev(np.hstack([A, A[:, :1]])), dev(np.hstack([B, B[:, :5]])), S)
     _lib.check(_lib.load().nsk_release_scratch())
+
+
+@pytest.mark.parametrize("k", [2, 7, 24])
+def test_tls_multi_rhs_real(nsk, oracle, k):
+    """X = -V_k1 V_k2^{-1} for several right-hand sides (the corner LU needs its row interchanges
+    applied before the forward substitution) against the oracle (tls.cpp:26-43)."""
+    rng = np.random.default_rng(k)
+    m, n, s = 500, 40, 200
+    A = rng.standard_normal((m, n))
+    B = A @ rng.standard_normal((n, k)) + 1e-5 * rng.standard_normal((m, k))
+    S = nsk.SketchOperator.draw("srdct", s, m, 12)
+    sol = nsk.tls_solve_sketched(dev(A), dev(B), S, allow_marginal=True)
+    Xr, Vr, sr, _, _ = oracle.tls_solve_sketched(A, B, oracle.draw("srdct", s, m, 12), allow_marginal=True)
+    assert _angle(host(sol.Vk), Vr) <= 1e-10
+    assert rel(host(sol.X), Xr) <= 1e-10
