@@ -5,10 +5,10 @@
 // (matrix.hpp:32-105).  A cudaMemcpy from pageable memory is staged by the
 // driver at ~11 GB/s on the B200 hosts; registering the buffer
 // (cudaHostRegister) costs ~0.25 s per 2 GiB (tools/micro/h2d_paths.cu).  So a
-// pageable source is streamed through a ring of pinned 32 MiB slots: host
+// pageable source is streamed through a ring of 16 pinned 16 MiB slots: 8 host
 // threads pack tiles of the matrix into free slots while the copy engine DMAs
-// the filled ones (48 GB/s measured with 8 threads, against 55.6 GB/s from a
-// pinned source).  A pinned source (cudaHostAlloc / cudaHostRegister memory) is
+// the filled ones (~46 GB/s for a 2 GiB matrix, against 55.6 GB/s from a
+// pinned source; ring / slot / thread counts swept on the B200 host).  A pinned source (cudaHostAlloc / cudaHostRegister memory) is
 // DMAed directly.  Either way the matrix moves in row chunks and the compute
 // stream waits per chunk, so the caller can sketch chunk c while chunk c + 1
 // is in flight.  On the device the chunks are laid out chunk-major: chunk c
@@ -30,8 +30,24 @@ namespace nsk {
 
 namespace {
 
-constexpr int RING = 8;                    // pinned slots
-constexpr size_t SLOT = size_t(32) << 20;  // bytes per slot
+constexpr int RING_MAX = 32;
+// pinned slots and bytes per slot (NSK_STAGE_RING / NSK_STAGE_SLOT_MB override; defaults measured best)
+int ring_slots() {
+  static const int r = [] {
+    const char* e = std::getenv("NSK_STAGE_RING");
+    const int v = e ? std::atoi(e) : 16;
+    return v >= 2 && v <= RING_MAX ? v : 16;
+  }();
+  return r;
+}
+size_t slot_bytes() {
+  static const size_t b = [] {
+    const char* e = std::getenv("NSK_STAGE_SLOT_MB");
+    const long v = e ? std::atol(e) : 16;
+    return static_cast<size_t>(v >= 1 && v <= 256 ? v : 16) << 20;
+  }();
+  return b;
+}
 
 struct Staging {
   std::mutex mu;  // one staged transfer at a time per process
@@ -122,6 +138,8 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
                cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
   Staging& stg = staging();
   std::lock_guard<std::mutex> lock(stg.mu);
+  const int RING = ring_slots();
+  const size_t SLOT = slot_bytes();
   if (!stg.buf) NSK_CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&stg.buf), SLOT * RING, cudaHostAllocPortable));
   // tiles: row chunks, each split into slot-sized (rows x cols) pieces
   std::vector<Tile> tiles;
@@ -138,7 +156,7 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
   const size_t T = tiles.size();
   std::vector<std::atomic<int>> filled(T);
   for (auto& f : filled) f.store(0, std::memory_order_relaxed);
-  std::atomic<size_t> owner[RING];
+  std::atomic<size_t> owner[RING_MAX];
   for (int s = 0; s < RING; ++s) owner[s].store(static_cast<size_t>(s), std::memory_order_relaxed);
   std::atomic<size_t> next{0};
   std::atomic<bool> abort{false};
@@ -163,7 +181,7 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
         filled[t].store(1, std::memory_order_release);
       }
     });
-  cudaEvent_t ev[RING];
+  cudaEvent_t ev[RING_MAX];
   int rc = OK;
   int made = 0;
   for (; made < RING && rc == OK; ++made)
