@@ -22,7 +22,7 @@
 // SA, and P = 1, g = 0 is the unsharded apply.)
 //
 // W at the sampled frequencies by decimation in time, N = Q P2 with Q the
-// largest 2,3,5,7-smooth divisor of N up to 1024:
+// largest 2,3,5,7-smooth divisor of N up to 512 (1024 with NSK_GEN_QMAX):
 //   W[f] = sum_{k1 < P2} w_N^{f k1} F_{k1}[f mod Q],  F_{k1} = DFT_Q(u[k1 + P2 k2]).
 // A CTA owns one column and a range of k1; it stages G = 4 consecutive k1
 // sequences at a time (32-byte row segments), runs a self-sorting mixed-radix
@@ -47,7 +47,7 @@ int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
 namespace {
 
 constexpr int GT = 256;     // threads per CTA
-constexpr int GG = 4;       // sequences (consecutive k1) per batch
+constexpr int GG_MAX = 4;   // sequences (consecutive k1) per batch: 4, or 2 when Q > 704 (shared memory)
 constexpr int QMAX = 1024;  // inner DFT length bound (shared memory: 2 G Q + 2 Q complex)
 constexpr int MAXPASS = 12;
 
@@ -153,8 +153,8 @@ __device__ void stockham_pass(const double2* __restrict__ in, double2* __restric
   }
 }
 
-template <int KIND, int NCIN, int NQ>  // KIND 0 srft, 1 srdct
-__global__ void __launch_bounds__(GT) srtt_gen_kernel(GenParams p) {
+template <int KIND, int NCIN, int NQ, int GG>  // KIND 0 srft, 1 srdct; GG sequences per batch
+__global__ void __launch_bounds__(GT, 2) srtt_gen_kernel(GenParams p) {  // two CTAs (16 warps) per SM
   extern __shared__ __align__(16) double2 smem[];
   const int Q = static_cast<int>(p.Q);
   double2* buf0 = smem;               // [G][Q]
@@ -276,10 +276,12 @@ __global__ void srtt_gen_reduce(const double2* __restrict__ part, int64_t rstrid
 
 // Largest 2,3,5,7-smooth divisor of N not above QMAX, and its radix sequence (4s first).
 int64_t plan_q(int64_t N, std::vector<int>& radix) {
-  int64_t qmax = QMAX;  // NSK_GEN_QMAX (<= 1024): smaller Q = less shared memory, more CTAs per SM
+  // Q <= 512 by default (NSK_GEN_QMAX up to 1024): four sequences per batch and two CTAs per SM fit; at
+  // m = 10^6 this measured 5.75 ms against 6.57 ms for Q = 1000 (a longer outer sum, better occupancy)
+  int64_t qmax = 512;
   if (const char* e = std::getenv("NSK_GEN_QMAX")) {
     const int64_t v = std::atoll(e);
-    if (v >= 2 && v <= QMAX) qmax = v;
+    if (v >= 2 && v <= QMAX) qmax = v;  // QMAX = 1024: the shared-memory bound
   }
   int64_t best = 1;
   for (int64_t a = 1; a <= qmax; a *= 2)
@@ -301,8 +303,8 @@ int64_t plan_q(int64_t N, std::vector<int>& radix) {
   return best;
 }
 
-template <int KIND, int NCIN>
-int launch_gen(int nq, const GenParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+template <int KIND, int NCIN, int GG>
+int launch_gen_g(int nq, const GenParams& p, dim3 grid, size_t smem, cudaStream_t st) {
   auto go = [&](auto kern) -> int {
     NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     KernelTimer tm(st, "srtt_gen_kernel");
@@ -312,10 +314,15 @@ int launch_gen(int nq, const GenParams& p, dim3 grid, size_t smem, cudaStream_t 
     NSK_CUDA_OK(cudaGetLastError());
     return OK;
   };
-  if (nq <= 1) return go(srtt_gen_kernel<KIND, NCIN, 1>);
-  if (nq <= 2) return go(srtt_gen_kernel<KIND, NCIN, 2>);
-  if (nq <= 4) return go(srtt_gen_kernel<KIND, NCIN, 4>);
-  return go(srtt_gen_kernel<KIND, NCIN, 8>);
+  if (nq <= 1) return go(srtt_gen_kernel<KIND, NCIN, 1, GG>);
+  if (nq <= 2) return go(srtt_gen_kernel<KIND, NCIN, 2, GG>);
+  if (nq <= 4) return go(srtt_gen_kernel<KIND, NCIN, 4, GG>);
+  return go(srtt_gen_kernel<KIND, NCIN, 8, GG>);
+}
+
+template <int KIND, int NCIN>
+int launch_gen(int gg, int nq, const GenParams& p, dim3 grid, size_t smem, cudaStream_t st) {
+  return gg == 4 ? launch_gen_g<KIND, NCIN, 4>(nq, p, grid, smem, st) : launch_gen_g<KIND, NCIN, 2>(nq, p, grid, smem, st);
 }
 
 }  // namespace
@@ -407,8 +414,10 @@ int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_
   double2* dpost = nullptr;
   uint8_t* dconj = nullptr;
   if (int rc = shard_slot_tables(op, g, N, dtab, &dfreq, &dpost, &dconj, st)) return rc;
-  // CTA ranges of k1: about two CTAs per SM over all columns, each range a multiple of G
-  const int64_t target = 2L * sm_count();
+  // two CTAs per SM: (2 GG + 2) Q complex doubles <= ~113 KiB
+  const int GG = (2 * GG_MAX + 2) * Q * 16 <= 113 * 1024 ? GG_MAX : 2;
+  // CTA ranges of k1: about four CTAs per SM over all columns, each range a multiple of G
+  const int64_t target = 4L * sm_count();
   int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((target + n - 1) / n, (P2 + GG - 1) / GG));
   int64_t per = (P2 + ranges - 1) / ranges;
   per = (per + GG - 1) / GG * GG;
@@ -443,8 +452,9 @@ int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_
     for (size_t r = 0; r < radix.size(); ++r) p.radix[r] = radix[r];
     p.part = part.as<double2>();
     const dim3 grid(static_cast<unsigned>(ranges), static_cast<unsigned>(n));
-    int rc = kind == 0 ? (ncomp == 1 ? launch_gen<0, 1>(nq, p, grid, smem, st) : launch_gen<0, 2>(nq, p, grid, smem, st))
-                       : launch_gen<1, 1>(nq, p, grid, smem, st);
+    int rc = kind == 0 ? (ncomp == 1 ? launch_gen<0, 1>(GG, nq, p, grid, smem, st)
+                                     : launch_gen<0, 2>(GG, nq, p, grid, smem, st))
+                       : launch_gen<1, 1>(GG, nq, p, grid, smem, st);
     if (rc != OK) return rc;
     if (int rc2 = srtt_post_reduce(kind, part.as<double2>(), n * NQ * GT, NQ * GT, ranges, n, ns, static_cast<int>(base),
                                    dpost, dconj, scale, SA, ldsa, st))
