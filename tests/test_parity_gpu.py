@@ -699,3 +699,45 @@ def test_tls_multi_rhs_real(nsk, oracle, k):
     Xr, Vr, sr, _, _ = oracle.tls_solve_sketched(A, B, oracle.draw("srdct", s, m, 12), allow_marginal=True)
     assert _angle(host(sol.Vk), Vr) <= 1e-10
     assert rel(host(sol.X), Xr) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,s,m,n,pinned", [("srht", 256, 1 << 20, 33, False), ("gaussian", 96, 300000, 40, False),
+                                               ("countsketch", 2048, 600000, 17, True), ("srdct", 128, 1 << 18, 9, False),
+                                               ("srft", 64, 20000, 3, True)])
+def test_host_strided_input(nsk, oracle, kind, s, m, n, pinned):
+    """Host A with a leading dimension larger than m (a block of a bigger Eigen matrix): the staged and
+    pinned copies honour lda, pipelined (>= 256 MiB) or not, against the oracle on the same rows."""
+    import ctypes
+    import torch
+    from paper_2206_00975_b200 import _lib
+    lda = m + 37
+    rng = np.random.default_rng(m % 1000)
+    big = rng.standard_normal((lda, n))
+    if pinned:
+        buf = torch.empty((n, lda), dtype=torch.float64, pin_memory=True).t()
+        buf.copy_(torch.from_numpy(big))
+        ptr = buf.data_ptr()
+    else:
+        big = np.asfortranarray(big)
+        ptr = big.ctypes.data
+    A = np.asfortranarray(big[:m])
+    S = nsk.SketchOperator.draw(kind, s, m, 71)
+    cplx_out = kind == "srft"
+    SA = np.empty((s, n), dtype=np.complex128 if cplx_out else np.float64, order="F")
+    _lib.check(_lib.load().nsk_apply_host(S.handle, 0, m, n, ctypes.c_void_p(ptr), lda,
+                                          SA.ctypes.data_as(ctypes.c_void_p), s))
+    assert rel(SA, oracle.apply(oracle.draw(kind, s, m, 71), A)) <= SA_TOL
+
+
+def test_nccl_empty_shard(nsk, oracle):
+    """A rank with no rows contributes zeros (nsk_apply_allreduce with mloc = 0)."""
+    from paper_2206_00975_b200.distributed import NcclComm, RowShard, sharded_apply_nccl
+    import torch
+    S = nsk.SketchOperator.draw("gaussian", 32, 1000, 3)
+    comm = NcclComm()
+    try:
+        A = torch.empty((0, 4), dtype=torch.float64, device="cuda")
+        SA = host(sharded_apply_nccl(S, A, RowShard(500, 1, 0), comm))
+        assert np.array_equal(SA, np.zeros((32, 4)))
+    finally:
+        comm.close()
