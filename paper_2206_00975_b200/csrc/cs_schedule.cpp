@@ -159,11 +159,19 @@ bool build_tile(const uint32_t* bucket_sign, int T, uint64_t* ent, uint8_t* cnt)
 
 int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, std::vector<uint64_t>& ent,
                       std::vector<uint8_t>& cnt) {
+  const size_t per_tile = static_cast<size_t>(CS_WARPS) * CS_GMAX * 32;
+  ent.resize(static_cast<size_t>(ntiles) * per_tile);
+  cnt.resize(static_cast<size_t>(ntiles) * CS_WARPS);
+  return build_cs_schedule_into(table, ntiles, T, s, ent.data(), cnt.data());
+}
+
+// The same into caller buffers (ntiles * CS_WARPS * CS_GMAX * 32 u64, ntiles * CS_WARPS u8); every
+// worker thread zeroes its own tiles, so a pinned buffer is filled without a serial memset.
+int build_cs_schedule_into(const uint32_t* table, int64_t ntiles, int T, int64_t s, uint64_t* ent_out,
+                           uint8_t* cnt_out) {
   if (s < 1 || s > 4 * CS_THREADS) return EINVAL_;
   if (T < 16 || T > CS_T_MAX || T % 16) return EINVAL_;
   const size_t per_tile = static_cast<size_t>(CS_WARPS) * CS_GMAX * 32;
-  ent.assign(static_cast<size_t>(ntiles) * per_tile, 0);
-  cnt.assign(static_cast<size_t>(ntiles) * CS_WARPS, 0);
   unsigned nth = std::thread::hardware_concurrency();
   if (nth < 1) nth = 1;
   if (nth > 32) nth = 32;
@@ -172,12 +180,16 @@ int build_cs_schedule(const uint32_t* table, int64_t ntiles, int T, int64_t s, s
   std::vector<std::thread> pool;
   for (unsigned q = 0; q < nth; ++q)
     pool.emplace_back([&, q]() {
-      for (int64_t t = q; t < ntiles; t += nth)
-        if (!build_tile(table + t * T, T, ent.data() + static_cast<size_t>(t) * per_tile,
-                        cnt.data() + static_cast<size_t>(t) * CS_WARPS)) {
+      for (int64_t t = q; t < ntiles; t += nth) {
+        uint64_t* et = ent_out + static_cast<size_t>(t) * per_tile;
+        uint8_t* ct = cnt_out + static_cast<size_t>(t) * CS_WARPS;
+        std::memset(et, 0, per_tile * sizeof(uint64_t));
+        std::memset(ct, 0, CS_WARPS);
+        if (!build_tile(table + t * T, T, et, ct)) {
           ok[q] = 0;
           return;
         }
+      }
     });
   for (auto& th : pool) th.join();
   for (char c : ok)

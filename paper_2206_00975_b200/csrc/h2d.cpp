@@ -76,6 +76,27 @@ struct Tile {
 
 }  // namespace
 
+std::unique_lock<std::mutex> pinned_scratch(size_t bytes, void** out) {
+  static std::mutex mu;
+  static void* buf = nullptr;
+  static size_t have = 0;
+  std::unique_lock<std::mutex> lock(mu);
+  *out = nullptr;
+  if (bytes > have) {
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    have = 0;
+    if (cudaHostAlloc(&buf, bytes, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      buf = nullptr;
+      return lock;
+    }
+    have = bytes;
+  }
+  *out = buf;
+  return lock;
+}
+
 cudaStream_t copy_stream() {
   thread_local cudaStream_t cs = nullptr;
   thread_local int dev = -1;

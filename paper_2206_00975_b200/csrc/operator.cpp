@@ -6,6 +6,8 @@
 // sketch.cpp:117-121); signs and hash buckets are regenerated on the device
 // from stream (seed, 0).  Only the sorted sample of s indices is stored.
 #include <algorithm>
+#include <cstdlib>
+#include <chrono>
 #include <cinttypes>
 #include <cstdio>
 #include <cstring>
@@ -224,21 +226,41 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     return bail();
   if (kind == COUNTSKETCH && t.cs_rows > 0 && cs_owner_eligible(s, m)) {
     // Owner schedule over the window's full CS_T-row tiles, from the device row table.
+    const bool dbg = std::getenv("NSK_TABLES_DEBUG") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto t0 = now();
     const int64_t ntiles = t.cs_rows / CS_T;
-    std::vector<uint32_t> tab(static_cast<size_t>(ntiles * CS_T));
-    std::vector<uint64_t> ent;
-    std::vector<uint8_t> cnt;
-    if (cudaMemcpy(tab.data(), t.cs_table, tab.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    // one pinned buffer: [table (ntiles CS_T u32) | schedule entries | counts]
+    const size_t per_tile = static_cast<size_t>(CS_WARPS) * CS_GMAX * 32;
+    const size_t tab_b = static_cast<size_t>(ntiles) * CS_T * 4, ent_b = static_cast<size_t>(ntiles) * per_tile * 8,
+                 cnt_b = static_cast<size_t>(ntiles) * CS_WARPS;
+    void* hbuf = nullptr;
+    auto hold = pinned_scratch(tab_b + ent_b + cnt_b, &hbuf);
+    if (!hbuf) {
+      fail(ENOMEM_, "countsketch schedule: pinned host scratch");
+      return bail();
+    }
+    uint32_t* tab = static_cast<uint32_t*>(hbuf);
+    uint64_t* ent = reinterpret_cast<uint64_t*>(static_cast<char*>(hbuf) + tab_b);
+    uint8_t* cnt = reinterpret_cast<uint8_t*>(ent) + ent_b;
+    if (cudaMemcpy(tab, t.cs_table, tab_b, cudaMemcpyDeviceToHost) != cudaSuccess) {
       cuda_fail(cudaGetLastError(), "countsketch table readback");
       return bail();
     }
-    if (ntiles > 0 && build_cs_schedule(tab.data(), ntiles, CS_T, s, ent, cnt) == OK) {
-      if (up(reinterpret_cast<void**>(&t.cs_ent), ent.data(), ent.size() * 8) != cudaSuccess ||
-          up(reinterpret_cast<void**>(&t.cs_cnt), cnt.data(), cnt.size()) != cudaSuccess) {
+    const auto t1 = now();
+    if (ntiles > 0 && build_cs_schedule_into(tab, ntiles, CS_T, s, ent, cnt) == OK) {
+      const auto t2 = now();
+      if (up(reinterpret_cast<void**>(&t.cs_ent), ent, ent_b) != cudaSuccess ||
+          up(reinterpret_cast<void**>(&t.cs_cnt), cnt, cnt_b) != cudaSuccess) {
         cuda_fail(cudaGetLastError(), "countsketch schedule upload");
         return bail();
       }
       t.cs_ntiles = ntiles;
+      if (dbg) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "nsk tables: cs readback %.1f ms, schedule %.1f ms, upload %.1f ms (%zu MB)\n",
+                     ms(t0, t1), ms(t1, t2), ms(t2, now()), ent_b >> 20);
+      }
     }  // else: the streaming kernel covers every tile
   }
   if ((kind == SRFT || kind == SRDCT) && build_sign_bits(key0, m, &t.sign_bits) != OK) return bail();

@@ -1,7 +1,13 @@
 #!/bin/bash
-# usage (inside gpurun): tools/bench_all.sh "<kinds>"  -- one bench line per kind into gpurun_out/bench_<kind>.log
+# usage (inside gpurun): tools/bench_all.sh [tag] -- one bench line per BASELINE config + the reference arm
 cd "$(dirname "$0")/.."
-for k in $1; do
-  timeout 600 python bench.py --kind $k --steps 20 --warmup 3 --e2e-steps 3 > gpurun_out/bench_$k.log 2>&1
-  tail -1 gpurun_out/bench_$k.log | timeout 10 python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(k:=d['config']['kind'], 'value=%.4g'%d['value'], 'kernel_ms=', r['kernel_ms'], 'achieved=', r['achieved'], r['unit'], 'frac=', r['frac'], 'svd_ms=', d['breakdown']['svd_ms'], 'e2e_ms=', d['e2e']['ms'], 'cpu=', d['cpu_baseline']['value'])" 2>&1 | tail -1
+TAG=${1:-r02}
+mkdir -p gpurun_out
+for k in srht countsketch gaussian srdct srft cfg0 cfg4; do
+  timeout 900 python bench.py --kind $k --steps 20 --warmup 5 --e2e-steps 3 > gpurun_out/bench_${TAG}_$k.log 2>&1
+  tail -1 gpurun_out/bench_${TAG}_$k.log | timeout 10 python tools/bsum.py $TAG
+done
+for k in srht countsketch srdct cfg0 cfg4; do
+  timeout 900 python bench.py --impl reference --kind $k --steps 5 --warmup 1 > gpurun_out/bench_${TAG}_reference_$k.log 2>&1
+  tail -1 gpurun_out/bench_${TAG}_reference_$k.log | cut -c1-200
 done
