@@ -22,7 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 SOURCES = ["operator.cpp", "capi.cpp", "gaussian_sketch.cu", "srht_sketch.cu", "countsketch.cu",
            "srtt_sketch.cu", "srtt_fast.cu", "srtt_general.cu", "jacobi_svd.cu", "residual.cu", "instrument.cpp", "updates.cu",
-           "cs_schedule.cpp", "h2d.cpp", "nccl_shard.cpp", "cluster_jacobi.cu", "srtt_tile.cu", "tall_qr.cu", "srdct_tile.cu", "srft_stream.cu", "srdct_stream.cu", "srft_ws.cu"]
+           "cs_schedule.cpp", "h2d.cpp", "nccl_shard.cpp", "cluster_jacobi.cu", "srtt_tile.cu", "tall_qr.cu", "srdct_stream.cu", "srft_ws.cu"]
 
 
 def _deps():

@@ -36,8 +36,8 @@ struct DeviceTables {
   int64_t* srtt_freq = nullptr;     // srft/srdct: sample indices sorted by idx mod 1024 (tile FFT bin)
   int32_t* srtt_row = nullptr;      // output row of each sorted slot
   uint64_t* srdct_sgn = nullptr;    // srdct (srdct_stream.cu): per tile, row class and column, main | mirror negate bits
-  uint64_t* srft_sgn = nullptr;     // srft (srft_stream.cu): per tile, row class and column pair, 64 negate bits
-  int64_t* dct_freq = nullptr;      // srdct (srdct_tile.cu): v index n(a) of each sample, sorted by n mod 1024
+  uint64_t* srft_sgn = nullptr;     // srft (srft_ws.cu): per 16-column tile, row class and column pair, 64 negate bits
+  int64_t* dct_freq = nullptr;      // srdct (srdct_stream.cu): v index n(a) of each sample, sorted by n mod 1024
   int32_t* dct_row = nullptr;       // output row of each sorted srdct slot
   // CountSketch owner schedule (cs_schedule.cpp) over CS_T-row tiles.
   uint64_t* cs_ent = nullptr;       // [tile][warp][CS_GMAX][32] packed entries

@@ -282,7 +282,7 @@ const DeviceTables* Operator::tables(int64_t row_lo, int64_t row_hi) const {
     }
   }
   if (kind == SRDCT && !idx.empty()) {
-    // Makhoul index of each sample (srdct_tile.cu): y_{2n} = v_n, y_{2n+1} = v_{m-1-n}.
+    // Makhoul index of each sample (srdct_stream.cu): y_{2n} = v_n, y_{2n+1} = v_{m-1-n}.
     std::vector<int64_t> nv(idx.size());
     for (size_t r = 0; r < idx.size(); ++r) {
       const int64_t a = idx[r];

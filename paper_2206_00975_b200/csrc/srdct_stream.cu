@@ -3,11 +3,11 @@
 // Reference: apply(), srdct branch (/root/reference/proj/src/sketch.cpp:218-229)
 // and dct3_unitary_columns (transforms.cpp:38-64):
 //   y_a = sum_k X_k cos(pi k (2a+1) / 2N),  X_k = c_k d_k A[k],  SA = sqrt(N/s) y_idx.
-// Algebra as in srdct_tile.cu (Makhoul: G_k = (X_k - i X_{N-k}) w^k / 2 with
-// w = e^{i pi / 2N} is Hermitian, v_n = sum_k G_k W^{kn} is real, y_{2n} = v_n,
-// y_{2n+1} = v_{N-1-n}; with k = k1 + P k2, L = 1024, only k1 in [0, P/2] is
-// transformed and v_n = sum_{k1} 2 Re(W^{n k1} F_{k1}[n mod L])), reorganised
-// like srft_stream.cu for the FP64 pipe:
+// Makhoul: G_k = (X_k - i X_{N-k}) w^k / 2 with w = e^{i pi / 2N} is Hermitian,
+// v_n = sum_k G_k W^{kn} is real, y_{2n} = v_n, y_{2n+1} = v_{N-1-n}; with
+// k = k1 + P k2, L = 1024, only k1 in [0, P/2] is transformed and
+// v_n = sum_{k1} 2 Re(W^{n k1} F_{k1}[n mod L]).  Organised for the FP64 pipe
+// (register-streamed tiles, no shared-memory staging of A):
 //
 //  * the factor w^{k1} of a column is constant over k2, so it moves out of the
 //    FFT into the sampled stage: the per-column step becomes

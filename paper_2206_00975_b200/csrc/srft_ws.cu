@@ -2,10 +2,13 @@
 // sampler warps) so the sampled stage of one tile overlaps the FFT of the next.
 //
 // Reference: apply(), srft branch (/root/reference/proj/src/sketch.cpp:206-217)
-// and idft_unitary_columns (transforms.cpp:17-36).  Same algebra as
-// srft_stream.cu (decimation in time, L = 1024, j = k1 + P k2, real columns
-// paired into complex sequences z = u_e + i u_o, Hermitian unpacking in the
-// sampled stage), with tiles of 8 real columns (4 sequences) and two roles in
+// and idft_unitary_columns (transforms.cpp:17-36).  srft as s samples of one
+// length-m DFT by decimation in time, L = 1024, j = k1 + P k2: the real k1
+// sequences of a column are paired into complex sequences z = u_e + i u_o
+// (u_k1 = d_j A[j]), each z gets a 1024-point DFT (two register DFT32 passes
+// with an in-place transpose), and the sampled stage forms
+// sum_k1 w_m^{f k1} U_k1[f mod L] with the Hermitian unpacking of each pair
+// (Z[q], conj Z[-q]); tiles of 8 real k1 columns (4 sequences), two roles in
 // one CTA of 8 warps:
 //
 //  * FFT warps 0-3: a lane (sequence i, row class a, 8 row classes per warp)
@@ -86,6 +89,25 @@ __device__ __forceinline__ double flipx(double v, uint32_t mask) {
 // output (a, k) lives in row 32 a + (k ^ (a & 1)).  V: bin q, sequence i at
 // q * 4 + (i ^ ((q >> 1) & 3)).
 __device__ __forceinline__ int uidx(int r, int i) { return r * 4 + (i ^ ((r >> 1) & 3)); }
+
+// Negate masks (16-k1 tiles of 8 sequence pairs): word (T, a, i) bit 2b + e = 1 iff the Rademacher
+// bit of row j = 16 T + 2 i + e + P (a + 32 b) is 0 (rng.hpp:57: bit 1 -> +1).  srft_ws_kernel reads
+// the masks of two 8-column tiles from one 16-column word set.
+__global__ void build_srft_sgn_kernel(const uint32_t* __restrict__ bits, int64_t P, int64_t words,
+                                      uint64_t* __restrict__ out) {
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t T = w / 256, a = (w / 8) % 32, i = w % 8;
+    uint64_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t j = 16 * T + 2 * i + P * (a + 32 * b);  // even: j and j + 1 share a word
+      const uint32_t wd = bits[j >> 5];
+      v |= static_cast<uint64_t>((~wd >> (j & 31)) & 1u) << (2 * b);
+      v |= static_cast<uint64_t>((~wd >> ((j + 1) & 31)) & 1u) << (2 * b + 1);
+    }
+    out[w] = v;
+  }
+}
 
 __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
   extern __shared__ __align__(16) double2 smx[];
@@ -299,6 +321,20 @@ __global__ void srft_ws_reduce(const double2* __restrict__ part, int64_t tiles, 
 }
 
 }  // namespace
+
+int build_srft_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out) {
+  *out = nullptr;
+  if (m % (XL * 16) != 0) return OK;  // the tile kernel does not apply
+  const int64_t P = m / XL, words = (P / 16) * 256;
+  NSK_CUDA_OK(cudaMalloc(out, sizeof(uint64_t) * words));
+  int64_t blocks = (words + 255) / 256;
+  if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+  build_srft_sgn_kernel<<<static_cast<unsigned>(blocks), 256>>>(sign_bits, P, words, *out);
+  count_launch();
+  NSK_CUDA_OK(cudaGetLastError());
+  NSK_CUDA_OK(cudaStreamSynchronize(0));  // the table kernels ran on the legacy stream (copies on other streams continue)
+  return OK;
+}
 
 // NOTAPPLICABLE unless the whole column of a real A is applied, m is a
 // multiple of 16 * 1024 (the srft_sgn table) and A is 16-byte aligned with an

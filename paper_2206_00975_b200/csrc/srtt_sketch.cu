@@ -23,12 +23,8 @@ int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
                     int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
 int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                   double* SA, int64_t ldsa, cudaStream_t st);
-int srft_stream_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
-                      double* SA, int64_t ldsa, cudaStream_t st);
 int srdct_stream_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
                        int64_t ldsa, cudaStream_t st);
-int srdct_tile_apply(const Operator& op, const RowMap& rows, int64_t n, const double* A, int64_t lda, double* SA,
-                     int64_t ldsa, cudaStream_t st);
 
 namespace {
 
@@ -120,20 +116,18 @@ int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
 
 int srtt_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                double* SA, int64_t ldsa, cudaStream_t st) {
-  // srdct: Makhoul-paired tiles (srdct_tile.cu); then the tiled single-pass
-  // FFT (srtt_tile.cu) when the shape allows, else the strided FFT
-  // (srtt_fast.cu), else the direct evaluator.
+  // srdct: register-streamed Makhoul tiles (srdct_stream.cu), srft of a real A:
+  // warp-specialised tiles (srft_ws.cu), both for m % 16384 == 0; then the
+  // tiled single-pass FFT (srtt_tile.cu: complex srft input, m % 4096 == 0
+  // srdct), else the strided FFT / cyclic shards (srtt_fast.cu), else the
+  // general-length engine (srtt_general.cu), else the direct evaluator.
   if (op.kind == SRDCT && ncomp == 1) {
     const int rsd = srdct_stream_apply(op, rows, n, A, lda, SA, ldsa, st);
     if (rsd != NOTAPPLICABLE) return rsd;
-    const int rd = srdct_tile_apply(op, rows, n, A, lda, SA, ldsa, st);
-    if (rd != NOTAPPLICABLE) return rd;
   }
   if (op.kind == SRFT && ncomp == 1) {
     const int rw = srft_ws_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
     if (rw != NOTAPPLICABLE) return rw;
-    const int rs = srft_stream_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
-    if (rs != NOTAPPLICABLE) return rs;
   }
   const int rc = srtt_tile_apply(op, ncomp, rows, n, A, lda, SA, ldsa, st);
   if (rc != NOTAPPLICABLE) return rc;

@@ -96,13 +96,13 @@ def test_srtt_fast_path_parity(nsk, oracle, kind, s, m, n, cplx):
                                    (1 << 14, 1 << 14, 2), (7, 5 << 14, 149)])
 def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
     """Register-streamed Makhoul tiles (srdct_stream.cu, the default for m % 16384 == 0) against
-    scipy's DCT-III, and against the shared-memory Makhoul tiles (srdct_tile.cu) and the
-    zero-padded tile path."""
+    scipy's DCT-III, and against the shared-memory tile path (srtt_tile.cu) and the strided FFT
+    (srtt_fast.cu) on the same operator."""
     A = oracle.random_real(m, n, 13)
     got, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
     ref = oracle.apply(oracle.draw("srdct", s, m, 91), A)
     assert rel(got, ref) <= SA_TOL
-    for env in ("NSK_SRDCT_NOSTREAM", "NSK_SRDCT_NOMAKHOUL"):  # cumulative: Makhoul tiles, then padded tiles
+    for env in ("NSK_SRDCT_NOSTREAM", "NSK_SRTT_NOTILE"):  # cumulative: shared-memory tiles, then strided FFT
         monkeypatch.setenv(env, "1")
         other, _ = gpu_apply(nsk, "srdct", s, m, 91, A)
         assert rel(got, other) <= SA_TOL, env
@@ -113,13 +113,13 @@ def test_srdct_makhoul_parity(nsk, oracle, monkeypatch, s, m, n):
                                    (7, 5 << 14, 149)])
 def test_srft_stream_parity(nsk, oracle, monkeypatch, s, m, n):
     """Warp-specialised srft tiles (srft_ws.cu, the default for real A with m % 16384 == 0)
-    against numpy's inverse FFT, and against the register-streamed tiles (srft_stream.cu) and
-    the shared-memory tile path on the same operator."""
+    against numpy's inverse FFT, and against the shared-memory tile path (srtt_tile.cu) and the
+    strided FFT (srtt_fast.cu) on the same operator."""
     A = oracle.random_real(m, n, 17)
     got, _ = gpu_apply(nsk, "srft", s, m, 93, A)
     ref = oracle.apply(oracle.draw("srft", s, m, 93), A)
     assert rel(got, ref) <= SA_TOL
-    for env in ("NSK_SRFT_WS", "NSK_SRFT_NOSTREAM"):  # cumulative: stream tiles, then shared-memory tiles
+    for env in ("NSK_SRFT_WS", "NSK_SRTT_NOTILE"):  # cumulative: shared-memory tiles, then strided FFT
         monkeypatch.setenv(env, "0" if env == "NSK_SRFT_WS" else "1")
         other, _ = gpu_apply(nsk, "srft", s, m, 93, A)
         assert rel(got, other) <= SA_TOL, env
