@@ -257,6 +257,10 @@ int nsk_apply_allreduce(const nsk_operator* op, int scalar, int64_t row0, int64_
 int nsk_solve_k_sharded(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep, int64_t mloc, int64_t n,
                         const void* A_local, int64_t lda, int64_t k, void* W, int64_t ldw, double* sigma,
                         void* nccl_comm, void* stream);
+/* The same from host buffers (A_local m_loc x n with lda, W n x k with ldw, sigma n). */
+int nsk_solve_k_sharded_host(const nsk_operator* op, int scalar, int64_t row0, int64_t rstep, int64_t mloc,
+                             int64_t n, const void* A_local, int64_t lda, int64_t k, void* W, int64_t ldw,
+                             double* sigma, void* nccl_comm);
 
 /* ---- memory --------------------------------------------------------------
  * Scratch (device copies of host inputs, partial sketches, SVD workspaces)

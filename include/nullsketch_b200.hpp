@@ -232,6 +232,50 @@ inline NullspaceResult solve_k(const Matrix& A, Index k, const SketchOperator& S
   return r;
 }
 
+// ---- multi-GPU (one process per GPU; not in the reference, which is single-process) ----------
+// This rank's rows of A: local row j is global row row0 + rstep * j (contiguous blocks for gaussian /
+// srht / countsketch, cyclic row0 = g, rstep = P for srft / srdct).
+struct RowShard {
+  Index row0 = 0, rstep = 1;
+};
+
+// An NCCL communicator made by the library (ncclGetUniqueId on rank 0, the 128-byte id distributed by
+// the caller, ncclCommInitRank); callers that already own an ncclComm_t pass it to solve_k_sharded.
+class NcclComm {
+ public:
+  static std::string unique_id() {
+    std::string id(NSK_NCCL_UNIQUE_ID_BYTES, '\0');
+    check(nsk_nccl_unique_id(&id[0]));
+    return id;
+  }
+  NcclComm(int nranks, const std::string& id, int rank) { check(nsk_nccl_comm_init(nranks, id.data(), rank, &c_)); }
+  ~NcclComm() { nsk_nccl_comm_destroy(c_); }
+  NcclComm(const NcclComm&) = delete;
+  NcclComm& operator=(const NcclComm&) = delete;
+  void* get() const { return c_; }
+
+ private:
+  void* c_ = nullptr;
+};
+
+// solve_k (nullspace.hpp:24) with A row-sharded across the ranks of `nccl_comm` (an ncclComm_t):
+// every rank passes its rows and receives the same W and sigma.
+inline NullspaceResult solve_k_sharded(const Matrix& A_local, const RowShard& shard, Index k, const SketchOperator& S,
+                                       void* nccl_comm) {
+  NullspaceResult r;
+  const Index n = A_local.cols();
+  if (k < 0 || k >= n)
+    throw std::invalid_argument("nullspace: k must satisfy 0 <= k < n, got k = " + std::to_string(k) +
+                                ", n = " + std::to_string(n));
+  r.W = Matrix(n, k, out_kind(S, A_local));
+  r.sketched_singular_values.resize(static_cast<size_t>(n));
+  check(nsk_solve_k_sharded_host(S.handle(), static_cast<int>(A_local.kind()), shard.row0, shard.rstep,
+                                 A_local.rows(), n, A_local.data(), A_local.rows() > 0 ? A_local.rows() : 1, k,
+                                 r.W.data(), n, r.sketched_singular_values.data(), nccl_comm));
+  r.k = k;
+  return r;
+}
+
 // nullspace.hpp:30
 inline NullspaceResult solve_tol(const Matrix& A, double eps, const SketchOperator& S) {
   NullspaceResult r;

@@ -29,6 +29,7 @@ EXPORTS = (
     "nsk_update_column", "nsk_tls_solve_sketched", "nsk_tls_solve_sketched_host", "nsk_tls_solve_exact", "nsk_tls_solve_exact_host", "nsk_update_row_host",
     "nsk_downdate_row_host", "nsk_update_column_host", "nsk_nccl_unique_id", "nsk_nccl_comm_init",
     "nsk_nccl_comm_destroy", "nsk_apply_allreduce", "nsk_solve_k_sharded", "nsk_release_scratch",
+    "nsk_solve_k_sharded_host",
 )
 
 
@@ -98,6 +99,7 @@ def load():
     L.nsk_nccl_comm_destroy.argtypes = [vp]
     L.nsk_apply_allreduce.argtypes = [vp, c_int, i64, i64, i64, i64, vp, i64, vp, i64, vp, vp]
     L.nsk_solve_k_sharded.argtypes = [vp, c_int, i64, i64, i64, i64, vp, i64, i64, vp, i64, vp, vp, vp]
+    L.nsk_solve_k_sharded_host.argtypes = [vp, c_int, i64, i64, i64, i64, vp, i64, i64, vp, i64, vp, vp]
     L.nsk_kernel_launches.restype = i64
     L.nsk_timing_enable.argtypes = [c_int]
     L.nsk_timing_enable.restype = None

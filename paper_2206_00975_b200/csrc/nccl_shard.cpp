@@ -184,4 +184,40 @@ int nsk_solve_k_sharded(const nsk_operator* h, int scalar, int64_t row0, int64_t
   return nsk::jacobi_trailing(nc, op.s, n, sa.as<double>(), op.s, k, static_cast<double*>(W), ldw, sigma, st);
 }
 
+int nsk_solve_k_sharded_host(const nsk_operator* h, int scalar, int64_t row0, int64_t rstep, int64_t mloc, int64_t n,
+                             const void* A_local, int64_t lda, int64_t k, void* W, int64_t ldw, double* sigma,
+                             void* comm) {
+  if (!h) return nsk::fail(nsk::EINVAL_, "null sketch operator");
+  if (int rc = check_comm(comm)) return rc;
+  const nsk::Operator& op = *reinterpret_cast<const nsk::Operator*>(h);
+  if (scalar != NSK_REAL && scalar != NSK_COMPLEX) return nsk::fail(nsk::EINVAL_, "unknown scalar kind");
+  if (n < 1 || k < 0 || k >= n) return nsk::fail(nsk::EINVAL_, "nullspace: k must satisfy 0 <= k < n");
+  if (mloc > 0 && (lda < mloc || !A_local)) return nsk::fail(nsk::EINVAL_, "sketch apply: lda < rows");
+  if ((k > 0 && (!W || ldw < n)) || !sigma) return nsk::fail(nsk::EINVAL_, "solve_k: bad outputs");
+  thread_local cudaStream_t st_tl = nullptr;  // this thread's compute stream (h2d_rows copies on another)
+  thread_local int st_dev = -1;
+  int dev = 0;
+  NSK_CUDA_OK(cudaGetDevice(&dev));
+  if (!st_tl || st_dev != dev) {
+    NSK_CUDA_OK(cudaStreamCreateWithFlags(&st_tl, cudaStreamNonBlocking));
+    st_dev = dev;
+  }
+  cudaStream_t st = st_tl;
+  const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_nc(op, scalar);
+  nsk::Scratch a, w, sg;
+  NSK_CUDA_OK(a.alloc(sizeof(double) * nc_in * (mloc > 0 ? mloc : 1) * n, st));
+  if (int rc = nsk::h2d_rows(A_local, mloc, n, lda, sizeof(double) * nc_in, a.p, mloc, st, nullptr)) return rc;
+  NSK_CUDA_OK(w.alloc(sizeof(double) * nc * n * (k > 0 ? k : 1), st));
+  NSK_CUDA_OK(sg.alloc(sizeof(double) * n, st));
+  if (int rc = nsk_solve_k_sharded(h, scalar, row0, rstep, mloc, n, a.p, mloc > 0 ? mloc : 1, k, w.p, n,
+                                   sg.as<double>(), comm, st))
+    return rc;
+  if (k > 0)
+    NSK_CUDA_OK(cudaMemcpy2DAsync(W, sizeof(double) * nc * ldw, w.p, sizeof(double) * nc * n, sizeof(double) * nc * n,
+                                  k, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaMemcpyAsync(sigma, sg.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  NSK_CUDA_OK(cudaStreamSynchronize(st));
+  return nsk::OK;
+}
+
 }  // extern "C"

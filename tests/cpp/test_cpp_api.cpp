@@ -222,6 +222,23 @@ int main() {
     CHECK(self.rel_err == 0.0 && self.sin_Vk < 1e-12);
     CHECK_THROWS_AS(tls_solve_exact({A0, B}), TlsExistenceError);
   }
+  {  // multi-GPU entry point on a one-rank NCCL communicator made by the library: equals solve_k
+    const Index m = 5000, n = 12;
+    Matrix A = random_real(m, n, 91);
+    auto S = SketchOperator::draw(SketchKind::srht, 64, 8192, 5);
+    Matrix A8(8192, n, ScalarKind::real);  // srht needs m = 2^13 here: pad with zero rows
+    for (Index j = 0; j < n; ++j)
+      for (Index i = 0; i < m; ++i) A8(i, j) = A(i, j);
+    NullspaceResult one = solve_k(A8, 2, S);
+    NcclComm comm(1, NcclComm::unique_id(), 0);
+    NullspaceResult sh = solve_k_sharded(A8, RowShard{0, 1}, 2, S, comm.get());
+    CHECK(sh.W.rows() == n && sh.W.cols() == 2);
+    double dmax = 0.0;
+    for (size_t i = 0; i < sh.sketched_singular_values.size(); ++i)
+      dmax = std::max(dmax, std::abs(sh.sketched_singular_values[i] - one.sketched_singular_values[i]));
+    CHECK(dmax < 1e-12 * one.sketched_singular_values[0]);
+    CHECK_THROWS_AS(solve_k_sharded(A8, RowShard{0, 1}, n, S, comm.get()), std::invalid_argument);
+  }
   if (failures) {
     std::fprintf(stderr, "%d check(s) failed\n", failures);
     return 1;
