@@ -110,6 +110,19 @@ struct Operator {
   // silent "no zeroed rows".
   int zero_mask(const uint32_t** out) const;
   mutable std::vector<std::pair<int, uint32_t*>> zmask_dev;  // (device, mask)
+  // srft cyclic-shard tables for the warp-specialised tile kernel (srft_ws.cu), per (device, g, P):
+  // the shard's sign bits and negate masks, its frequencies a mod (m / P) sorted by bin, the output
+  // row of each slot and the shard twiddle w_m^{a g} of each output row.
+  struct ShardTables {
+    int device = -1;
+    int64_t g = 0, P = 1;
+    uint32_t* bits = nullptr;
+    uint64_t* sgn = nullptr;
+    int64_t* freq = nullptr;
+    int32_t* row = nullptr;
+    double2* post = nullptr;
+  };
+  mutable std::deque<ShardTables> shard_tabs;
   mutable uint64_t zmask_version = 0, state_version = 0;
   ~Operator();
 };

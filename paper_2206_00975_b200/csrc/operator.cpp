@@ -345,6 +345,12 @@ int Operator::zero_mask(const uint32_t** out) const {
 Operator::~Operator() {
   int cur = 0;
   cudaGetDevice(&cur);
+  for (auto& t : shard_tabs) {
+    cudaSetDevice(t.device);
+    void* ptrs[] = {t.bits, t.sgn, t.freq, t.row, t.post};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+  }
   for (auto& d : zmask_dev) {
     cudaSetDevice(d.first);
     cudaFree(d.second);

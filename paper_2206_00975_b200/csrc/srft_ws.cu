@@ -28,6 +28,10 @@
 // restaged only after the samplers have seen V_FULL of the tile that last
 // used it.  Shared memory: two tile buffers and V (64 KiB each, swizzled so
 // every access is 4 wavefronts per warp) and the w_1024 twiddles.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+#include <mutex>
 #include "fft32.cuh"
 #include "nsk_internal.hpp"
 
@@ -301,7 +305,7 @@ __global__ void srft_ws_anchor_kernel(const int64_t* __restrict__ freq, int nslo
 // SA(row, c) = scale * sum over the CTAs covering column c of their piece for c (fixed order).
 __global__ void srft_ws_reduce(const double2* __restrict__ part, int64_t tiles, int64_t chunk, int64_t jmax,
                                int64_t n, int nslots, const int32_t* __restrict__ row_of_slot, double scale,
-                               double* __restrict__ SA, int64_t ldsa) {
+                               const double2* __restrict__ post, double* __restrict__ SA, int64_t ldsa) {
   const int64_t total = n * nslots;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -315,8 +319,29 @@ __global__ void srft_ws_reduce(const double2* __restrict__ part, int64_t tiles, 
       v.y += x.y;
     }
     const int64_t row = row_of_slot[o];
+    if (post) {  // cyclic shard: w_m^{a g} of this output row
+      const double2 w = post[row];
+      v = make_double2(w.x * v.x - w.y * v.y, w.x * v.y + w.y * v.x);
+    }
     SA[2 * (row + c * ldsa)] = scale * v.x;
     SA[2 * (row + c * ldsa) + 1] = scale * v.y;
+  }
+}
+
+// Sign bits of a cyclic shard: bit l of the result = bit (g + P l) of the operator's sign bits.
+__global__ void gather_shard_bits(const uint32_t* __restrict__ bits, int64_t g, int64_t P, int64_t N,
+                                  uint32_t* __restrict__ out) {
+  const int64_t words = (N + 31) / 32;
+  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; w < words;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t v = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t l = 32 * w + b;
+      if (l >= N) break;
+      const int64_t j = g + P * l;
+      v |= ((bits[j >> 5] >> (j & 31)) & 1u) << b;
+    }
+    out[w] = v;
   }
 }
 
@@ -336,19 +361,13 @@ int build_srft_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out) {
   return OK;
 }
 
-// NOTAPPLICABLE unless the whole column of a real A is applied, m is a
-// multiple of 16 * 1024 (the srft_sgn table) and A is 16-byte aligned with an
-// even lda.  NSK_SRFT_WS=0 selects the single-role stream kernel instead.
-int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
-                  double* SA, int64_t ldsa, cudaStream_t st) {
-  const char* e = std::getenv("NSK_SRFT_WS");
-  if (e && !std::atoi(e)) return NOTAPPLICABLE;
-  const int64_t m = op.m, s = op.s;
-  if (op.kind != SRFT || ncomp != 1 || n == 0) return NOTAPPLICABLE;
-  if (!(rows.row0 == 0 && rows.rstep == 1 && rows.mloc == m)) return NOTAPPLICABLE;
-  if (m % (XL * 16) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0) return NOTAPPLICABLE;
-  const DeviceTables* tb = op.tables();
-  if (!tb || !tb->srft_sgn || !tb->srtt_freq || !tb->srtt_row) return ECUDA;
+namespace {
+
+// The warp-specialised apply over one length-m sequence per column (the whole operator, or a cyclic
+// shard with its own tables and the shard twiddle `post`).
+int srft_ws_run(int64_t m, int64_t s, int64_t n, const double* A, int64_t lda, const uint64_t* sgn,
+                const int64_t* freq, const int32_t* row, const double2* post, double* SA, int64_t ldsa,
+                cudaStream_t st) {
   const int64_t P = m / XL, tiles = P / XKT, total = n * tiles;
   int64_t G = sm_count();
   if (G > total) G = total;
@@ -368,13 +387,12 @@ int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, 
     {
       int64_t blocks = (tiles * XNQ * 128 + 255) / 256;
       if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-      srft_ws_anchor_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(tb->srtt_freq + b, ns, m, tiles,
+      srft_ws_anchor_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(freq + b, ns, m, tiles,
                                                                            anc.as<double2>());
       count_launch();
       NSK_CUDA_OK(cudaGetLastError());
     }
-    WsParams p{A, lda, m, P, tiles, total, chunk, jmax, tb->srft_sgn, tb->srtt_freq + b, ns, anc.as<double2>(),
-               part.as<double2>()};
+    WsParams p{A, lda, m, P, tiles, total, chunk, jmax, sgn, freq + b, ns, anc.as<double2>(), part.as<double2>()};
     KernelTimer tm(st, "srft_ws_kernel");
     srft_ws_kernel<<<static_cast<unsigned>(G), XT, smem, st>>>(p);
     tm.stop();
@@ -383,11 +401,98 @@ int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, 
     int64_t blocks = (n * ns + 255) / 256;
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
     srft_ws_reduce<<<static_cast<unsigned>(blocks), 256, 0, st>>>(part.as<double2>(), tiles, chunk, jmax, n, ns,
-                                                                  tb->srtt_row + b, scale, SA, ldsa);
+                                                                  row + b, scale, post, SA, ldsa);
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
   }
   return OK;
+}
+
+}  // namespace
+
+// NOTAPPLICABLE unless the whole column of a real A is applied, m is a multiple of 16 * 1024 and A
+// is 16-byte aligned with an even lda.
+int srft_ws_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                  double* SA, int64_t ldsa, cudaStream_t st) {
+  const char* e = std::getenv("NSK_SRFT_WS");
+  if (e && !std::atoi(e)) return NOTAPPLICABLE;
+  const int64_t m = op.m;
+  if (op.kind != SRFT || ncomp != 1 || n == 0) return NOTAPPLICABLE;
+  if (!(rows.row0 == 0 && rows.rstep == 1 && rows.mloc == m)) return NOTAPPLICABLE;
+  if (m % (XL * 16) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0) return NOTAPPLICABLE;
+  const DeviceTables* tb = op.tables();
+  if (!tb || !tb->srft_sgn || !tb->srtt_freq || !tb->srtt_row) return ECUDA;
+  return srft_ws_run(m, op.s, n, A, lda, tb->srft_sgn, tb->srtt_freq, tb->srtt_row, nullptr, SA, ldsa, st);
+}
+
+// Cyclic shard g of P (local rows g + P l, N = m / P a multiple of 16 * 1024): the same kernel on the
+// local sequence with the shard's own signs and frequencies a mod N, then the twiddle w_m^{a g}
+// (decimation in time, srtt_general.cu header).  Tables are built once per (operator, device, g, P).
+int srft_ws_shard(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                  double* SA, int64_t ldsa, cudaStream_t st) {
+  const char* e = std::getenv("NSK_SRFT_WS");
+  if (e && !std::atoi(e)) return NOTAPPLICABLE;
+  const int64_t m = op.m, s = op.s, P = rows.rstep, g = rows.row0, N = rows.mloc;
+  if (op.kind != SRFT || ncomp != 1 || n == 0 || P < 2 || g < 0 || g >= P || m % P != 0 || N != m / P)
+    return NOTAPPLICABLE;
+  if (N % (XL * 16) != 0 || (reinterpret_cast<uintptr_t>(A) & 15) != 0 || (lda & 1) != 0) return NOTAPPLICABLE;
+  const DeviceTables* tb = op.tables();
+  if (!tb || !tb->sign_bits) return ECUDA;
+  int devno = 0;
+  NSK_CUDA_OK(cudaGetDevice(&devno));
+  const Operator::ShardTables* sh = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(op.mu);
+    for (auto& t : op.shard_tabs)
+      if (t.device == devno && t.g == g && t.P == P) sh = &t;
+    if (!sh) {
+      Operator::ShardTables t;
+      t.device = devno;
+      t.g = g;
+      t.P = P;
+      auto bail = [&t](cudaError_t err, const char* what) {
+        void* ptrs[] = {t.bits, t.sgn, t.freq, t.row, t.post};
+        for (void* q : ptrs)
+          if (q) cudaFree(q);
+        return cuda_fail(err, what);
+      };
+      const int64_t words = (N + 31) / 32;
+      if (cudaError_t err = cudaMalloc(&t.bits, sizeof(uint32_t) * words)) return bail(err, "shard sign bits");
+      int64_t blocks = (words + 255) / 256;
+      if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
+      gather_shard_bits<<<static_cast<unsigned>(blocks), 256>>>(tb->sign_bits, g, P, N, t.bits);
+      count_launch();
+      if (cudaError_t err = cudaStreamSynchronize(0)) return bail(err, "shard sign bits");
+      if (build_srft_sgn(t.bits, N, &t.sgn) != OK || !t.sgn) return bail(cudaErrorUnknown, "shard negate masks");
+      // slots sorted by bin (a mod N) mod 1024, output row = original slot, twiddle w_m^{a g}
+      std::vector<int32_t> order(static_cast<size_t>(s));
+      for (int64_t r = 0; r < s; ++r) order[r] = static_cast<int32_t>(r);
+      std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+        return ((op.idx[x] % N) & (XL - 1)) < ((op.idx[y] % N) & (XL - 1));
+      });
+      std::vector<int64_t> freq(static_cast<size_t>(s));
+      std::vector<double2> post(static_cast<size_t>(s));
+      for (int64_t r = 0; r < s; ++r) {
+        freq[r] = op.idx[order[r]] % N;
+        const uint64_t e2 = static_cast<uint64_t>((static_cast<unsigned __int128>(op.idx[r]) * static_cast<uint64_t>(g)) %
+                                                  static_cast<uint64_t>(m));
+        const double ang = 2.0 * M_PI * static_cast<double>(e2) / static_cast<double>(m);
+        post[r] = make_double2(std::cos(ang), std::sin(ang));
+      }
+      if (cudaError_t err = cudaMalloc(&t.freq, sizeof(int64_t) * s)) return bail(err, "shard slots");
+      if (cudaError_t err = cudaMalloc(&t.row, sizeof(int32_t) * s)) return bail(err, "shard slots");
+      if (cudaError_t err = cudaMalloc(&t.post, sizeof(double2) * s)) return bail(err, "shard slots");
+      if (cudaError_t err = cudaMemcpy(t.freq, freq.data(), sizeof(int64_t) * s, cudaMemcpyHostToDevice))
+        return bail(err, "shard slots");
+      if (cudaError_t err = cudaMemcpy(t.row, order.data(), sizeof(int32_t) * s, cudaMemcpyHostToDevice))
+        return bail(err, "shard slots");
+      if (cudaError_t err = cudaMemcpy(t.post, post.data(), sizeof(double2) * s, cudaMemcpyHostToDevice))
+        return bail(err, "shard slots");
+      op.shard_tabs.push_back(t);
+      sh = &op.shard_tabs.back();
+    }
+  }
+  return srft_ws_run(N, s, n, A, lda, sh->sgn, sh->freq, sh->row, sh->post, SA, ldsa, st);
 }
 
 }  // namespace nsk

@@ -32,6 +32,8 @@ int srtt_direct_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t
                       int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
 int srtt_general_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A,
                        int64_t lda, double* SA, int64_t ldsa, cudaStream_t st);
+int srft_ws_shard(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
+                  double* SA, int64_t ldsa, cudaStream_t st);
 
 // ---- plain sign bitmask for srft/srdct (m/8 bytes) -------------------------
 __global__ void build_sign_bits_kernel(PhiloxKey key, int64_t m, uint32_t* __restrict__ out) {
@@ -310,8 +312,12 @@ int srtt_fast_apply(const Operator& op, int ncomp, const RowMap& rows, int64_t n
   const int64_t m = op.m, s = op.s;
   const bool full = rows.row0 == 0 && rows.rstep == 1 && rows.mloc == m;
   if (!full && n > 0 && rows.mloc % (L * W) == 0 && srtt_general_eligible(op, rows) &&
-      !std::getenv("NSK_SRTT_DIRECT") && !(op.kind == SRDCT && ncomp != 1))
+      !std::getenv("NSK_SRTT_DIRECT") && !(op.kind == SRDCT && ncomp != 1)) {
+    // srft of a real A on a shard of 16 * 1024 multiples: the warp-specialised tiles (srft_ws.cu)
+    const int rw = srft_ws_shard(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+    if (rw != NOTAPPLICABLE) return rw;
     return srtt_fast_shard(op, ncomp, rows, n, A, lda, SA, ldsa, st);
+  }
   if (!full || m % (L * W) != 0 || n == 0) {
     // any other length, and the cyclic shards: the mixed-radix engine (srtt_general.cu); the direct
     // O(s m n) evaluator only for contiguous partial shards (or NSK_SRTT_DIRECT=1)
