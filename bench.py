@@ -504,13 +504,41 @@ def e2e_measure(nsk, cfg, A, args, world, rank, mloc, comm=None):
     t_pin = timed(Ah_pin.data_ptr())
     bi = mloc * n * (16 if cfg["cplx"] else 8)
     bo = W.nbytes + sig.nbytes
+    tls = None
+    if kind == "gaussian" and not cfg["cplx"] and n == 512:
+        # configs[3] is a total-least-squares problem: the same call as the reference's tls command
+        # (tls_solve_sketched, tls.cpp:97-113) on [A | b] = the first 511 and the last column
+        X = np.empty((n - 1, 1), order="F")
+        Vk = np.empty((n, 1), order="F")
+        sg = np.empty(n)
+        info = np.zeros(4)
+
+        def tls_one(ptr):
+            h = ctypes.c_void_p()
+            _lib.check(L.nsk_op_draw(_lib.KIND_CODES[kind], s, mloc, 9000002, ctypes.byref(h)))
+            try:
+                _lib.check(L.nsk_tls_solve_sketched_host(
+                    h, 0, mloc, n - 1, 1, ctypes.c_void_p(ptr), mloc, ctypes.c_void_p(ptr + 8 * mloc * (n - 1)), mloc,
+                    1e12, 1, X.ctypes.data_as(ctypes.c_void_p), n - 1, Vk.ctypes.data_as(ctypes.c_void_p), n,
+                    sg.ctypes.data_as(ctypes.c_void_p), info.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+            finally:
+                L.nsk_op_destroy(h)
+        tls_one(Ah_page.ctypes.data)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            tls_one(Ah_page.ctypes.data)
+        t_tls = (time.perf_counter() - t0) / steps
+        tls = {"value": mloc / t_tls, "unit": "rows/s", "ms": round(t_tls * 1e3, 3),
+               "api": "nsk_op_draw + nsk_tls_solve_sketched_host + nsk_op_destroy on [A | b] in pageable memory "
+                      "(one-pass S [A | b], both SVDs, X = -V_k1 V_k2^{-1})"}
     return {"value": mloc / t_page, "unit": "rows/s", "ms": round(t_page * 1e3, 3), "steps": steps,
             "api": "nsk_op_draw + nsk_solve_k_host + nsk_op_destroy (draw and device tables, H2D of A from "
                    "pageable host memory through the library's pinned staging ring, sketch, QR + Jacobi SVD, "
                    "D2H of W and sigma); host wall clock",
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
             "pinned": {"value": mloc / t_pin, "unit": "rows/s", "ms": round(t_pin * 1e3, 3),
-                       "api": "same call with A in pinned (cudaHostAlloc) memory"}}
+                       "api": "same call with A in pinned (cudaHostAlloc) memory"},
+            **({"tls": tls} if tls else {})}
 
 
 def e2e_sharded(nsk, cfg, Ah, steps, rank, mloc, comm):

@@ -741,3 +741,38 @@ def test_nccl_empty_shard(nsk, oracle):
         assert np.array_equal(SA, np.zeros((32, 4)))
     finally:
         comm.close()
+
+
+def test_host_staging_complex_and_tls_pipeline(nsk, oracle):
+    """Complex pageable input through the staging ring (16-byte entries, chunk-major device copy), and
+    sketched TLS from pageable host buffers large enough for the chunked pipeline with the B block
+    copied first (capi.cpp host_sketch with kb > 0) against the device-buffer TLS on the same data."""
+    import ctypes
+    import torch
+    from paper_2206_00975_b200 import _lib
+    rng = np.random.default_rng(21)
+    m, n = 300000, 6
+    A = np.asfortranarray(rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n)))
+    S = nsk.SketchOperator.draw("gaussian", 48, m, 5)
+    got = np.asarray(nsk.apply(S, A).data)
+    assert rel(got, oracle.apply(oracle.draw("gaussian", 48, m, 5), A)) <= SA_TOL
+    # TLS: [A | b] 2^21 x 32 real = 512 MiB -> pipelined host path
+    m2, n2 = 1 << 21, 31
+    A2 = np.asfortranarray(rng.standard_normal((m2, n2)))
+    b2 = np.asfortranarray(A2 @ rng.standard_normal((n2, 1)) + 1e-4 * rng.standard_normal((m2, 1)))
+    for kind, s in (("gaussian", 64), ("srht", 128), ("countsketch", 1024)):
+        S2 = nsk.SketchOperator.draw(kind, s, m2, 8)
+        L = _lib.load()
+        X = np.empty((n2, 1), order="F")
+        Vk = np.empty((n2 + 1, 1), order="F")
+        sg = np.empty(n2 + 1)
+        info = np.zeros(4)
+        _lib.check(L.nsk_tls_solve_sketched_host(S2.handle, 0, m2, n2, 1, A2.ctypes.data_as(ctypes.c_void_p), m2,
+                                                 b2.ctypes.data_as(ctypes.c_void_p), m2, 1e12, 1,
+                                                 X.ctypes.data_as(ctypes.c_void_p), n2,
+                                                 Vk.ctypes.data_as(ctypes.c_void_p), n2 + 1,
+                                                 sg.ctypes.data_as(ctypes.c_void_p),
+                                                 info.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        ref = nsk.tls_solve_sketched(dev(A2), dev(b2), S2, allow_marginal=True)
+        assert np.max(np.abs(sg - host(ref.augmented_singular_values))) <= 1e-12 * sg[0], kind
+        assert rel(X, host(ref.X)) <= 1e-10, kind
