@@ -267,7 +267,9 @@ int nsk_solve_k_sharded_host(const nsk_operator* op, int scalar, int64_t row0, i
  * comes from a library-private stream-ordered pool per device, so it never
  * holds on to the default pool other libraries (PyTorch) allocate from.  Freed
  * blocks stay mapped for the next call; this returns them to the device
- * (synchronises the current device first). */
+ * (synchronises the current device first) and frees the pinned host buffers of
+ * the host-buffer entry points (the pageable-input staging ring and the
+ * CountSketch schedule scratch), which the next such call allocates again. */
 int nsk_release_scratch(void);
 
 /* ---- instrumentation (bench.py; no effect on results) ------------------- */

@@ -76,11 +76,23 @@ struct Tile {
 
 }  // namespace
 
+namespace {
+struct PinnedScratch {
+  std::mutex mu;
+  void* buf = nullptr;
+  size_t have = 0;
+};
+PinnedScratch& pinned_state() {
+  static PinnedScratch p;
+  return p;
+}
+}  // namespace
+
 std::unique_lock<std::mutex> pinned_scratch(size_t bytes, void** out) {
-  static std::mutex mu;
-  static void* buf = nullptr;
-  static size_t have = 0;
-  std::unique_lock<std::mutex> lock(mu);
+  PinnedScratch& ps = pinned_state();
+  void*& buf = ps.buf;
+  size_t& have = ps.have;
+  std::unique_lock<std::mutex> lock(ps.mu);
   *out = nullptr;
   if (bytes > have) {
     if (buf) cudaFreeHost(buf);
@@ -95,6 +107,22 @@ std::unique_lock<std::mutex> pinned_scratch(size_t bytes, void** out) {
   }
   *out = buf;
   return lock;
+}
+
+// Frees the process-wide pinned host buffers (staging ring, schedule scratch) when no transfer uses
+// them; the next host-buffer call allocates them again.
+void release_pinned_host() {
+  {
+    Staging& stg = staging();
+    std::lock_guard<std::mutex> lock(stg.mu);
+    if (stg.buf) cudaFreeHost(stg.buf);
+    stg.buf = nullptr;
+  }
+  PinnedScratch& ps = pinned_state();
+  std::lock_guard<std::mutex> lock(ps.mu);
+  if (ps.buf) cudaFreeHost(ps.buf);
+  ps.buf = nullptr;
+  ps.have = 0;
 }
 
 cudaStream_t copy_stream() {

@@ -82,6 +82,7 @@ int nsk_release_scratch(void) {
   if (!pool) return nsk::fail(nsk::ECUDA, "no scratch pool on this device");
   if (cudaError_t e = cudaDeviceSynchronize()) return nsk::cuda_fail(e, "release scratch");
   if (cudaError_t e = cudaMemPoolTrimTo(pool, 0)) return nsk::cuda_fail(e, "release scratch");
+  nsk::release_pinned_host();
   return nsk::OK;
 }
 

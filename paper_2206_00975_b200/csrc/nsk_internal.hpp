@@ -60,6 +60,7 @@ int build_cs_schedule_into(const uint32_t* table, int64_t ntiles, int T, int64_t
 // Process-wide pinned host scratch (grown on demand, kept): the CountSketch table readback and schedule
 // upload go through it at DMA speed.  Callers hold the returned lock while they use the buffer.
 std::unique_lock<std::mutex> pinned_scratch(size_t bytes, void** out);
+void release_pinned_host();
 // Whether the owner kernel applies (bins fit 4 registers per thread, s large
 // enough that ~4 rows per lane per tile spread over distinct owners, at least
 // one full tile; NSK_CS_MODE=stream|tma forces the older kernels).

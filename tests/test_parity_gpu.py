@@ -684,6 +684,10 @@ def test_tls_complex_many_rhs_and_release(nsk, oracle):
     with pytest.raises(ValueError):
         nsk.tls_solve_sketched(dev(np.hstack([A, A[:, :1]])), dev(np.hstack([B, B[:, :5]])), S)
     _lib.check(_lib.load().nsk_release_scratch())
+    # the host-buffer path reallocates what the release freed (pageable input > 4 MiB: staging ring)
+    A2 = np.asfortranarray(rng.standard_normal((1 << 16, 12)))
+    S2 = nsk.SketchOperator.draw("srht", 64, 1 << 16, 3)
+    assert rel(np.asarray(nsk.apply(S2, A2).data), oracle.apply(oracle.draw("srht", 64, 1 << 16, 3), A2)) <= SA_TOL
 
 
 @pytest.mark.parametrize("k", [2, 7, 24])
