@@ -6,9 +6,10 @@
 // driver at ~11 GB/s on the B200 hosts; registering the buffer
 // (cudaHostRegister) costs ~0.25 s per 2 GiB (tools/micro/h2d_paths.cu).  So a
 // pageable source is streamed through a ring of 16 pinned 16 MiB slots: 8 host
-// threads pack tiles of the matrix into free slots while the copy engine DMAs
-// the filled ones (~46 GB/s for a 2 GiB matrix, against 55.6 GB/s from a
-// pinned source; ring / slot / thread counts swept on the B200 host).  A pinned source (cudaHostAlloc / cudaHostRegister memory) is
+// threads pack tiles of the matrix into free slots with streaming stores while
+// the copy engine DMAs the filled ones (~51 GB/s for a 2 GiB matrix, against
+// 55.6 GB/s from a pinned source and ~42 GB/s with ordinary memcpy stores;
+// ring / slot / thread counts swept on the B200 host).  A pinned source (cudaHostAlloc / cudaHostRegister memory) is
 // DMAed directly.  Either way the matrix moves in row chunks and the compute
 // stream waits per chunk, so the caller can sketch chunk c while chunk c + 1
 // is in flight.  On the device the chunks are laid out chunk-major: chunk c
@@ -18,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <emmintrin.h>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -53,6 +55,40 @@ struct Staging {
   std::mutex mu;  // one staged transfer at a time per process
   char* buf = nullptr;
 };
+
+// Copy into the pinned ring with streaming (non-temporal) stores: the slot is only read back by the
+// copy engine, so allocating its lines in the CPU caches (and reading them first, for ordinary stores)
+// would only add host memory traffic.  Head and tail up to a 16-byte boundary go through memcpy.
+void copy_stream_nt(char* dst, const char* src, size_t n) {
+  size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+  if (head > n) head = n;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  const size_t blocks = n / 64;
+  for (size_t b = 0; b < blocks; ++b) {
+    const __m128i x0 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src));
+    const __m128i x1 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 16));
+    const __m128i x2 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 32));
+    const __m128i x3 = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst), x0);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 16), x1);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 32), x2);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 48), x3);
+    src += 64;
+    dst += 64;
+  }
+  std::memcpy(dst, src, n - blocks * 64);
+}
+
+bool stage_nt() {  // NSK_STAGE_NT=0: plain memcpy (A/B)
+  static const bool v = [] {
+    const char* e = std::getenv("NSK_STAGE_NT");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 // Host threads packing the ring (NSK_STAGE_THREADS overrides; default 8, measured best of 4/8/16).
 int stage_threads() {
@@ -209,6 +245,7 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
   for (int s = 0; s < RING; ++s) owner[s].store(static_cast<size_t>(s), std::memory_order_relaxed);
   std::atomic<size_t> next{0};
   std::atomic<bool> abort{false};
+  const bool nt = stage_nt();
   const int nthreads = static_cast<int>(std::min<size_t>(
       std::min<unsigned>(static_cast<unsigned>(stage_threads()), std::max(1u, std::thread::hardware_concurrency())), T));
   std::vector<std::thread> workers;
@@ -225,8 +262,13 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
         const Tile& tl = tiles[t];
         char* dst = stg.buf + s * SLOT;
         const size_t seg = static_cast<size_t>(tl.nr) * elem;
-        for (int64_t c = 0; c < tl.nc; ++c)
-          std::memcpy(dst + c * seg, A + (tl.r0 + (tl.c0 + c) * lda) * elem, seg);
+        for (int64_t c = 0; c < tl.nc; ++c) {
+          if (nt)
+            copy_stream_nt(dst + c * seg, A + (tl.r0 + (tl.c0 + c) * lda) * elem, seg);
+          else
+            std::memcpy(dst + c * seg, A + (tl.r0 + (tl.c0 + c) * lda) * elem, seg);
+        }
+        if (nt) _mm_sfence();  // the streaming stores are visible before the slot is marked filled
         filled[t].store(1, std::memory_order_release);
       }
     });
