@@ -14,10 +14,13 @@
 //    W_{4N}^{4n+1} = W^n w.  The remaining pre-twiddle w^{P k2} = W_{4L}^{k2}
 //    with k2 = a + 32 b splits into W_128^b (a compile-time constant of the
 //    register holding row b) and W_4096^a, which merges with the inter-pass
-//    twiddle into W_4096^{a (4k + 1)} (a 4096-entry shared table);
+//    twiddle into W_4096^{a (4k + 1)} (a [k][a] shared table of 1024 entries);
 //  * a lane (sequence i, row class a) loads its main elements
 //    A[K + i + P (a + 32 b)] and mirror elements A[N - (K + i + P k2)] straight
-//    into the FFT registers (two 8-byte loads per b, 64-byte row segments),
+//    into the FFT registers (two 8-byte loads per b, 64-byte row segments; the
+//    mirror set [P-K-7, P-K] straddles two aligned blocks, so lane 0 reads the
+//    aligned block's first element P-K-8 for the next tile and takes its own
+//    P-K from a shared-memory carry written one tile earlier),
 //    the next tile's loads land during the sampled stage, an L2 prefetch runs
 //    one tile further ahead; signs come as one 64-bit negate mask per lane;
 //  * the sampled stage is one complex Horner chain per slot (v is real:
@@ -42,7 +45,7 @@ constexpr int SW = 8;          // warps = sequences per tile
 constexpr int ST = 32 * SW;    // threads
 constexpr int SNQ = 1024 / ST; // output slots per thread
 constexpr int SANCH = 16;      // exact twiddles every SANCH tiles
-constexpr int STW = 4096;      // W_4096 table
+constexpr int STW = 1024;      // [k][a] table of W_4096^{a (4k+1)}
 static_assert(SNQ == 4, "the next tile loads in SNQ parts of 8 rows");
 
 struct DStreamParams {
@@ -171,14 +174,16 @@ template <int PF>
 __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
   extern __shared__ __align__(16) double2 sm2[];
   double2* U = sm2;              // [SL][SW], sequence i of row r at column i ^ (r & 7)
-  double2* tw = U + SL * SW;     // W_4096^j
+  double2* tw = U + SL * SW;     // [k][a]: W_4096^{a (4k+1)} (a warp's 4 row classes: one wavefront)
   double2* STP = tw + STW;       // [2][SNQ][ST]: W_4N^{4n+1} (one column), its 8th power (one tile)
+  double* CARRY = reinterpret_cast<double*>(STP + 2 * SNQ * ST);  // [b][a]: sequence-0 mirror carried one tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int li = lane & 7, a = 4 * warp + (lane >> 3);
   const int64_t N = p.N, P = p.P;
   const uint64_t N4 = 4 * static_cast<uint64_t>(N);
 
-  for (int k = threadIdx.x; k < STW; k += ST) tw[k] = unit_phase(static_cast<uint64_t>(k), 2.0 / STW);
+  for (int e = threadIdx.x; e < STW; e += ST)
+    tw[e] = unit_phase(static_cast<uint64_t>((e & 31) * (4 * (e >> 5) + 1)), 2.0 / 4096);
   double acc[SNQ];
   double2 base[SNQ];
   int bin[SNQ];
@@ -205,8 +210,9 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
   double2 x[32];
   uint64_t sw;
   // registers <- tile TT of column cc (regular tiles: setup + four parts of
-  // eight rows b); mirror loads keep normal L2 priority: the mirror block of a
-  // row ends one element into the block the previous tile of the column read.
+  // eight rows b); main and mirror loads are aligned 64-byte blocks (normal
+  // L2 priority: the other half of each 128-byte line is the neighbouring
+  // tile's), sequence 0's mirror is carried one tile through CARRY.
   const double* mp = nullptr;
   const double* rp = nullptr;
   int64_t rs = 0;
@@ -225,14 +231,17 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
     const double* col = p.A + cc * p.lda;
     const int64_t jm0 = 8 * (TT - 1) + li + P * a;
     mp = col + jm0;
-    // mirror of element b: N - jm0 - 32 P b (row jm0 = 0 has none: read a valid dummy)
-    rp = jm0 > 0 ? col + (N - jm0) : col;
-    rs = jm0 > 0 ? 32 * P : 0;
+    // mirror of element b: N - jm0 - 32 P b.  Lane 0 reads N - jm0 - 8 - 32 P b instead, the
+    // first element of the 64-byte-aligned block [P-K-8, P-K) of the row, which is the NEXT
+    // tile's sequence-0 mirror; its own arrives through CARRY from the previous tile's block.
+    // Every mirror block is then read once, aligned (was 1.22x the algorithmic DRAM bytes).
+    rp = col + (N - jm0 - (li == 0 ? 8 : 0));
+    rs = 32 * P;
     sw = __ldg(p.sgn + (TT * 32 + a) * 8 + li);
   };
   auto issue_part = [&](int part) {
 #pragma unroll
-    for (int b = 8 * part; b < 8 * part + 8; ++b) x[b] = make_double2(__ldcs(mp + 32 * P * b), __ldcg(rp - rs * b));
+    for (int b = 8 * part; b < 8 * part + 8; ++b) x[b] = make_double2(__ldcg(mp + 32 * P * b), __ldcg(rp - rs * b));
   };
   auto prefetch = [&](int64_t cc, int64_t TT) {  // L2 <- main and mirror row segments of a regular tile
     if (!PF || TT == 0) return;
@@ -251,6 +260,12 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
       ++cc;
     }
   };
+  if (T >= 2 && li == 0) {  // chunk starts inside a column: the first tile's carry is read directly
+    const double* col = p.A + c * p.lda;
+    const int64_t jm0 = 8 * (T - 1) + P * a;
+#pragma unroll 8
+    for (int b = 0; b < 32; ++b) CARRY[32 * b + a] = __ldcg(col + (N - jm0 - 32 * P * b));
+  }
   if (T == 0) {
     issue_special(c);
   } else {
@@ -269,6 +284,19 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
     const bool special = T == 0;
     // ---- pass 1: signs, weights, pre-twiddle W_128^b, 32-point DFT over b, twiddle W_4096^{a(4k+1)}
     {
+      if (!special && li == 0) {  // sequence 0: swap the carried mirror in, keep the next tile's
+        if (T == 1) {
+#pragma unroll
+          for (int b = 0; b < 32; ++b) CARRY[32 * b + a] = x[b].y;
+        } else {
+#pragma unroll
+          for (int b = 0; b < 32; ++b) {
+            const double t = CARRY[32 * b + a];
+            CARRY[32 * b + a] = x[b].y;
+            x[b].y = t;
+          }
+        }
+      }
       const uint32_t lo = static_cast<uint32_t>(sw), hi = static_cast<uint32_t>(sw >> 32);
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
@@ -293,7 +321,7 @@ __global__ void __launch_bounds__(ST, 1) srdct_stream_kernel(DStreamParams p) {
     }
     dft32f(x);
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = cmul(x[k], tw[a * (4 * k + 1)]);
+    for (int k = 0; k < 32; ++k) x[k] = cmul(x[k], tw[32 * k + a]);
     __syncthreads();  // previous tile's sampled stage has read U
 #pragma unroll
     for (int k = 0; k < 32; ++k) U[(32 * a + k) * SW + (li ^ (k & 7))] = x[k];
@@ -423,7 +451,7 @@ int srdct_stream_apply(const Operator& op, const RowMap& rows, int64_t n, const 
   const int64_t chunk = (total + G - 1) / G;
   G = (total + chunk - 1) / chunk;
   const int64_t jmax = chunk / tiles + 2;
-  const size_t smem = sizeof(double2) * (SL * SW + STW + 2 * SNQ * ST);
+  const size_t smem = sizeof(double2) * (SL * SW + STW + 2 * SNQ * ST) + sizeof(double) * 32 * 32;
   const char* pfe = std::getenv("NSK_STREAM_PF");
   auto kern = pfe && !std::atoi(pfe) ? srdct_stream_kernel<0> : srdct_stream_kernel<1>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
