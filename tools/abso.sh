@@ -1,0 +1,13 @@
+#!/bin/bash
+# usage (inside gpurun): tools/abso.sh <kind> <so-dir>  -- bench <kind> with each prebuilt libnullsketch_b200.so under <so-dir>/*/
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+LIB=paper_2206_00975_b200/libnullsketch_b200.so
+cp $LIB /tmp/orig.so
+for d in $2/*/; do
+  v=$(basename $d)
+  cp $d/libnullsketch_b200.so $LIB
+  timeout 300 python bench.py --kind $1 --steps 20 --warmup 5 --e2e-steps 1 --no-cpu > gpurun_out/abso_$v.log 2>&1
+  echo "$v: $(tail -1 gpurun_out/abso_$v.log | timeout 10 python tools/bsum.py)"
+done
+cp /tmp/orig.so $LIB
