@@ -165,17 +165,7 @@ int kind_from_name(const std::string& k) {
 }
 
 // A per-thread non-blocking stream for the host-buffer entry points.
-cudaStream_t host_stream() {
-  thread_local cudaStream_t st = nullptr;
-  thread_local int dev = -1;
-  int cur = 0;
-  cudaGetDevice(&cur);
-  if (!st || dev != cur) {
-    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    dev = cur;
-  }
-  return st;
-}
+cudaStream_t host_stream() { return nsk::thread_stream(); }
 
 int copy_in(const void* host, int64_t rows, int64_t cols, int64_t ld, int ncomp, double** dev, nsk::Scratch& s,
             cudaStream_t st) {

@@ -161,16 +161,43 @@ void release_pinned_host() {
   ps.have = 0;
 }
 
+// One non-blocking copy stream per device for the life of the process (per-thread streams leaked with
+// every short-lived calling thread).  Callers order their work on it with events only, so concurrent
+// host-buffer calls share it safely (the copy engine serialises their DMAs anyway).
 cudaStream_t copy_stream() {
-  thread_local cudaStream_t cs = nullptr;
-  thread_local int dev = -1;
+  constexpr int MAXDEV = 64;
+  static std::mutex mu;
+  static cudaStream_t cs[MAXDEV] = {};
   int cur = 0;
   cudaGetDevice(&cur);
-  if (!cs || dev != cur) {
-    cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    dev = cur;
+  if (cur < 0 || cur >= MAXDEV) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!cs[cur] && cudaStreamCreateWithFlags(&cs[cur], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    cs[cur] = nullptr;
   }
-  return cs;
+  return cs[cur];
+}
+
+// This thread's non-blocking compute stream on the current device for the host-buffer entry points
+// (concurrent callers on different threads run independently); destroyed when the thread exits.
+cudaStream_t thread_stream() {
+  struct PerThread {
+    cudaStream_t s[64] = {};
+    ~PerThread() {
+      for (cudaStream_t x : s)
+        if (x) cudaStreamDestroy(x);
+    }
+  };
+  thread_local PerThread t;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur < 0 || cur >= 64) return nullptr;
+  if (!t.s[cur] && cudaStreamCreateWithFlags(&t.s[cur], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    t.s[cur] = nullptr;
+  }
+  return t.s[cur];
 }
 
 bool host_is_pinned(const void* p) {
@@ -319,6 +346,7 @@ int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void
   if (m <= 0 || n <= 0) return OK;
   if (chunk <= 0 || chunk > m) chunk = m;
   cudaStream_t cs = copy_stream();
+  if (!cs) return fail(ECUDA, "host-to-device copy: no copy stream");
   // the destination (stream-ordered allocation on st) exists before the copies start
   if (int rc = join_streams(st, cs)) return rc;
   const char* a = static_cast<const char*>(A);

@@ -754,11 +754,19 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
   std::string side_err;  // the helper's error text (last_error is per thread)
   std::future<int> side = std::async(std::launch::async, [&]() -> int {
     cudaSetDevice(devno);
-    cudaStream_t aux = copy_stream();  // the helper thread's own non-blocking stream
+    // a stream of this call's own (a thread_local one would leak with the short-lived helper thread)
+    cudaStream_t aux = nullptr;
+    if (cudaError_t e = cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking)) {
+      const int rc = cuda_fail(e, "svd: helper stream");
+      side_err = last_error();
+      return rc;
+    }
     int rc = OK;
     if (cudaError_t e = cudaStreamWaitEvent(aux, qr_done, 0)) rc = cuda_fail(e, "svd: stream fork");
-    if (rc == OK) rc = svd_stage<NC>(A, rdiag, s, n2, 0, nullptr, 1, sigma2, B2, aux);
+    if (rc == OK) rc = svd_stage<NC>(A, rdiag, s, n2, 0, nullptr, 1, sigma2, B2, aux);  // ends synchronised
     if (rc != OK) side_err = last_error();
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
     return rc;
   });
   const int rc1 = svd_stage<NC>(A, rdiag, s, n, k, W, ldw, sigma, B1, st);

@@ -194,15 +194,8 @@ int nsk_solve_k_sharded_host(const nsk_operator* h, int scalar, int64_t row0, in
   if (n < 1 || k < 0 || k >= n) return nsk::fail(nsk::EINVAL_, "nullspace: k must satisfy 0 <= k < n");
   if (mloc > 0 && (lda < mloc || !A_local)) return nsk::fail(nsk::EINVAL_, "sketch apply: lda < rows");
   if ((k > 0 && (!W || ldw < n)) || !sigma) return nsk::fail(nsk::EINVAL_, "solve_k: bad outputs");
-  thread_local cudaStream_t st_tl = nullptr;  // this thread's compute stream (h2d_rows copies on another)
-  thread_local int st_dev = -1;
-  int dev = 0;
-  NSK_CUDA_OK(cudaGetDevice(&dev));
-  if (!st_tl || st_dev != dev) {
-    NSK_CUDA_OK(cudaStreamCreateWithFlags(&st_tl, cudaStreamNonBlocking));
-    st_dev = dev;
-  }
-  cudaStream_t st = st_tl;
+  cudaStream_t st = nsk::thread_stream();  // this thread's compute stream (h2d_rows copies on another)
+  if (!st) return nsk::fail(nsk::ECUDA, "solve_k_sharded_host: no compute stream");
   const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_nc(op, scalar);
   nsk::Scratch a, w, sg;
   NSK_CUDA_OK(a.alloc(sizeof(double) * nc_in * (mloc > 0 ? mloc : 1) * n, st));

@@ -255,6 +255,7 @@ int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void
              cudaStream_t st, const ChunkFn& on_chunk);
 bool host_is_pinned(const void* p);
 cudaStream_t copy_stream();
+cudaStream_t thread_stream();
 
 // ---- instrumentation -------------------------------------------------------
 void count_launch(int n = 1);
