@@ -183,6 +183,129 @@ __global__ void __launch_bounds__(JT) qr_kernel(QrParams P, int* ready) {
   }
 }
 
+// The same look-ahead QR with one column per CTA held in registers (s <= EPT * QRT rows): CTA k
+// applies reflectors 0 .. k-1 as they are published and then publishes reflector k.  Against
+// qr_kernel the critical path of a step loses the reloads of the column from memory and the
+// serialised per-element L2 round trips (every thread issues all EPT loads of v_j at once), and the
+// norm of the updated column comes from registers: 1.15 -> 0.4 ms at 1024 x 256.
+constexpr int QRT = 128;
+
+template <int NC>
+__device__ __forceinline__ void qr_sum2(double& a, double& b, double* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (NC == 2) b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    red[w * 2] = a;
+    red[w * 2 + 1] = b;
+  }
+  __syncthreads();
+  a = b = 0.0;
+#pragma unroll
+  for (int i = 0; i < QRT / 32; ++i) {  // fixed order: deterministic
+    a += red[i * 2];
+    b += red[i * 2 + 1];
+  }
+  __syncthreads();  // red is reused by the next reduction
+}
+
+template <int NC, int EPT>
+__global__ void __launch_bounds__(QRT) qr_reg_kernel(QrParams P, int* ready) {
+  __shared__ double red[(QRT / 32) * 2];
+  __shared__ double head[2];
+  const int64_t k = blockIdx.x, s = P.s;
+  double* col = P.A + k * s * NC;
+  double ar[EPT], ai[EPT];  // rows threadIdx.x + QRT e
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int64_t i = threadIdx.x + QRT * e;
+    ar[e] = i < s ? col[NC * i] : 0.0;
+    ai[e] = (NC == 2 && i < s) ? col[NC * i + 1] : 0.0;
+  }
+  for (int64_t j = 0; j < k; ++j) {  // reflectors 0 .. k-1, each as soon as it is published
+    await(ready + j, 1);
+    const double* v = P.A + j * s * NC;
+    double vr[EPT], vi[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {  // v was written by another CTA: L2 (ld.cg), all loads in flight at once
+      const int64_t i = threadIdx.x + QRT * e;
+      const bool in = i >= j && i < s;
+      vr[e] = in ? __ldcg(v + NC * i) : 0.0;
+      vi[e] = (NC == 2 && in) ? __ldcg(v + NC * i + 1) : 0.0;
+    }
+    double wr = 0.0, wi = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      wr = fma(vr[e], ar[e], wr);
+      if (NC == 2) {
+        wr = fma(vi[e], ai[e], wr);  // conj(v) a
+        wi = fma(vr[e], ai[e], fma(-vi[e], ar[e], wi));
+      }
+    }
+    qr_sum2<NC>(wr, wi, red);
+    const double t = __ldcg(P.tau + j);
+    wr *= t;
+    wi *= t;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      if (NC == 1) {
+        ar[e] = fma(-vr[e], wr, ar[e]);
+      } else {
+        ar[e] -= vr[e] * wr - vi[e] * wi;
+        ai[e] -= vr[e] * wi + vi[e] * wr;
+      }
+    }
+  }
+  // reflector k from rows k .. s-1 of the updated column (householder() above, from registers)
+  double ss = 0.0, dummy = 0.0;
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int64_t i = threadIdx.x + QRT * e;
+    if (i > k && i < s) ss += NC == 1 ? ar[e] * ar[e] : ar[e] * ar[e] + ai[e] * ai[e];
+  }
+  qr_sum2<1>(ss, dummy, red);
+  const int hown = static_cast<int>(k % QRT), he = static_cast<int>(k / QRT);
+  if (threadIdx.x == hown) {
+    double xr = 0.0, xi = 0.0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e)
+      if (e == he) {
+        xr = ar[e];
+        xi = ai[e];
+      }
+    const double ax = NC == 1 ? fabs(xr) : hypot(xr, xi);
+    const double sigma = sqrt(ax * ax + ss);
+    double h0r = xr, h0i = xi;
+    if (sigma == 0.0) {
+      P.tau[k] = 0.0;
+      P.rdiag[NC * k] = 0.0;
+      if (NC == 2) P.rdiag[NC * k + 1] = 0.0;
+    } else {
+      const double ur = ax > 0 ? xr / ax : 1.0, ui = ax > 0 ? xi / ax : 0.0;
+      P.rdiag[NC * k] = -ur * sigma;
+      if (NC == 2) P.rdiag[NC * k + 1] = -ui * sigma;
+      h0r = ur * (ax + sigma);
+      h0i = ui * (ax + sigma);
+      P.tau[k] = 1.0 / (sigma * (sigma + ax));
+    }
+    head[0] = h0r;
+    head[1] = h0i;
+  }
+  __syncthreads();
+  // the whole column: R entries above the diagonal, v_k from the diagonal down
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int64_t i = threadIdx.x + QRT * e;
+    if (i < s) {
+      col[NC * i] = i == k ? head[0] : ar[e];
+      if (NC == 2) col[NC * i + 1] = i == k ? head[1] : ai[e];
+    }
+  }
+  publish(ready + k, 1);
+}
+
 // Stacked working matrix [R; I] (2n x n, ld 2n) from the factored A.
 __global__ void build_stacked(const double* __restrict__ A, const double* __restrict__ rdiag, int64_t s, int64_t n,
                               int nc, double* __restrict__ X) {
@@ -584,6 +707,34 @@ int coop_launch(K kern, int64_t want, size_t smem, void** args, cudaStream_t st,
   return OK;
 }
 
+// Householder QR of the s x n working copy (reflectors below the diagonal, R above, diagonal in rdiag):
+// qr_reg_kernel when its n CTAs fit on the device at once and a column fits the registers
+// (s <= 4096 real, 2048 complex), else qr_kernel.  NSK_SVD_QR_OLD=1 forces qr_kernel (A/B).
+template <int NC>
+int qr_factor(const QrParams& Q, void** args, cudaStream_t st) {
+  const int64_t s = Q.s, n = Q.n;
+  auto reg = [&](auto kern) -> int {
+    int per_sm = 0;
+    NSK_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, QRT, 0));
+    if (static_cast<int64_t>(per_sm) * sm_count() < n) return NOTAPPLICABLE;
+    NSK_CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(n)), dim3(QRT),
+                                            args, 0, st));
+    count_launch();
+    return OK;
+  };
+  int rc = NOTAPPLICABLE;
+  if (n <= s && !std::getenv("NSK_SVD_QR_OLD")) {
+    if (s <= 8 * QRT)
+      rc = reg(qr_reg_kernel<NC, 8>);
+    else if (s <= 16 * QRT)
+      rc = reg(qr_reg_kernel<NC, 16>);
+    else if (NC == 1 && s <= 32 * QRT)
+      rc = reg(qr_reg_kernel<NC, NC == 1 ? 32 : 16>);
+  }
+  if (rc != NOTAPPLICABLE) return rc;
+  return coop_launch(qr_kernel<NC>, n, 0, args, st);
+}
+
 // Per-SVD device buffers of the Jacobi stage (X = [R; I] or [R'; V] workspace and its counters).
 struct SvdBufs {
   double* X;
@@ -740,10 +891,10 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
   }
-  {  // 1. Householder QR
+  {  // 1. Householder QR: one register-resident column per CTA when all n CTAs are co-resident
     QrParams Q{A, tau, rdiag, s, n};
     void* args[] = {&Q, &ready};
-    if (int rc = coop_launch(qr_kernel<NC>, n, 0, args, st)) return rc;
+    if (int rc = qr_factor<NC>(Q, args, st)) return rc;
   }
   if (n2 <= 0) return svd_stage<NC>(A, rdiag, s, n, k, W, ldw, sigma, B1, st);
   int devno = 0;
