@@ -204,7 +204,9 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
     nsk::RowMap rows{0, 1, m};
     return dispatch_apply2(op, nc_in, rows, n, dA, m, kb, dB, m, SA, op.s, st);
   }
-  NSK_CUDA_OK(a_buf.alloc(elem * m * n, st));
+  // each row chunk lands as one rows x (n + kb) block: A's rows, then (copied on the device) the same
+  // rows of B, so the chunk apply sees a single matrix [A | B] (the Gaussian kernel's TMA path)
+  NSK_CUDA_OK(a_buf.alloc(elem * m * ntot, st));
   dA = a_buf.as<double>();
   const int64_t nchunks = (m + chunk - 1) / chunk;
   nsk::Scratch parts;
@@ -230,8 +232,14 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
     cudaEventDestroy(c.landed);
     if (e != cudaSuccess) return nsk::cuda_fail(e, "chunk wait");
     nsk::RowMap shard{c.r0, 1, c.rows};  // chunk-major device copy: this chunk's block, ld = its rows
-    return dispatch_main2(op, nc_in, shard, n, dA + c.r0 * n * nc_in, c.rows, kb, dB ? dB + c.r0 * nc_in : nullptr, m,
-                          parts.as<double>() + (c.r0 / chunk) * psz, op.s, st);
+    double* blk = dA + c.r0 * ntot * nc_in;
+    if (kb > 0) {
+      if (cudaError_t e2 = cudaMemcpy2DAsync(blk + c.rows * n * nc_in, elem * c.rows, dB + c.r0 * nc_in, elem * m,
+                                             elem * c.rows, kb, cudaMemcpyDeviceToDevice, st))
+        return nsk::cuda_fail(e2, "chunk of B");
+    }
+    return dispatch_main2(op, nc_in, shard, ntot, blk, c.rows, 0, nullptr, m, parts.as<double>() + (c.r0 / chunk) * psz,
+                          op.s, st);
   };
   auto flush = [&]() {
     have_tables = true;
@@ -261,7 +269,7 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
     }
     return run_chunk(c);
   };
-  int rc = nsk::h2d_rows(A, m, n, lda, elem, dA, chunk, st, sketch_chunk);
+  int rc = nsk::h2d_rows(A, m, n, lda, elem, dA, chunk, st, sketch_chunk, ntot);
   if (!have_tables) {
     const int rf = flush();  // also joins the helper thread on the error path
     if (rc == nsk::OK) rc = rf;

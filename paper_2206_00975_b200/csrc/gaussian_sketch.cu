@@ -20,6 +20,10 @@
 //     full/empty handshakes overlaps generation, loads and MMAs.
 //   * split-K over m: every CTA writes a partial tile; reduce_partials sums
 //     them in fixed order (bit-identical re-runs).
+#include <cuda.h>
+#include <cstring>
+#include <cudaTypedefs.h>
+
 #include "nsk_internal.hpp"
 
 namespace nsk {
@@ -49,6 +53,25 @@ struct Tile {
   static constexpr int STAGES = BN == 512 ? 3 : (BN == 256 ? 4 : 3);   // ring depth (<= 216 KiB)
   static constexpr int WGM = BM / 32;                                  // consumer warp grid rows
 };
+// A tile by TMA: boxes {BK = 16 rows, <= 256 columns} with the 128-byte swizzle, i.e. column c's 16
+// rows are one 128-byte line whose 16-byte pairs are XOR-permuted by c mod 8 (conflict-free m8n8k4
+// fragment loads); the cp.async path keeps the k4 layout.
+template <int BN, bool TMA> constexpr int box_w() { return TMA && BN > 256 ? 256 : BN; }
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ int k4(int x, int k, int X) { return (k >> 2) * (4 * X) + 4 * x + (k & 3); }
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -169,12 +192,17 @@ __device__ __forceinline__ void gen_g_tile(const GaussParams& p, double* sa, int
   }
 }
 
-template <int BN, int NCOMP, bool VEC16>
-__global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams p) {
+// TMA: the A tile of a stage comes in by cp.async.bulk.tensor (one producer thread, completion on the
+// stage's mbarrier) instead of 16 cp.async per producer thread -- the producers keep their issue slots
+// and registers for the Box-Muller work (real A without a second column block, mloc % 4 == 0).
+template <int BN, int NCOMP, bool VEC16, bool TMA>
+__global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams p,
+                                                                     const __grid_constant__ CUtensorMap tmA) {
   using T = Tile<BN>;
+  constexpr int BW = box_w<BN, TMA>();
   constexpr int TN = 64 / 8;  // 8-col MMA tiles per warp
   constexpr int TM = 32 / 8;  // 8-row MMA tiles per warp
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(1024) double smem[];
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * T::BM;
   const int64_t q0 = static_cast<int64_t>(blockIdx.y) * BN;
   const int64_t split = blockIdx.z;
@@ -183,8 +211,18 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
   if (kend > p.mloc) kend = p.mloc;
   const int64_t nchunks = kend > kbeg ? (kend - kbeg + T::BK - 1) / T::BK : 0;
 
+  uint64_t* full_mb = reinterpret_cast<uint64_t*>(smem + T::STAGES * T::STAGE);  // [STAGES] (TMA)
   if (threadIdx.x >= CONSUMERS) {
     if (PRODUCERS == 256) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_PRODUCER));
+    if constexpr (TMA) {
+      if (threadIdx.x == CONSUMERS) {
+        for (int s2 = 0; s2 < T::STAGES; ++s2)
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(full_mb + s2)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+      }
+      named_sync(15, PRODUCERS);  // barriers initialised before any producer waits on them
+    }
     // ---------------- producers ----------------
     // Loads of LAG + 1 stages are in flight at once: stage c is issued (one
     // cp.async group) and its G tile generated while stages c-1 .. c-LAG are
@@ -204,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     const double* abase[PER];  // row-0 address of the slot's column ([A | B]), + r2
     uint32_t okmask = 0;
     const uint32_t soff0 = static_cast<uint32_t>(k4(pt / (T::BK / 2), (pt % (T::BK / 2)) * 2, BN));
-    if (NCOMP == 1 && VEC16) {
+    if (NCOMP == 1 && VEC16 && !TMA) {
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int cc = pt + PRODUCERS * i, colx = cc / (T::BK / 2), r2 = (cc % (T::BK / 2)) * 2;
@@ -220,7 +258,21 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         double* sa = smem + st * T::STAGE;
         double* sb = sa + T::BM * T::BK;
         const int64_t k0 = kbeg + c * T::BK;
-        if (NCOMP == 1 && VEC16 && k0 + T::BK <= p.mloc) {
+        if constexpr (TMA) {
+          if (pt == 0) {  // the whole A tile: BN / BW boxes {4 rows, BW columns, BK / 4 row groups}
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(full_mb + st)),
+                         "r"(static_cast<uint32_t>(sizeof(double) * BN * T::BK))
+                         : "memory");
+#pragma unroll
+            for (int h = 0; h < BN / BW; ++h)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                  "[%4];\n" ::"r"(smem_addr(sb + h * BW * T::BK)),
+                  "l"(&tmA), "r"(static_cast<int>(k0)), "r"(static_cast<int>(q0 + h * BW)),
+                  "r"(smem_addr(full_mb + st))
+                  : "memory");
+          }
+        } else if (NCOMP == 1 && VEC16 && k0 + T::BK <= p.mloc) {
 #pragma unroll
           for (int i = 0; i < PER; ++i) {
             const bool ok = (okmask >> i) & 1u;
@@ -229,14 +281,18 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         } else {
           load_a_tile<BN, NCOMP, VEC16>(p, sb, k0, q0, pt);
         }
-        cp_async_commit();
+        if constexpr (!TMA) cp_async_commit();
         gen_g_tile<BN>(p, sa, i0, k0, pt);
       }
       if (c >= LAG) {
-        if (c < nchunks)
+        if constexpr (TMA) {
+          const int64_t cl = c - LAG;  // its A tile has landed (use cl / STAGES of that stage's barrier)
+          mbar_wait(full_mb + cl % T::STAGES, static_cast<uint32_t>((cl / T::STAGES) & 1));
+        } else if (c < nchunks) {
           cp_async_wait_group<LAG>();
-        else
+        } else {
           cp_async_wait_all();
+        }
         named_arrive(1 + static_cast<int>((c - LAG) % T::STAGES), THREADS);  // stage c-LAG full
       }
     }
@@ -259,6 +315,9 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     // k4 layout: fragment (x = lane/4, k = lane%4) of k-step kk at (kk/4)*4X + 4x + k.
     const double* A_ = smem + st * T::STAGE + 4 * (wm * 32) + lane;
     const double* B_ = smem + st * T::STAGE + T::BM * T::BK + 4 * (wn * 64) + lane;
+    // TMA layout: element (k, col) at col * 16 + (((k >> 1) ^ (col & 7)) << 1 | (k & 1)); a fragment's
+    // column is wn * 64 + 8 b + lane / 4, so col & 7 = lane >> 2
+    const double* Bt = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * 64 + (lane >> 2));
 #pragma unroll
     for (int kk = 0; kk < T::BK; kk += 4) {
       double af[TM];
@@ -268,7 +327,14 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
       for (int h = 0; h < 2; ++h) {
         double bf[TN / 2];
 #pragma unroll
-        for (int b = 0; b < TN / 2; ++b) bf[b] = B_[kk * BN + (h * (TN / 2) + b) * 32];
+        for (int b = 0; b < TN / 2; ++b) {
+          if constexpr (TMA) {
+            const int kx = (((kk >> 1) + ((lane >> 1) & 1)) ^ (lane >> 2)) << 1 | (lane & 1);
+            bf[b] = Bt[(h * (TN / 2) + b) * 8 * 16 + kx];
+          } else {
+            bf[b] = B_[kk * BN + (h * (TN / 2) + b) * 32];
+          }
+        }
 #pragma unroll
         for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -312,25 +378,51 @@ __global__ void reduce_partials(const double* __restrict__ P, int64_t splits, in
   }
 }
 
-template <int BN, int NCOMP, bool VEC16>
-int launch(const GaussParams& p0, int64_t n_tiles_q, int64_t s_tiles, int64_t splits, cudaStream_t st) {
-  const size_t smem = sizeof(double) * Tile<BN>::STAGES * Tile<BN>::STAGE;
-  auto kern = gaussian_sketch_kernel<BN, NCOMP, VEC16>;
+template <int BN, int NCOMP, bool VEC16, bool TMA>
+int launch(const GaussParams& p0, const CUtensorMap& tm_a, int64_t n_tiles_q, int64_t s_tiles, int64_t splits,
+           cudaStream_t st) {
+  const size_t smem = sizeof(double) * Tile<BN>::STAGES * Tile<BN>::STAGE + sizeof(uint64_t) * Tile<BN>::STAGES;
+  auto kern = gaussian_sketch_kernel<BN, NCOMP, VEC16, TMA>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   dim3 grid(static_cast<unsigned>(s_tiles), static_cast<unsigned>(n_tiles_q), static_cast<unsigned>(splits));
   KernelTimer tm(st, "gaussian_sketch_kernel");
-  kern<<<grid, THREADS, smem, st>>>(p0);
+  kern<<<grid, THREADS, smem, st>>>(p0, tm_a);
   tm.stop();
   count_launch();
   NSK_CUDA_OK(cudaGetLastError());
   return OK;
 }
 
-template <int NCOMP, bool VEC16>
-int launch_bn(int BN, const GaussParams& p, int64_t q_tiles, int64_t s_tiles, int64_t splits, cudaStream_t st) {
-  return BN == 128 ? launch<128, NCOMP, VEC16>(p, q_tiles, s_tiles, splits, st)
-       : BN == 256 ? launch<256, NCOMP, VEC16>(p, q_tiles, s_tiles, splits, st)
-                   : launch<512, NCOMP, VEC16>(p, q_tiles, s_tiles, splits, st);
+template <int NCOMP, bool VEC16, bool TMA = false>
+int launch_bn(int BN, const GaussParams& p, const CUtensorMap& tm_a, int64_t q_tiles, int64_t s_tiles, int64_t splits,
+              cudaStream_t st) {
+  return BN == 128 ? launch<128, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st)
+       : BN == 256 ? launch<256, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st)
+                   : launch<512, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st);
+}
+
+// Tensor map of a real column-major A (mloc x nq, ld lda): a box {BK = 16 rows, BW columns} lands in
+// shared memory as [col][16 rows] with the 128-byte swizzle.  false when the driver entry point is
+// unavailable or the encode fails (the cp.async path runs instead).
+bool encode_a_map(const double* A, int64_t lda, int64_t mloc, int64_t nq, int BW, int BK, CUtensorMap* out) {
+  static PFN_cuTensorMapEncodeTiled encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<PFN_cuTensorMapEncodeTiled>(nullptr);
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(mloc), static_cast<cuuint64_t>(nq)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(BW)};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -395,9 +487,19 @@ int gaussian_apply_key2(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t
                 zmask, zoff};
   const bool vec16 = ncomp == 1 && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
                      (!B || ((ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0)));
-  int rc = ncomp == 2 ? launch_bn<2, false>(BN, p, q_tiles, s_tiles, splits, st)
-         : vec16     ? launch_bn<1, true>(BN, p, q_tiles, s_tiles, splits, st)
-                     : launch_bn<1, false>(BN, p, q_tiles, s_tiles, splits, st);
+  // TMA A tiles: real A without a second column block, whole 4-row groups, lda even, 16-byte aligned
+  CUtensorMap tm_a;
+  std::memset(&tm_a, 0, sizeof(tm_a));
+  const char* te = std::getenv("NSK_GAUSS_TMA");
+  // [A | B] stored back to back with one leading dimension (the usual sketched-TLS caller: one m x (n+k)
+  // buffer) is a single matrix to the tensor map
+  const bool one_matrix = !B || (ldb == lda && B == A + nqa * lda);
+  const bool tma = vec16 && one_matrix && BK == 16 && !(te && te[0] == '0') &&
+                   encode_a_map(A, lda, mloc, nq, BN > 256 ? 256 : BN, BK, &tm_a);
+  int rc = ncomp == 2 ? launch_bn<2, false>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
+         : tma       ? launch_bn<1, true, true>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
+         : vec16     ? launch_bn<1, true>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
+                     : launch_bn<1, false>(BN, p, tm_a, q_tiles, s_tiles, splits, st);
   if (rc != OK) return rc;
   const int64_t total = s * nq;
   const int threads = 256;

@@ -235,11 +235,12 @@ int chunk_landed(int64_t r0, int64_t rows, cudaStream_t cs, cudaStream_t st, con
 }
 
 int h2d_pinned(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, char* dA, int64_t chunk,
-               cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
+               int64_t dcols, cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
   for (int64_t r0 = 0; r0 < m; r0 += chunk) {
     const int64_t rows = std::min(chunk, m - r0);
-    // chunk-major destination: chunk c is its own rows x n column-major block (ld = rows) at row offset r0 * n
-    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * n * elem, elem * rows, A + r0 * elem, elem * lda, elem * rows, n,
+    // chunk-major destination: chunk c is its own rows x dcols column-major block (ld = rows) at row
+    // offset r0 * dcols, A in its first n columns
+    NSK_CUDA_OK(cudaMemcpy2DAsync(dA + r0 * dcols * elem, elem * rows, A + r0 * elem, elem * lda, elem * rows, n,
                                   cudaMemcpyHostToDevice, cs));
     if (int rc = chunk_landed(r0, rows, cs, st, on_chunk)) return rc;
   }
@@ -247,7 +248,7 @@ int h2d_pinned(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
 }
 
 int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, char* dA, int64_t chunk,
-               cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
+               int64_t dcols, cudaStream_t cs, cudaStream_t st, const ChunkFn& on_chunk) {
   Staging& stg = staging();
   std::lock_guard<std::mutex> lock(stg.mu);
   const int RING = ring_slots();
@@ -310,7 +311,7 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
     const Tile& tl = tiles[t];
     // chunk-major destination (see h2d_pinned): a tile spanning the chunk's rows is one contiguous run
     const int64_t cr0 = tl.r0 / chunk * chunk, crows = std::min(chunk, m - cr0);
-    char* dst = dA + (cr0 * n + (tl.r0 - cr0) + tl.c0 * crows) * elem;
+    char* dst = dA + (cr0 * dcols + (tl.r0 - cr0) + tl.c0 * crows) * elem;
     cudaError_t e = tl.nr == crows
                         ? cudaMemcpyAsync(dst, stg.buf + s * SLOT, elem * tl.nr * tl.nc, cudaMemcpyHostToDevice, cs)
                         : cudaMemcpy2DAsync(dst, elem * crows, stg.buf + s * SLOT, elem * tl.nr, elem * tl.nr, tl.nc,
@@ -342,9 +343,10 @@ int h2d_staged(const char* A, int64_t m, int64_t n, int64_t lda, size_t elem, ch
 }  // namespace
 
 int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void* dA, int64_t chunk,
-             cudaStream_t st, const ChunkFn& on_chunk) {
+             cudaStream_t st, const ChunkFn& on_chunk, int64_t dcols) {
   if (m <= 0 || n <= 0) return OK;
   if (chunk <= 0 || chunk > m) chunk = m;
+  if (dcols < n) dcols = n;
   cudaStream_t cs = copy_stream();
   if (!cs) return fail(ECUDA, "host-to-device copy: no copy stream");
   // the destination (stream-ordered allocation on st) exists before the copies start
@@ -352,8 +354,8 @@ int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void
   const char* a = static_cast<const char*>(A);
   char* d = static_cast<char*>(dA);
   const bool small = static_cast<double>(m) * static_cast<double>(n) * static_cast<double>(elem) < 4.0 * (1 << 20);
-  if (host_is_pinned(A) || small) return h2d_pinned(a, m, n, lda, elem, d, chunk, cs, st, on_chunk);
-  return h2d_staged(a, m, n, lda, elem, d, chunk, cs, st, on_chunk);
+  if (host_is_pinned(A) || small) return h2d_pinned(a, m, n, lda, elem, d, chunk, dcols, cs, st, on_chunk);
+  return h2d_staged(a, m, n, lda, elem, d, chunk, dcols, cs, st, on_chunk);
 }
 
 }  // namespace nsk

@@ -26,7 +26,7 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include <future>
+#include <mutex>
 #include <string>
 
 #include "nsk_internal.hpp"
@@ -759,42 +759,42 @@ SvdBufs svd_bufs_at(void* base, int64_t n, int nc) {
 }
 
 // Trailing k right singular vectors and all n singular values of the leading s x n block of the
-// QR'd matrix (R in the upper triangle of A, ld s, diagonal in rdiag): the Jacobi stage.
+// QR'd matrix (R in the upper triangle of A, ld s, diagonal in rdiag): the Jacobi stage.  launch()
+// only enqueues work on st (so two stages on two streams can be in flight from one host thread);
+// finish() reads the three host-visible flags and reruns on [R; I] when R was exactly singular.
 template <int NC>
-int svd_stage(const double* A, const double* rdiag, int64_t s, int64_t n, int64_t k, double* W, int64_t ldw,
-              double* sigma, SvdBufs B, cudaStream_t st) {
-  double* X = B.X;
-  double* norms = B.norms;
-  int* counter = B.counter;
-  int* bad = B.bad;
-  int* version = B.version;
-  {
+struct SvdStage {
+  const double* A;
+  const double* rdiag;
+  int64_t s, n, k;
+  double* W;
+  int64_t ldw;
+  double* sigma;
+  SvdBufs B;
+  cudaStream_t st;
+  double tol = 0.0;
+  int b = 16;
+  bool blocked = false;
+  int host[3] = {0, 0, 0};  // sweeps, non-finite flag, path (1: preconditioned, 0: [R; I], -1: rerun)
+  int flag = 0;
+
+  int stacked() {
     int64_t blocks = (2 * n * n * NC + 255) / 256;
     if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-    build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, X);
+    build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, B.X);
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
+    return OK;
   }
-  // Stopping rule n * eps: the computed |u_p^T u_q| of converged columns
-  // carries ~sqrt(n) * eps relative rounding noise, so the tighter
-  // sqrt(n) * eps of dgesvj can stall on 1e-10-graded spectra.
-  const double tol = static_cast<double>(n) * 2.220446049250313e-16;
-  // Block width: the rotations of a round are FP64-throughput bound on the SMs
-  // that hold a block pair, so spread them -- the widest b in {16, 8, 4, 2}
-  // that still leaves >= 32 block pairs (CTAs) -- and a block pair of [R; I]
-  // columns must fit in shared memory.  NSK_SVD_B overrides (tuning).
-  int b = 16;
-  while (b > 2 && n / b < 64) b >>= 1;
-  if (const char* e = std::getenv("NSK_SVD_B")) b = std::atoi(e) >= 1 && std::atoi(e) <= 16 ? std::atoi(e) : b;
-  while (b > 1 && sizeof(double) * 2 * b * 2 * n * NC > 200 * 1024) b >>= 1;
-  const bool blocked = sizeof(double) * 2 * b * 2 * n * NC <= 200 * 1024 && std::getenv("NSK_SVD_PAIRS") == nullptr;
-  int* degenerate = version;  // flag of the preconditioned path (version[] is zero here)
-  auto solve = [&](bool precondition, int host[3]) -> int {
+
+  int solve(bool precondition) {
+    double* X = B.X;
+    int* degenerate = B.version;  // flag of the preconditioned path (version[] is zero here)
     int crc = NOTAPPLICABLE;
-    if (n >= 2 && precondition) crc = cluster_svd_rt(NC, X, n, tol, counter, degenerate, st);  // 2a. QRCP + R'^H
+    if (n >= 2 && precondition) crc = cluster_svd_rt(NC, X, n, tol, B.counter, degenerate, st);  // 2a. QRCP + R'^H
     if (crc != OK && crc != NOTAPPLICABLE) return crc;
     host[2] = crc == OK;
-    if (crc != OK && n >= 2) crc = cluster_jacobi(NC, X, n, tol, counter, st);  // 2b. whole [R; I] in one cluster
+    if (crc != OK && n >= 2) crc = cluster_jacobi(NC, X, n, tol, B.counter, st);  // 2b. whole [R; I] in one cluster
     if (crc != OK && crc != NOTAPPLICABLE) return crc;
     if (crc == OK) {
     } else if (n >= 2 && blocked) {  // 2c. block one-sided Jacobi on [R; I] through L2
@@ -805,7 +805,7 @@ int svd_stage(const double* A, const double* rdiag, int64_t s, int64_t n, int64_
       P.B = (n + b - 1) / b;
       P.B += P.B & 1;
       P.tol = tol;
-      P.counter = counter;
+      P.counter = B.counter;
       void* args[] = {&P};
       if (int rc = coop_launch(block_jacobi_kernel<NC>, P.B / 2, sizeof(double) * 2 * b * 2 * n * NC, args, st, BJT))
         return rc;
@@ -815,53 +815,99 @@ int svd_stage(const double* A, const double* rdiag, int64_t s, int64_t n, int64_
       P.n = n;
       P.N = n + (n & 1);
       P.tol = tol;
-      P.counter = counter;
+      P.counter = B.counter;
       size_t smem = sizeof(double) * 2 * 2 * n * NC;
       P.use_smem = smem <= 160 * 1024;
       if (!P.use_smem) smem = 0;
+      int* version = B.version;
       void* args[] = {&P, &version};
       if (int rc = coop_launch(jacobi_kernel<NC>, P.N / 2, smem, args, st)) return rc;
     }
-    norms_kernel<NC><<<static_cast<unsigned>(n), JT, 0, st>>>(X, n, norms);
+    norms_kernel<NC><<<static_cast<unsigned>(n), JT, 0, st>>>(X, n, B.norms);
     NSK_CUDA_OK(cudaGetLastError());
-    NSK_CUDA_OK(cudaMemsetAsync(bad, 0, sizeof(int), st));
-    order_kernel<NC><<<1, 256, sizeof(int) * n, st>>>(X, n, k, W, ldw, sigma, norms, bad);
+    NSK_CUDA_OK(cudaMemsetAsync(B.bad, 0, sizeof(int), st));
+    order_kernel<NC><<<1, 256, sizeof(int) * n, st>>>(X, n, k, W, ldw, sigma, B.norms, B.bad);
     count_launch(2);
     NSK_CUDA_OK(cudaGetLastError());
-    // Convergence, NaN and degeneracy checks need host visibility of three ints.
-    int flag = 0;
-    NSK_CUDA_OK(cudaMemcpyAsync(&host[0], counter + MAX_SWEEPS, sizeof(int), cudaMemcpyDeviceToHost, st));
-    NSK_CUDA_OK(cudaMemcpyAsync(&host[1], bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-    if (host[2]) NSK_CUDA_OK(cudaMemcpyAsync(&flag, degenerate, sizeof(int), cudaMemcpyDeviceToHost, st));
+    return OK;
+  }
+
+  // Convergence, NaN and degeneracy checks need host visibility of three ints.
+  int collect() {
+    flag = 0;
+    NSK_CUDA_OK(cudaMemcpyAsync(&host[0], B.counter + MAX_SWEEPS, sizeof(int), cudaMemcpyDeviceToHost, st));
+    NSK_CUDA_OK(cudaMemcpyAsync(&host[1], B.bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (host[2]) NSK_CUDA_OK(cudaMemcpyAsync(&flag, B.version, sizeof(int), cudaMemcpyDeviceToHost, st));
     NSK_CUDA_OK(cudaStreamSynchronize(st));
     if (flag) host[2] = -1;
     return OK;
-  };
-  int host[3] = {0, 0, 0};
-  if (int rc = solve(true, host)) return rc;
-  if (host[2] < 0) {  // exactly singular R: What undefined, rerun on [R; I]
-    NSK_CUDA_OK(cudaMemsetAsync(version, 0, sizeof(int) * n, st));
-    NSK_CUDA_OK(cudaMemsetAsync(counter, 0, sizeof(int) * (MAX_SWEEPS + 1), st));
-    int64_t blocks = (2 * n * n * NC + 255) / 256;
-    if (blocks > 8L * sm_count()) blocks = 8L * sm_count();
-    build_stacked<<<static_cast<unsigned>(blocks), 256, 0, st>>>(A, rdiag, s, n, NC, X);
-    count_launch();
-    NSK_CUDA_OK(cudaGetLastError());
-    if (int rc = solve(false, host)) return rc;
   }
-  if (std::getenv("NSK_SVD_DEBUG")) std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d path=%d\n",
-                                                 static_cast<long long>(s), static_cast<long long>(n), b, host[0],
-                                                 host[2]);
-  if (n >= 2 && host[0] >= MAX_SWEEPS) return fail(ENOCONV, "svd: one-sided Jacobi did not converge");
-  if (host[1]) return fail(ENOCONV, "svd: non-finite singular values (input contains NaN/Inf)");
-  return OK;
+
+  int launch() {
+    if (int rc = stacked()) return rc;
+    // Stopping rule n * eps: the computed |u_p^T u_q| of converged columns
+    // carries ~sqrt(n) * eps relative rounding noise, so the tighter
+    // sqrt(n) * eps of dgesvj can stall on 1e-10-graded spectra.
+    tol = static_cast<double>(n) * 2.220446049250313e-16;
+    // Block width: the rotations of a round are FP64-throughput bound on the SMs
+    // that hold a block pair, so spread them -- the widest b in {16, 8, 4, 2}
+    // that still leaves >= 32 block pairs (CTAs) -- and a block pair of [R; I]
+    // columns must fit in shared memory.  NSK_SVD_B overrides (tuning).
+    b = 16;
+    while (b > 2 && n / b < 64) b >>= 1;
+    if (const char* e = std::getenv("NSK_SVD_B")) b = std::atoi(e) >= 1 && std::atoi(e) <= 16 ? std::atoi(e) : b;
+    while (b > 1 && sizeof(double) * 2 * b * 2 * n * NC > 200 * 1024) b >>= 1;
+    blocked = sizeof(double) * 2 * b * 2 * n * NC <= 200 * 1024 && std::getenv("NSK_SVD_PAIRS") == nullptr;
+    return solve(true);
+  }
+
+  int finish() {
+    if (int rc = collect()) return rc;
+    if (host[2] < 0) {  // exactly singular R: What undefined, rerun on [R; I]
+      NSK_CUDA_OK(cudaMemsetAsync(B.version, 0, sizeof(int) * n, st));
+      NSK_CUDA_OK(cudaMemsetAsync(B.counter, 0, sizeof(int) * (MAX_SWEEPS + 1), st));
+      if (int rc = stacked()) return rc;
+      if (int rc = solve(false)) return rc;
+      if (int rc = collect()) return rc;
+    }
+    if (std::getenv("NSK_SVD_DEBUG")) std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d path=%d\n",
+                                                   static_cast<long long>(s), static_cast<long long>(n), b, host[0],
+                                                   host[2]);
+    if (n >= 2 && host[0] >= MAX_SWEEPS) return fail(ENOCONV, "svd: one-sided Jacobi did not converge");
+    if (host[1]) return fail(ENOCONV, "svd: non-finite singular values (input contains NaN/Inf)");
+    return OK;
+  }
+};
+
+template <int NC>
+int svd_stage(const double* A, const double* rdiag, int64_t s, int64_t n, int64_t k, double* W, int64_t ldw,
+              double* sigma, SvdBufs B, cudaStream_t st) {
+  SvdStage<NC> g{A, rdiag, s, n, k, W, ldw, sigma, B, st};
+  if (int rc = g.launch()) return rc;
+  return g.finish();
+}
+
+// The second stage of jacobi_trailing_pair runs on this per-device stream (created once).
+cudaStream_t side_stream() {
+  constexpr int MAXDEV = 64;
+  static std::mutex mu;
+  static cudaStream_t cs[MAXDEV] = {};
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur < 0 || cur >= MAXDEV) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!cs[cur] && cudaStreamCreateWithFlags(&cs[cur], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    cs[cur] = nullptr;
+  }
+  return cs[cur];
 }
 
 // Householder QR of the s x n copy of SA (R above the diagonal of A, diagonal in rdiag), then the
 // Jacobi stage on R; with n2 > 0 also the singular values of the leading n2 columns (the
 // existence check of sketched TLS, tls.cpp:110-111): their R is the leading block of the same
-// factor, so that second Jacobi stage needs no QR of its own and runs concurrently on a helper
-// thread and stream (each stage fills one 16-CTA cluster).
+// factor, so that second Jacobi stage needs no QR of its own and runs concurrently on a second
+// stream (each stage fills one 16-CTA cluster).
 template <int NC>
 int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double* W, int64_t ldw, double* sigma,
         int64_t n2, double* sigma2, cudaStream_t st) {
@@ -897,34 +943,33 @@ int run(int64_t s, int64_t n, const double* SA, int64_t ldsa, int64_t k, double*
     if (int rc = qr_factor<NC>(Q, args, st)) return rc;
   }
   if (n2 <= 0) return svd_stage<NC>(A, rdiag, s, n, k, W, ldw, sigma, B1, st);
-  int devno = 0;
-  NSK_CUDA_OK(cudaGetDevice(&devno));
+  // both Jacobi stages in flight at once: stage 2 on the side stream after the QR (each fills one
+  // 16-CTA cluster; the device holds several), enqueued from this thread before either is collected
+  cudaStream_t aux = side_stream();
+  if (!aux) return fail(ECUDA, "svd: no side stream");
   cudaEvent_t qr_done;
   NSK_CUDA_OK(cudaEventCreateWithFlags(&qr_done, cudaEventDisableTiming));
   NSK_CUDA_OK(cudaEventRecord(qr_done, st));
-  std::string side_err;  // the helper's error text (last_error is per thread)
-  std::future<int> side = std::async(std::launch::async, [&]() -> int {
-    cudaSetDevice(devno);
-    // a stream of this call's own (a thread_local one would leak with the short-lived helper thread)
-    cudaStream_t aux = nullptr;
-    if (cudaError_t e = cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking)) {
-      const int rc = cuda_fail(e, "svd: helper stream");
-      side_err = last_error();
-      return rc;
-    }
-    int rc = OK;
-    if (cudaError_t e = cudaStreamWaitEvent(aux, qr_done, 0)) rc = cuda_fail(e, "svd: stream fork");
-    if (rc == OK) rc = svd_stage<NC>(A, rdiag, s, n2, 0, nullptr, 1, sigma2, B2, aux);  // ends synchronised
-    if (rc != OK) side_err = last_error();
-    cudaStreamSynchronize(aux);
-    cudaStreamDestroy(aux);
-    return rc;
-  });
-  const int rc1 = svd_stage<NC>(A, rdiag, s, n, k, W, ldw, sigma, B1, st);
-  const int rc2 = side.get();
+  const cudaError_t fork = cudaStreamWaitEvent(aux, qr_done, 0);
   cudaEventDestroy(qr_done);
+  NSK_CUDA_OK(fork);
+  SvdStage<NC> g1{A, rdiag, s, n, k, W, ldw, sigma, B1, st};
+  SvdStage<NC> g2{A, rdiag, s, n2, 0, nullptr, 1, sigma2, B2, aux};
+  const int l1 = g1.launch();
+  const int l2 = l1 == OK ? g2.launch() : OK;
+  // the scratch (ws) is released on st: st must not run ahead of the side stream's use of it
+  cudaEvent_t side_done;
+  NSK_CUDA_OK(cudaEventCreateWithFlags(&side_done, cudaEventDisableTiming));
+  NSK_CUDA_OK(cudaEventRecord(side_done, aux));
+  const cudaError_t join = cudaStreamWaitEvent(st, side_done, 0);
+  cudaEventDestroy(side_done);
+  NSK_CUDA_OK(join);
+  if (l1 != OK) return l1;
+  if (l2 != OK) return l2;
+  const int rc1 = g1.finish();
+  const int rc2 = g2.finish();
   if (rc1 != OK) return rc1;
-  if (rc2 != OK) return fail(rc2, side_err);
+  if (rc2 != OK) return rc2;
   return OK;
 }
 

@@ -251,8 +251,9 @@ int sm_count();
 // Pageable sources stream through a pinned staging ring filled by host
 // threads; pinned sources are DMAed directly.
 using ChunkFn = std::function<int(int64_t, int64_t, cudaEvent_t)>;
+// dcols (>= n): columns of each destination chunk block (room for a second column block after A).
 int h2d_rows(const void* A, int64_t m, int64_t n, int64_t lda, size_t elem, void* dA, int64_t chunk,
-             cudaStream_t st, const ChunkFn& on_chunk);
+             cudaStream_t st, const ChunkFn& on_chunk, int64_t dcols = 0);
 bool host_is_pinned(const void* p);
 cudaStream_t copy_stream();
 cudaStream_t thread_stream();
