@@ -56,6 +56,11 @@ struct Tile {
 // A tile by TMA: boxes {BK = 16 rows, <= 256 columns} with the 128-byte swizzle, i.e. column c's 16
 // rows are one 128-byte line whose 16-byte pairs are XOR-permuted by c mod 8 (conflict-free m8n8k4
 // fragment loads); the cp.async path keeps the k4 layout.
+// Complex A: the column-major complex matrix as a 2-D array of doubles {2 mloc, columns}; two boxes of 8
+// complex rows (128 bytes) x BN / 2 columns per tile, i.e. per half [col][8 rows][re/im] with the same
+// 128-byte swizzle (complex row k of column c is 16-byte chunk (k % 8) ^ (c % 8) of c's line).  An MMA
+// fragment's 8 logical columns are complex columns {0, 1, 4, 5} (+2 for odd fragments) of a group of 8,
+// re and im, so its 16-byte chunks cover both halves of the bank space (2 wavefronts per load).
 template <int BN, bool TMA> constexpr int box_w() { return TMA && BN > 256 ? 256 : BN; }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -259,10 +264,20 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         double* sb = sa + T::BM * T::BK;
         const int64_t k0 = kbeg + c * T::BK;
         if constexpr (TMA) {
-          if (pt == 0) {  // the whole A tile: BN / BW boxes {4 rows, BW columns, BK / 4 row groups}
+          if (pt == 0) {  // the whole A tile: BN / BW boxes {16 rows, BW columns} (complex: one 3-D box)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(full_mb + st)),
                          "r"(static_cast<uint32_t>(sizeof(double) * BN * T::BK))
                          : "memory");
+            if constexpr (NCOMP == 2) {
+#pragma unroll
+              for (int hk = 0; hk < 2; ++hk)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];\n" ::"r"(smem_addr(sb + hk * (BN / 2) * 16)),
+                    "l"(&tmA), "r"(static_cast<int>(2 * k0 + 16 * hk)), "r"(static_cast<int>(q0 >> 1)),
+                    "r"(smem_addr(full_mb + st))
+                    : "memory");
+            } else
 #pragma unroll
             for (int h = 0; h < BN / BW; ++h)
               asm volatile(
@@ -318,6 +333,7 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     // TMA layout: element (k, col) at col * 16 + (((k >> 1) ^ (col & 7)) << 1 | (k & 1)); a fragment's
     // column is wn * 64 + 8 b + lane / 4, so col & 7 = lane >> 2
     const double* Bt = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * 64 + (lane >> 2));
+    const double* Bc = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * 32);  // complex TMA layout
 #pragma unroll
     for (int kk = 0; kk < T::BK; kk += 4) {
       double af[TM];
@@ -328,7 +344,17 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
         double bf[TN / 2];
 #pragma unroll
         for (int b = 0; b < TN / 2; ++b) {
-          if constexpr (TMA) {
+          if constexpr (TMA && NCOMP == 2) {
+            // fragment f = h 4 + b of the warp: group g = f / 2 of 8 complex columns, complex column
+            // c = wn 32 + 8 g + 2 (f & 1) + (j & 1) + 4 (j >> 1), j = lane / 8, re/im r = (lane / 4) & 1,
+            // row k = kk + lane % 4: doubles (k / 8) (BN / 2) 16 + c 16 + 2 ((k % 8) ^ (c % 8)) + r
+            const int f = h * (TN / 2) + b;
+            const int j = lane >> 3;
+            const int cx = 2 * (f & 1) + (j & 1) + 4 * (j >> 1);  // c % 8 (wn 32 + 8 g is a multiple of 8)
+            const int off = (kk >> 3) * (BN / 2) * 16 + (8 * (f >> 1) + cx) * 16 +
+                            ((((kk & 7) + (lane & 3)) ^ cx) << 1) + ((lane >> 2) & 1);
+            bf[b] = Bc[off];
+          } else if constexpr (TMA) {
             const int kx = (((kk >> 1) + ((lane >> 1) & 1)) ^ (lane >> 2)) << 1 | (lane & 1);
             bf[b] = Bt[(h * (TN / 2) + b) * 8 * 16 + kx];
           } else {
@@ -352,7 +378,12 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     const int64_t i = i0 + wm * 32 + a * 8 + (lane >> 2);
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
-      const int64_t q = q0 + wn * 64 + b * 8 + 2 * (lane & 3);
+      // complex TMA: output column 2 (lane % 4) + e of fragment b is complex column
+      // wn 32 + 8 (b / 2) + 2 (b & 1) + (j & 1) + 4 (j >> 1), j = lane % 4, re/im e
+      const int jj = lane & 3;
+      const int64_t q = (TMA && NCOMP == 2)
+                            ? q0 + 2 * (wn * 32 + 8 * (b >> 1) + 2 * (b & 1) + (jj & 1) + 4 * (jj >> 1))
+                            : q0 + wn * 64 + b * 8 + 2 * jj;
       if (i < p.s) {
         if (q < p.nq) P[q * p.s + i] = acc[a][b][0];
         if (q + 1 < p.nq) P[(q + 1) * p.s + i] = acc[a][b][1];
@@ -401,10 +432,7 @@ int launch_bn(int BN, const GaussParams& p, const CUtensorMap& tm_a, int64_t q_t
                    : launch<512, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st);
 }
 
-// Tensor map of a real column-major A (mloc x nq, ld lda): a box {BK = 16 rows, BW columns} lands in
-// shared memory as [col][16 rows] with the 128-byte swizzle.  false when the driver entry point is
-// unavailable or the encode fails (the cp.async path runs instead).
-bool encode_a_map(const double* A, int64_t lda, int64_t mloc, int64_t nq, int BW, int BK, CUtensorMap* out) {
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -415,6 +443,28 @@ bool encode_a_map(const double* A, int64_t lda, int64_t mloc, int64_t nq, int BW
     }
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }();
+  return encode;
+}
+
+// Complex A (mloc x nc complex columns, ld lda complex elements) as doubles {2 mloc, nc}: a box
+// {16 doubles = 8 complex rows, BWc columns} lands as [col][8 rows][re/im] with the 128-byte swizzle.
+bool encode_c_map(const double* A, int64_t lda, int64_t mloc, int64_t nc, int BWc, int BK, CUtensorMap* out) {
+  PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
+  if (!encode || BWc > 256 || BK != 16) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * mloc), static_cast<cuuint64_t>(nc)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * 2 * sizeof(double)};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(BWc)};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Tensor map of a real column-major A (mloc x nq, ld lda): a box {BK = 16 rows, BW columns} lands in
+// shared memory as [col][16 rows] with the 128-byte swizzle.  false when the driver entry point is
+// unavailable or the encode fails (the cp.async path runs instead).
+bool encode_a_map(const double* A, int64_t lda, int64_t mloc, int64_t nq, int BW, int BK, CUtensorMap* out) {
+  PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
   if (!encode) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(mloc), static_cast<cuuint64_t>(nq)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(lda) * sizeof(double)};
@@ -494,9 +544,12 @@ int gaussian_apply_key2(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t
   // [A | B] stored back to back with one leading dimension (the usual sketched-TLS caller: one m x (n+k)
   // buffer) is a single matrix to the tensor map
   const bool one_matrix = !B || (ldb == lda && B == A + nqa * lda);
-  const bool tma = vec16 && one_matrix && BK == 16 && !(te && te[0] == '0') &&
-                   encode_a_map(A, lda, mloc, nq, BN > 256 ? 256 : BN, BK, &tm_a);
-  int rc = ncomp == 2 ? launch_bn<2, false>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
+  const bool tma_ok = one_matrix && BK == 16 && !(te && te[0] == '0');
+  const bool tma = vec16 && tma_ok && encode_a_map(A, lda, mloc, nq, BN > 256 ? 256 : BN, BK, &tm_a);
+  const bool tma_c = ncomp == 2 && tma_ok && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                     encode_c_map(A, lda, mloc, nq / 2, BN / 2, BK, &tm_a);
+  int rc = tma_c       ? launch_bn<2, false, true>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
+         : ncomp == 2 ? launch_bn<2, false>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
          : tma       ? launch_bn<1, true, true>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
          : vec16     ? launch_bn<1, true>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
                      : launch_bn<1, false>(BN, p, tm_a, q_tiles, s_tiles, splits, st);
