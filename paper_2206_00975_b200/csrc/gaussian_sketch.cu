@@ -47,11 +47,12 @@ constexpr int REG_CONSUMER = 168, REG_PRODUCER = 88;
 // consecutive A rows of one column stays contiguous.
 template <int BN>
 struct Tile {
-  static constexpr int BM = 16384 / BN;                                // 128, 64, 32
+  static constexpr int BM = BN == 384 ? 32 : 16384 / BN;              // 128, 64, 32, 32
   static constexpr int BK = BN == 128 ? 32 : 16;                       // A rows per stage
   static constexpr int STAGE = (BM + BN) * BK;                         // doubles per stage
-  static constexpr int STAGES = BN == 512 ? 3 : (BN == 256 ? 4 : 3);   // ring depth (<= 216 KiB)
+  static constexpr int STAGES = BN == 512 ? 3 : (BN == 256 || BN == 384 ? 4 : 3);  // ring depth (<= 216 KiB)
   static constexpr int WGM = BM / 32;                                  // consumer warp grid rows
+  static constexpr int TN = BN / (8 / WGM) / 8;                        // 8-column MMA tiles per warp (8 or 6)
 };
 // A tile by TMA: boxes {BK = 16 rows, <= 256 columns} with the 128-byte swizzle, i.e. column c's 16
 // rows are one 128-byte line whose 16-byte pairs are XOR-permuted by c mod 8 (conflict-free m8n8k4
@@ -61,7 +62,7 @@ struct Tile {
 // 128-byte swizzle (complex row k of column c is 16-byte chunk (k % 8) ^ (c % 8) of c's line).  An MMA
 // fragment's 8 logical columns are complex columns {0, 1, 4, 5} (+2 for odd fragments) of a group of 8,
 // re and im, so its 16-byte chunks cover both halves of the bank space (2 wavefronts per load).
-template <int BN, bool TMA> constexpr int box_w() { return TMA && BN > 256 ? 256 : BN; }
+template <int BN, bool TMA> constexpr int box_w() { return TMA && BN > 256 ? (BN == 384 ? 192 : 256) : BN; }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
                                                                      const __grid_constant__ CUtensorMap tmA) {
   using T = Tile<BN>;
   constexpr int BW = box_w<BN, TMA>();
-  constexpr int TN = 64 / 8;  // 8-col MMA tiles per warp
+  constexpr int TN = T::TN;   // 8-col MMA tiles per warp (a warp tile is 32 x 8 TN)
   constexpr int TM = 32 / 8;  // 8-row MMA tiles per warp
   extern __shared__ __align__(1024) double smem[];
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * T::BM;
@@ -329,11 +330,11 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
     named_sync(1 + st, THREADS);  // wait: stage full
     // k4 layout: fragment (x = lane/4, k = lane%4) of k-step kk at (kk/4)*4X + 4x + k.
     const double* A_ = smem + st * T::STAGE + 4 * (wm * 32) + lane;
-    const double* B_ = smem + st * T::STAGE + T::BM * T::BK + 4 * (wn * 64) + lane;
+    const double* B_ = smem + st * T::STAGE + T::BM * T::BK + 4 * (wn * TN * 8) + lane;
     // TMA layout: element (k, col) at col * 16 + (((k >> 1) ^ (col & 7)) << 1 | (k & 1)); a fragment's
-    // column is wn * 64 + 8 b + lane / 4, so col & 7 = lane >> 2
-    const double* Bt = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * 64 + (lane >> 2));
-    const double* Bc = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * 32);  // complex TMA layout
+    // column is wn * 8 TN + 8 b + lane / 4, so col & 7 = lane >> 2
+    const double* Bt = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * TN * 8 + (lane >> 2));
+    const double* Bc = smem + st * T::STAGE + T::BM * T::BK + 16 * (wn * TN * 4);  // complex TMA layout
 #pragma unroll
     for (int kk = 0; kk < T::BK; kk += 4) {
       double af[TM];
@@ -345,12 +346,12 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
 #pragma unroll
         for (int b = 0; b < TN / 2; ++b) {
           if constexpr (TMA && NCOMP == 2) {
-            // fragment f = h 4 + b of the warp: group g = f / 2 of 8 complex columns, complex column
-            // c = wn 32 + 8 g + 2 (f & 1) + (j & 1) + 4 (j >> 1), j = lane / 8, re/im r = (lane / 4) & 1,
+            // fragment f = h TN / 2 + b of the warp: group g = f / 2 of 8 complex columns, complex column
+            // c = wn 4 TN + 8 g + 2 (f & 1) + (j & 1) + 4 (j >> 1), j = lane / 8, re/im r = (lane / 4) & 1,
             // row k = kk + lane % 4: doubles (k / 8) (BN / 2) 16 + c 16 + 2 ((k % 8) ^ (c % 8)) + r
             const int f = h * (TN / 2) + b;
             const int j = lane >> 3;
-            const int cx = 2 * (f & 1) + (j & 1) + 4 * (j >> 1);  // c % 8 (wn 32 + 8 g is a multiple of 8)
+            const int cx = 2 * (f & 1) + (j & 1) + 4 * (j >> 1);  // c % 8 (wn 4 TN + 8 g is a multiple of 8)
             const int off = (kk >> 3) * (BN / 2) * 16 + (8 * (f >> 1) + cx) * 16 +
                             ((((kk & 7) + (lane & 3)) ^ cx) << 1) + ((lane >> 2) & 1);
             bf[b] = Bc[off];
@@ -379,11 +380,11 @@ __global__ void __launch_bounds__(THREADS, 1) gaussian_sketch_kernel(GaussParams
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
       // complex TMA: output column 2 (lane % 4) + e of fragment b is complex column
-      // wn 32 + 8 (b / 2) + 2 (b & 1) + (j & 1) + 4 (j >> 1), j = lane % 4, re/im e
+      // wn 4 TN + 8 (b / 2) + 2 (b & 1) + (j & 1) + 4 (j >> 1), j = lane % 4, re/im e
       const int jj = lane & 3;
       const int64_t q = (TMA && NCOMP == 2)
-                            ? q0 + 2 * (wn * 32 + 8 * (b >> 1) + 2 * (b & 1) + (jj & 1) + 4 * (jj >> 1))
-                            : q0 + wn * 64 + b * 8 + 2 * jj;
+                            ? q0 + 2 * (wn * TN * 4 + 8 * (b >> 1) + 2 * (b & 1) + (jj & 1) + 4 * (jj >> 1))
+                            : q0 + wn * TN * 8 + b * 8 + 2 * jj;
       if (i < p.s) {
         if (q < p.nq) P[q * p.s + i] = acc[a][b][0];
         if (q + 1 < p.nq) P[(q + 1) * p.s + i] = acc[a][b][1];
@@ -429,6 +430,7 @@ int launch_bn(int BN, const GaussParams& p, const CUtensorMap& tm_a, int64_t q_t
               cudaStream_t st) {
   return BN == 128 ? launch<128, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st)
        : BN == 256 ? launch<256, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st)
+       : BN == 384 ? launch<384, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st)
                    : launch<512, NCOMP, VEC16, TMA>(p, tm_a, q_tiles, s_tiles, splits, st);
 }
 
@@ -507,13 +509,15 @@ int gaussian_apply_key2(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t
     return OK;
   }
   // Widest n-tile that the problem fills (each G entry is regenerated once per n-tile).
-  int BN = nq <= 128 ? 128 : (nq <= 256 ? 256 : 512);
+  // (384: a 32 x 384 tile with 6-fragment warp tiles for 256 < nq <= 384, e.g. the 300 logical
+  // columns of configs[4], 78% useful against 59% in a 512-wide tile)
+  int BN = nq <= 128 ? 128 : (nq <= 256 ? 256 : (nq <= 384 ? 384 : 512));
   if (const char* e = std::getenv("NSK_GAUSS_BN")) {  // A/B override: 128, 256 or 512
     const int v = std::atoi(e);
-    if (v == 128 || v == 256 || v == 512) BN = v;
+    if (v == 128 || v == 256 || v == 384 || v == 512) BN = v;
   }
   // Must match Tile<BN>::BK: the kernel walks chunks of Tile<BN>::BK rows.
-  const int BM = 16384 / BN, BK = BN == 128 ? Tile<128>::BK : (BN == 256 ? Tile<256>::BK : Tile<512>::BK);
+  const int BM = BN == 384 ? Tile<384>::BM : 16384 / BN, BK = BN == 128 ? Tile<128>::BK : 16;
   const int64_t q_tiles = (nq + BN - 1) / BN;
   const int64_t s_tiles = (s + BM - 1) / BM;
   const int64_t chunks = (mloc + BK - 1) / BK;
@@ -545,7 +549,8 @@ int gaussian_apply_key2(PhiloxKey key, int64_t s, const uint32_t* zmask, int64_t
   // buffer) is a single matrix to the tensor map
   const bool one_matrix = !B || (ldb == lda && B == A + nqa * lda);
   const bool tma_ok = one_matrix && BK == 16 && !(te && te[0] == '0');
-  const bool tma = vec16 && tma_ok && encode_a_map(A, lda, mloc, nq, BN > 256 ? 256 : BN, BK, &tm_a);
+  const int bw = BN > 256 ? (BN == 384 ? 192 : 256) : BN;
+  const bool tma = vec16 && tma_ok && encode_a_map(A, lda, mloc, nq, bw, BK, &tm_a);
   const bool tma_c = ncomp == 2 && tma_ok && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
                      encode_c_map(A, lda, mloc, nq / 2, BN / 2, BK, &tm_a);
   int rc = tma_c       ? launch_bn<2, false, true>(BN, p, tm_a, q_tiles, s_tiles, splits, st)
