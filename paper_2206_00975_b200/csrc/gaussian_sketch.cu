@@ -12,10 +12,13 @@
 //     no f64 kind.  On B200 DMMA and DFMA share the FP64 pipe (measured
 //     36.9 TF/s DMMA-only), so the Box-Muller work competes with the MMAs:
 //     the CTA tile is as wide in n as the register file allows (BM x BN =
-//     16384 accumulators: 128x128, 64x256 or 32x512) so each G entry is
-//     regenerated ceil(n / BN) times.
-//   * warp specialisation: 4 producer warps regenerate the G tile into
-//     shared memory and stream the A tile in with cp.async; 8 consumer warps
+//     16384 accumulators: 128x128, 64x256 or 32x512; 32x384 when 256 < n <= 384
+//     so fewer columns are padding) so each G entry is regenerated ceil(n / BN)
+//     times.
+//   * A tiles by TMA (one producer thread, 128-byte swizzled boxes, stage
+//     mbarriers) for real A, contiguous [A | B] and complex A; cp.async otherwise.
+//   * warp specialisation: producer warps regenerate the G tile into
+//     shared memory (and stream the A tile in when TMA does not apply); 8 consumer warps
 //     run the DMMAs (warp tile 32 x 64).  A 3-stage ring with named-barrier
 //     full/empty handshakes overlaps generation, loads and MMAs.
 //   * split-K over m: every CTA writes a partial tile; reduce_partials sums
