@@ -183,7 +183,8 @@ int copy_in(const void* host, int64_t rows, int64_t cols, int64_t ld, int ncomp,
 // apply.  a_buf receives the device copy of A.
 int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void* A, int64_t lda, nsk::Scratch& a_buf,
                 double* SA, cudaStream_t st, int64_t kb = 0, const void* B = nullptr, int64_t ldb = 0,
-                nsk::Scratch* b_buf = nullptr) {
+                nsk::Scratch* b_buf = nullptr, int64_t row0 = 0) {
+  // row0: global row of A's first row (a contiguous multi-GPU shard of m rows; 0 for the whole matrix)
   const int nc_out = out_ncomp(op, nc_in);
   const size_t elem = sizeof(double) * nc_in;
   // [A | B] (sketched TLS): B (a few columns) is copied whole first, then A streams in chunks and
@@ -201,7 +202,7 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   double* dA = nullptr;
   if (!pipelined) {
     if (int rc = copy_in(A, m, n, lda, nc_in, &dA, a_buf, st)) return rc;
-    nsk::RowMap rows{0, 1, m};
+    nsk::RowMap rows{row0, 1, m};
     return dispatch_apply2(op, nc_in, rows, n, dA, m, kb, dB, m, SA, op.s, st);
   }
   // each row chunk lands as one rows x (n + kb) block: A's rows, then (copied on the device) the same
@@ -216,9 +217,9 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
   // ~0.2 s of host work at m = 2^24) are built on a helper thread while the copy engine moves A.
   int devno = 0;
   NSK_CUDA_OK(cudaGetDevice(&devno));
-  std::future<const nsk::DeviceTables*> tab = std::async(std::launch::async, [&op, m, devno]() {
+  std::future<const nsk::DeviceTables*> tab = std::async(std::launch::async, [&op, m, row0, devno]() {
     cudaSetDevice(devno);
-    return op.tables(0, m);
+    return op.tables(row0, row0 + m);
   });
   bool have_tables = false;
   struct Pending {
@@ -231,7 +232,7 @@ int host_sketch(const Operator& op, int nc_in, int64_t m, int64_t n, const void*
     cudaError_t e = cudaStreamWaitEvent(st, c.landed, 0);
     cudaEventDestroy(c.landed);
     if (e != cudaSuccess) return nsk::cuda_fail(e, "chunk wait");
-    nsk::RowMap shard{c.r0, 1, c.rows};  // chunk-major device copy: this chunk's block, ld = its rows
+    nsk::RowMap shard{row0 + c.r0, 1, c.rows};  // chunk-major device copy: this chunk's block, ld = its rows
     double* blk = dA + c.r0 * ntot * nc_in;
     if (kb > 0) {
       if (cudaError_t e2 = cudaMemcpy2DAsync(blk + c.rows * n * nc_in, elem * c.rows, dB + c.r0 * nc_in, elem * m,
@@ -291,6 +292,12 @@ int copy_out(void* host, int64_t ld, const double* dev, int64_t rows, int64_t co
 }  // namespace
 
 namespace nsk {
+// The pipelined host-buffer sketch of a contiguous row shard (nccl_shard.cpp's host entry point).
+int host_sketch_shard(const Operator& op, int nc_in, int64_t row0, int64_t mloc, int64_t n, const void* A,
+                      int64_t lda, double* SA, cudaStream_t st) {
+  Scratch a;
+  return host_sketch(op, nc_in, mloc, n, A, lda, a, SA, st, 0, nullptr, 0, nullptr, row0);
+}
 // dispatch_apply for the multi-GPU entry points (nccl_shard.cpp)
 int dispatch_apply_c(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                      double* SA, int64_t ldsa, cudaStream_t st) {

@@ -29,6 +29,8 @@
 namespace nsk {
 int dispatch_apply_c(const Operator& op, int ncomp, const RowMap& rows, int64_t n, const double* A, int64_t lda,
                      double* SA, int64_t ldsa, cudaStream_t st);
+int host_sketch_shard(const Operator& op, int nc_in, int64_t row0, int64_t mloc, int64_t n, const void* A,
+                      int64_t lda, double* SA, cudaStream_t st);
 }
 
 namespace {
@@ -198,13 +200,33 @@ int nsk_solve_k_sharded_host(const nsk_operator* h, int scalar, int64_t row0, in
   if (!st) return nsk::fail(nsk::ECUDA, "solve_k_sharded_host: no compute stream");
   const int nc_in = scalar == NSK_COMPLEX ? 2 : 1, nc = out_nc(op, scalar);
   nsk::Scratch a, w, sg;
-  NSK_CUDA_OK(a.alloc(sizeof(double) * nc_in * (mloc > 0 ? mloc : 1) * n, st));
-  if (int rc = nsk::h2d_rows(A_local, mloc, n, lda, sizeof(double) * nc_in, a.p, mloc, st, nullptr)) return rc;
   NSK_CUDA_OK(w.alloc(sizeof(double) * nc * n * (k > 0 ? k : 1), st));
   NSK_CUDA_OK(sg.alloc(sizeof(double) * n, st));
-  if (int rc = nsk_solve_k_sharded(h, scalar, row0, rstep, mloc, n, a.p, mloc > 0 ? mloc : 1, k, w.p, n,
-                                   sg.as<double>(), comm, st))
-    return rc;
+  if (rstep == 1 && mloc > 0 && op.appended == 0) {
+    // contiguous shard: the single-GPU host pipeline (row chunks sketched as they land, the
+    // operator's tables for this shard's rows built during the copy), then reduce + SVD
+    if (row0 < 0 || row0 + mloc > op.m) return nsk::fail(nsk::ERANGE_, "apply_shard: rows beyond the operator's m");
+    if (op.s < n)
+      return nsk::fail(nsk::EINVAL_, "nullspace: sketch size s = " + std::to_string(op.s) +
+                                         " is smaller than n = " + std::to_string(n));
+    if (scalar == NSK_COMPLEX && (op.kind == nsk::SRDCT || op.kind == nsk::SRHT || op.kind == nsk::COUNTSKETCH))
+      return nsk::fail(nsk::EINVAL_, "sketch apply: complex input needs a gaussian or srft operator");
+    nsk::Scratch sa;
+    NSK_CUDA_OK(sa.alloc(sizeof(double) * op.s * n * nc, st));
+    if (int rc = nsk::host_sketch_shard(op, nc_in, row0, mloc, n, A_local, lda, sa.as<double>(), st)) return rc;
+    const size_t count = static_cast<size_t>(op.s) * static_cast<size_t>(n) * nc;
+    if (ncclResult_t r = nccl().all_reduce(sa.p, sa.p, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm), st))
+      return nccl_fail(r, "ncclAllReduce");
+    if (int rc = nsk::jacobi_trailing(nc, op.s, n, sa.as<double>(), op.s, k, static_cast<double*>(w.p), n,
+                                      sg.as<double>(), st))
+      return rc;
+  } else {
+    NSK_CUDA_OK(a.alloc(sizeof(double) * nc_in * (mloc > 0 ? mloc : 1) * n, st));
+    if (int rc = nsk::h2d_rows(A_local, mloc, n, lda, sizeof(double) * nc_in, a.p, mloc, st, nullptr)) return rc;
+    if (int rc = nsk_solve_k_sharded(h, scalar, row0, rstep, mloc, n, a.p, mloc > 0 ? mloc : 1, k, w.p, n,
+                                     sg.as<double>(), comm, st))
+      return rc;
+  }
   if (k > 0)
     NSK_CUDA_OK(cudaMemcpy2DAsync(W, sizeof(double) * nc * ldw, w.p, sizeof(double) * nc * n, sizeof(double) * nc * n,
                                   k, cudaMemcpyDeviceToHost, st));

@@ -180,3 +180,27 @@ def sharded_solve_k_nccl(S, A_local, k: int, shard: RowShard, comm: NcclComm):
                                      ctypes.c_void_p(A_local.data_ptr()), lda, int(k), ctypes.c_void_p(W.data_ptr()),
                                      max(n, 1), ctypes.c_void_p(sig.data_ptr()), comm.handle, _stream_ptr()))
     return W, sig
+
+
+def sharded_solve_k_host_nccl(S, A_host, k: int, shard: RowShard, comm: NcclComm):
+    """(W, sigma) on every rank from the rank's shard in HOST memory: nsk_solve_k_sharded_host (a
+    contiguous shard streams in row chunks that are sketched as they land; then ncclAllReduce and
+    the SVD on every rank).  numpy in, numpy out."""
+    import ctypes
+
+    import numpy as np
+
+    from . import _lib
+    from .sketch import NSK_COMPLEX, NSK_REAL
+    L = _lib.load()
+    cplx = np.iscomplexobj(A_host)
+    A = np.asfortranarray(A_host, dtype=np.complex128 if cplx else np.float64)
+    mloc, n = A.shape
+    cplx_out = cplx or S.kind == "srft"
+    W = np.empty((n, max(k, 0)), dtype=np.complex128 if cplx_out else np.float64, order="F")
+    sig = np.empty(n)
+    _lib.check(L.nsk_solve_k_sharded_host(S.handle, NSK_COMPLEX if cplx else NSK_REAL, shard.row0, shard.rstep, mloc,
+                                          n, A.ctypes.data_as(ctypes.c_void_p), max(mloc, 1), int(k),
+                                          W.ctypes.data_as(ctypes.c_void_p), max(n, 1),
+                                          sig.ctypes.data_as(ctypes.c_void_p), comm.handle))
+    return W, sig

@@ -666,6 +666,32 @@ def test_nccl_entry_points_single_rank(nsk, oracle, kind, cyclic):
         comm.close()
 
 
+@pytest.mark.parametrize("kind,m,row0,mloc", [("gaussian", 50000, 16000, 20000), ("srht", 1 << 17, 1 << 15, 1 << 15),
+                                              ("countsketch", 4 * 12288, 12288, 2 * 12288),
+                                              ("gaussian", 1 << 21, 0, 1 << 21)])
+def test_nccl_host_shard_single_rank(nsk, oracle, kind, m, row0, mloc):
+    """nsk_solve_k_sharded_host on a contiguous shard from host memory (a one-rank communicator, so
+    the all-reduce is the identity): the partial sketch S[:, rows] A_rows (the library's host
+    pipeline with the shard's global row offset; the 2^21 x 16 case is big enough to stream in row
+    chunks) and its SVD against the oracle applied to A zero outside the shard."""
+    from paper_2206_00975_b200.distributed import NcclComm, RowShard, sharded_solve_k_host_nccl
+    n = 16 if m == 1 << 21 else 8
+    s = 4096 if kind == "countsketch" else 64
+    A_loc = oracle.random_real(mloc, n, 23)
+    A_full = np.zeros((m, n))
+    A_full[row0:row0 + mloc] = A_loc
+    S = nsk.SketchOperator.draw(kind, s, m, 62)
+    comm = NcclComm()
+    try:
+        W, sig = sharded_solve_k_host_nccl(S, A_loc, 2, RowShard(row0, 1, mloc), comm)
+        ref = oracle.apply(oracle.draw(kind, s, m, 62), A_full)
+        Wref, sref = oracle.from_sketch_svd(ref, 2)
+        assert np.max(np.abs(sig - sref)) <= 1000 * U * sref[0]
+        assert _angle(W, Wref) <= 1e-8
+    finally:
+        comm.close()
+
+
 def test_tls_complex_many_rhs_and_release(nsk, oracle):
     """Complex sketched TLS with k = 60 right-hand sides (the corner solve needs 57.6 KiB of
     dynamic shared memory, above the 48 KiB default) against the oracle, k = 65 rejected before
