@@ -99,3 +99,23 @@ def test_qr_register_kernel_matches_memory_kernel(nsk, oracle, monkeypatch, s, n
     s1, s2 = host(s1), host(s2)
     assert np.max(np.abs(s1 - s2)) <= 1e3 * U * s1[0]
     assert oracle.sin_theta(host(W1), host(W2)) <= 1e-10
+
+
+# Row shards of a Gaussian operator through the TMA tiles (n = 200 / 300: the 256- and 384-wide
+# tiles): the shard partials sum to the whole sketch, and each matches the oracle on A zero
+# outside the shard (the tensor map covers the local rows; S is regenerated for the global ones).
+@pytest.mark.parametrize("n,cplx", [(200, False), (300, False), (150, True)])
+def test_gaussian_tma_row_shards(nsk, oracle, n, cplx):
+    m, s = 9000, 320
+    A = oracle.random_complex(m, n, 51) if cplx else oracle.random_real(m, n, 51)
+    S = nsk.SketchOperator.draw("gaussian", s, m, 5151)
+    op = oracle.draw("gaussian", s, m, 5151)
+    cuts = [0, 2000, 5120, m]
+    total = None
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        part = host(nsk.apply_shard(S, dev(A[a:b]), a))
+        Az = np.zeros_like(A)
+        Az[a:b] = A[a:b]
+        assert rel(part, oracle.apply(op, Az)) <= SA_TOL
+        total = part if total is None else total + part
+    assert rel(total, oracle.apply(op, A)) <= SA_TOL
