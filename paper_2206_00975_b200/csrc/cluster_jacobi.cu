@@ -387,8 +387,10 @@ __device__ __forceinline__ void push_candidate(cg::cluster_group& cluster, doubl
 
 // RPL = rows per lane of the register-resident QRCP step (n <= 32 RPL);
 // NB = block buffers per CTA (4, or 3 when four do not fit: two-phase moves).
+// Up to 16 warps (b <= 16) per CTA; the complex RPL = 8 kernel holds 162 registers and is capped at
+// 12 warps (cluster_svd_max_b).
 template <int NC, int RPL, int NB>
-__global__ void __launch_bounds__(32 * RPL) cluster_svd_kernel(CSParams p) {  // b <= RPL
+__global__ void __launch_bounds__(NC == 2 && RPL == 8 ? 384 : 512, 1) cluster_svd_kernel(CSParams p) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double buf[];  // [NB block buffers][b][n * NC], phys[n]
   __shared__ Circle cc;
@@ -773,19 +775,46 @@ int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cu
 int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, int* degenerate, cudaStream_t st) {
   if (std::getenv("NSK_SVD_NORT") || std::getenv("NSK_SVD_NOCLUSTER")) return NOTAPPLICABLE;
   if (n < 2 || n > 4096) return NOTAPPLICABLE;
-  int C = static_cast<int>((n + 3) / 4);
-  if (C > 16) C = 16;
-  const int b = static_cast<int>((n + 2 * C - 1) / (2 * C));
-  if (b > 16) return NOTAPPLICABLE;
-  // four block buffers when they fit, else three (two-phase block moves)
-  int nbuf = 4;
-  const size_t bstride = (static_cast<size_t>(b) * n * ncomp + 1) & ~static_cast<size_t>(1);  // as blksz
-  size_t smem = sizeof(double) * 4 * bstride + sizeof(int) * n;
-  if (smem > 200 * 1024) {
-    nbuf = 3;
-    smem = sizeof(double) * 3 * bstride + sizeof(int) * n;
+  // Cluster width: a sweep is 2Cb - 1 pair rounds (npad = 2Cb padded columns) plus 2C - 1 block
+  // moves.  A round costs more as b warps share one SM, a move (DSMEM copy + cluster barriers)
+  // ~3.5-4.5k cycles; measured on B200 (tools/svd_small.py, cycle stamps): real rounds ~700 + 65 b
+  // cycles, complex ~1270 + 100 b.  Pick the C in [Cmin, 16] with the smallest modelled sweep (n = 64:
+  // C = 4, n = 100: 5, n = 256 and 512: 16).  NSK_SVD_C overrides (A/B).
+  const int rpl_ = n <= 128 ? 4 : n <= 256 ? 8 : 16;
+  const int bmax = ncomp == 2 && rpl_ == 8 ? 12 : 16;
+  const double l0 = ncomp == 2 ? 1270.0 : 700.0, lb = ncomp == 2 ? 100.0 : 65.0, mv = ncomp == 2 ? 4200.0 : 3500.0;
+  int C = 16;
+  double best = 1e300;
+  for (int c = static_cast<int>((n + 2 * bmax - 1) / (2 * bmax)); c <= 16; ++c) {
+    const int bb = static_cast<int>((n + 2 * c - 1) / (2 * c));
+    const double cost = (2.0 * c * bb - 1.0) * (l0 + lb * bb) + (2.0 * c - 1.0) * mv;
+    if (cost < best) {
+      best = cost;
+      C = c;
+    }
   }
-  if (smem > 210 * 1024 || n > 512) return NOTAPPLICABLE;
+  if (const char* e = std::getenv("NSK_SVD_C")) {
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= 16) C = v;
+  }
+  if (C > 16) C = 16;
+  int b = 0, nbuf = 4;
+  size_t smem = 0;
+  for (;; ++C) {  // narrower blocks (more CTAs) until the block buffers fit
+    if (C > 16) return NOTAPPLICABLE;
+    b = static_cast<int>((n + 2 * C - 1) / (2 * C));
+    if (b > bmax) continue;
+    // four block buffers when they fit, else three (two-phase block moves)
+    const size_t bstride = (static_cast<size_t>(b) * n * ncomp + 1) & ~static_cast<size_t>(1);  // as blksz
+    nbuf = 4;
+    smem = sizeof(double) * 4 * bstride + sizeof(int) * n;
+    if (smem > 200 * 1024) {
+      nbuf = 3;
+      smem = sizeof(double) * 3 * bstride + sizeof(int) * n;
+    }
+    if (smem <= 210 * 1024 && (nbuf == 4 || rpl_ == 16)) break;  // three-buffer kernels: RPL = 16 only
+  }
+  if (n > 512) return NOTAPPLICABLE;
   const int threads = 32 * b;
   const bool dbg = std::getenv("NSK_SVD_DEBUG") != nullptr;
   unsigned long long* stamps = nullptr;
