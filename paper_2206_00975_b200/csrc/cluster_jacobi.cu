@@ -49,6 +49,7 @@ struct CJParams {
   int b;      // columns per block
   double tol;
   int* counter;  // [CJ_MAX_SWEEPS] rotations per sweep (CTA 0 writes), [CJ_MAX_SWEEPS] = sweeps
+  int early;     // stop after a sweep of small rotations only (NSK_SVD_FULLCHECK=1: 0)
 };
 
 __device__ __forceinline__ void cluster_arrive() {
@@ -81,8 +82,10 @@ struct Circle {
   int nb;                          // block buffers per CTA: 4 (two inboxes) or 3 (one free buffer, two-phase moves)
   int sentA;                       // nb = 3: buffer sent right in phase A of the current move
   int blockid[4];                  // block held by each buffer
-  int rotated;                     // any rotation in this CTA and sweep
-  int sweep_rot[16];               // CTA 0: per-CTA flags of the finished sweep
+  int rotated;                     // rotations in this CTA and sweep
+  int big;                         // a rotation with |cos| > sqrt(eps) / 2 in this CTA and sweep
+  int sweep_big[16];               // CTA 0: per-CTA big flags of the finished sweep
+  int sweep_rot[16];               // CTA 0: per-CTA rotation counts of the finished sweep
   unsigned char ptab[31 * 16][2];  // inner round-robin pairs (2b <= 32)
 };
 
@@ -106,6 +109,7 @@ __device__ void circle_init(Circle& cc, int c, int b, int nb = 4) {
     cc.blockid[1] = 2 * c + 1;
     cc.blockid[2] = cc.blockid[3] = -1;
     cc.rotated = 0;
+    cc.big = 0;
   }
 }
 
@@ -115,7 +119,7 @@ __device__ void circle_init(Circle& cc, int c, int b, int nb = 4) {
 // Returns the number of sweeps (CTA 0 also records per-sweep counts).
 template <int NC, int RPL>
 __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc, int n, int ld, int b, double tol2,
-                             int* counter, unsigned long long* prof = nullptr) {
+                             int* counter, bool early, unsigned long long* prof = nullptr) {
   long long t_inner = 0, t_move = 0, t0 = 0, t1 = 0;
   const int c = static_cast<int>(cluster.block_rank()), C = static_cast<int>(cluster.num_blocks());
   // blksz: buffer stride, rounded up to an even count so every block buffer is 16-byte aligned for
@@ -146,9 +150,10 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
             const int lq = r == 0 ? cc.ptab[t * b + warp][1] : b + (warp + t) % b;
             double* xp = cols[lp / b] + (lp % b) * colsz;
             double* xq = cols[lq / b] + (lq % b) * colsz;
-            const bool rot = REG ? jacobi_pair_reg<NC, RPL>(xp, xq, n, ld, lane, tol2)
-                                 : jacobi_pair<NC>(xp, xq, n, ld, lane, tol2);
-            if (rot && lane == 0) cc.rotated = 1;
+            const int rot = REG ? jacobi_pair_reg<NC, RPL>(xp, xq, n, ld, lane, tol2)
+                                : jacobi_pair<NC>(xp, xq, n, ld, lane, tol2);
+            if (rot && lane == 0) atomicAdd(&cc.rotated, 1);
+            if (rot == 2 && lane == 0) cc.big = 1;
           }
           __syncthreads();
         }
@@ -158,15 +163,18 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
         double* xp = cols[0] + warp * colsz;
         double pr[RPL], pim[RPL];
         load_col<NC, RPL>(xp, n, lane, pr, pim);
-        bool any = false;
+        int nrot = 0, big = 0;
         for (int t = 0; t < b; ++t) {
           double* xq = cols[1] + ((warp + t) % b) * colsz;
-          any |= jacobi_step_preg<NC, RPL>(pr, pim, xp, xq, n, ld, lane, tol2);
+          const int rot = jacobi_step_preg<NC, RPL>(pr, pim, xp, xq, n, ld, lane, tol2);
+          nrot += rot ? 1 : 0;
+          big |= rot == 2;
           __syncthreads();
         }
-        if (any) {
+        if (nrot) {
           store_col<NC, RPL>(xp, n, lane, pr, pim);
-          if (lane == 0) cc.rotated = 1;
+          if (lane == 0) atomicAdd(&cc.rotated, nrot);
+          if (big && lane == 0) cc.big = 1;
         }
         __syncwarp();
         __syncthreads();  // p columns visible before the move copies them
@@ -269,19 +277,31 @@ __device__ int circle_sweeps(cg::cluster_group& cluster, double* buf, Circle& cc
       cluster_arrive();  // split barrier: closed by the next move's copy phase
       if (prof) t_move += clock64() - t1;
     }
-    // ---- sweep end: did any CTA rotate?
-    if (threadIdx.x == 0) cluster.map_shared_rank(&cc, 0)->sweep_rot[c] = cc.rotated;
+    // ---- sweep end: did any CTA rotate, and was any rotation big?
+    if (threadIdx.x == 0) {
+      cluster.map_shared_rank(&cc, 0)->sweep_rot[c] = cc.rotated;
+      cluster.map_shared_rank(&cc, 0)->sweep_big[c] = cc.big;
+    }
     if (C > 1) cluster_wait();  // close the pending split barrier
     cluster.sync();             // flags visible
-    int tot = 0;
+    int tot = 0, big = 0;
     const Circle* c0 = cluster.map_shared_rank(&cc, 0);
-    for (int k = 0; k < C; ++k) tot += c0->sweep_rot[k];
+    for (int k = 0; k < C; ++k) {
+      tot += c0->sweep_rot[k];
+      big |= c0->sweep_big[k];
+    }
     if (c == 0 && threadIdx.x == 0) counter[sweep] = tot;
     __syncthreads();
-    if (threadIdx.x == 0) cc.rotated = 0;
+    if (threadIdx.x == 0) cc.rotated = cc.big = 0;
     cluster.sync();  // everyone has read the flags before they are overwritten
     if (C > 1) cluster_arrive();
     if (tot == 0) break;
+    // Every rotation of this sweep was small (|cos| <= sqrt(eps)/2): by quadratic convergence the
+    // next sweep would rotate nothing (it would only re-check), so stop here (JACOBI_BIG2).
+    if (early && !big) {
+      ++sweep;
+      break;
+    }
   }
   if (C > 1) cluster_wait();
   if (c == 0 && threadIdx.x == 0) {
@@ -316,7 +336,7 @@ __global__ void __launch_bounds__(512) cluster_jacobi_kernel(CJParams p) {
   }
   __syncthreads();
   cluster.sync();
-  circle_sweeps<NC, RPL>(cluster, buf, cc, n, ld, b, p.tol * p.tol, p.counter);
+  circle_sweeps<NC, RPL>(cluster, buf, cc, n, ld, b, p.tol * p.tol, p.counter, p.early != 0);
   // ---- write back the two live blocks by their global block index
   for (int s = 0; s < 2; ++s) {
     const int bi = cc.blockid[cc.slotbuf[s]];
@@ -365,6 +385,7 @@ struct CSParams {
   int* counter;
   int* degenerate;
   unsigned long long* stamps;  // debug: phase timestamps (ns) of CTA 0, or null
+  int early;                   // as CJParams::early
 };
 
 __device__ __forceinline__ void stamp(unsigned long long* st, int i) {
@@ -657,7 +678,8 @@ __global__ void __launch_bounds__(NC == 2 && RPL == 8 ? 384 : 512, 1) cluster_sv
 
   // ---- 3. one-sided Jacobi on X (no V accumulation)
   stamp(p.stamps, 2);
-  circle_sweeps<NC, RPL>(cluster, buf, cc, n, n, b, p.tol * p.tol, p.counter, p.stamps ? p.stamps + 4 : nullptr);
+  circle_sweeps<NC, RPL>(cluster, buf, cc, n, n, b, p.tol * p.tol, p.counter, p.early != 0,
+                         p.stamps ? p.stamps + 4 : nullptr);
   stamp(p.stamps, 3);
 
   // ---- 4. [W; P What] in the [R; I] layout
@@ -743,7 +765,7 @@ int cluster_jacobi(int ncomp, double* X, int64_t n, double tol, int* counter, cu
   const size_t smem = sizeof(double) * static_cast<size_t>(4 * b) * 2 * n * ncomp;
   if (smem > 220 * 1024) return NOTAPPLICABLE;
   const int threads = 32 * (b < 1 ? 1 : b);
-  CJParams prm{X, static_cast<int>(n), b, tol, counter};
+  CJParams prm{X, static_cast<int>(n), b, tol, counter, std::getenv("NSK_SVD_FULLCHECK") ? 0 : 1};
   const int rpl = n <= 128 ? 4 : n <= 256 ? 8 : 16;
   auto kern = ncomp == 1 ? (rpl == 4 ? cluster_jacobi_kernel<1, 4> : rpl == 8 ? cluster_jacobi_kernel<1, 8>
                                                                               : cluster_jacobi_kernel<1, 16>)
@@ -819,7 +841,7 @@ int cluster_svd_rt(int ncomp, double* X, int64_t n, double tol, int* counter, in
   const bool dbg = std::getenv("NSK_SVD_DEBUG") != nullptr;
   unsigned long long* stamps = nullptr;
   if (dbg) NSK_CUDA_OK(cudaMallocAsync(&stamps, 6 * sizeof(unsigned long long), st));
-  CSParams prm{X, static_cast<int>(n), b, tol, counter, degenerate, stamps};
+  CSParams prm{X, static_cast<int>(n), b, tol, counter, degenerate, stamps, std::getenv("NSK_SVD_FULLCHECK") ? 0 : 1};
   const int rpl = n <= 128 ? 4 : n <= 256 ? 8 : 16;
   // (three buffers are only needed for n > 256: b = 16, RPL = 16)
   auto kern = ncomp == 1

@@ -8,7 +8,9 @@
 // four per lane with all loads issued before any store, so shared-memory
 // latency overlaps instead of serialising the chain (the two columns never
 // alias).  Accumulation order is the row order: results do not depend on the
-// batching.  Returns whether the pair was rotated.
+// batching.  Returns 0 when the pair was not rotated, 1 for a rotation with
+// |cos(p, q)| <= sqrt(eps) / 2 ("small"), 2 for a larger one (JACOBI_BIG2).
+
 #pragma once
 
 #include <cuda_runtime.h>
@@ -66,8 +68,13 @@ __device__ __forceinline__ void rotate_cols(double* __restrict__ xp, double* __r
   }
 }
 
+// cos^2 above which a rotation is "big": eps / 4, i.e. |cos| > 7.45e-9.  A sweep whose rotations
+// are all small leaves every pair at |cos| <~ tol (quadratic convergence: each small rotation moves
+// the other pairs' cosines by O(cos^2) = O(eps)), so the sweep after it would rotate nothing.
+constexpr double JACOBI_BIG2 = 0.25 * 2.220446049250313e-16;
+
 template <int NC>
-__device__ __forceinline__ bool jacobi_pair(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
+__device__ __forceinline__ int jacobi_pair(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
                                             int lane, double tol2) {
   double a = 0, bb = 0, cr = 0, ci = 0;
   int row = lane;
@@ -128,7 +135,8 @@ __device__ __forceinline__ bool jacobi_pair(double* __restrict__ xp, double* __r
     if (NC == 2) ci += __shfl_xor_sync(0xffffffffu, ci, o);
   }
   const double c2 = cr * cr + ci * ci;
-  if (!(c2 > tol2 * a * bb && c2 > 0.0)) return false;
+  if (!(c2 > tol2 * a * bb && c2 > 0.0)) return 0;
+  const int kind = c2 > JACOBI_BIG2 * a * bb ? 2 : 1;
   const double cabs = NC == 1 ? fabs(cr) : sqrt(c2);
   const double zeta = (bb - a) / (2.0 * (NC == 1 ? cr : cabs));
   const double tt =
@@ -141,7 +149,7 @@ __device__ __forceinline__ bool jacobi_pair(double* __restrict__ xp, double* __r
     ph_im = -ci * inv;
   }
   rotate_cols<NC>(xp, xq, ld, lane, cs, sn, ph_re, ph_im);
-  return true;
+  return kind;
 }
 
 }  // namespace nsk
@@ -217,7 +225,7 @@ __device__ __forceinline__ void store_col(double* __restrict__ x, int n, int lan
 // q read from and written back to shared memory; rows [n, ld) of both (the V
 // part of [R; I]) rotated in place.
 template <int NC, int RPL>
-__device__ __forceinline__ bool jacobi_step_preg(double (&pr)[RPL], double (&pim)[RPL], double* __restrict__ xp,
+__device__ __forceinline__ int jacobi_step_preg(double (&pr)[RPL], double (&pim)[RPL], double* __restrict__ xp,
                                                  double* __restrict__ xq, int n, int ld, int lane, double tol2) {
   double qr[RPL], qim[RPL];
   load_col<NC, RPL>(xq, n, lane, qr, qim);
@@ -242,7 +250,8 @@ __device__ __forceinline__ bool jacobi_step_preg(double (&pr)[RPL], double (&pim
     if (NC == 2) ci += __shfl_xor_sync(0xffffffffu, ci, o);
   }
   const double c2 = cr * cr + ci * ci;
-  if (!(c2 > tol2 * a * bb && c2 > 0.0)) return false;
+  if (!(c2 > tol2 * a * bb && c2 > 0.0)) return 0;
+  const int kind = c2 > JACOBI_BIG2 * a * bb ? 2 : 1;
   double ph_re = 1.0, ph_im = 0.0, c = cr;
   if (NC == 2) {
     const double inv = rsqrt_fast(c2);
@@ -278,7 +287,7 @@ __device__ __forceinline__ bool jacobi_step_preg(double (&pr)[RPL], double (&pim
   }
   store_col<NC, RPL>(xq, n, lane, qr, qim);
   if (ld > n) rotate_cols<NC>(xp + n * NC, xq + n * NC, ld - n, lane, cs, sn, ph_re, ph_im);
-  return true;
+  return kind;
 }
 
 // One-sided Jacobi step on the pair (xp, xq) with the leading n rows held in
@@ -289,11 +298,11 @@ __device__ __forceinline__ bool jacobi_step_preg(double (&pr)[RPL], double (&pim
 //   t = sign(d) 2c / (|d| + sqrt(d^2 + 4 c^2)),  d = ||q||^2 - ||p||^2,
 // on power-of-two-scaled d, 2c (no overflow), with fast rcp / rsqrt.
 template <int NC, int RPL>
-__device__ __forceinline__ bool jacobi_pair_reg(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
-                                                int lane, double tol2) {
+__device__ __forceinline__ int jacobi_pair_reg(double* __restrict__ xp, double* __restrict__ xq, int n, int ld,
+                                               int lane, double tol2) {
   double pr[RPL], pim[RPL];
   load_col<NC, RPL>(xp, n, lane, pr, pim);
-  const bool rot = jacobi_step_preg<NC, RPL>(pr, pim, xp, xq, n, ld, lane, tol2);
+  const int rot = jacobi_step_preg<NC, RPL>(pr, pim, xp, xq, n, ld, lane, tol2);
   if (rot) store_col<NC, RPL>(xp, n, lane, pr, pim);
   return rot;
 }

@@ -870,9 +870,15 @@ struct SvdStage {
       if (int rc = solve(false)) return rc;
       if (int rc = collect()) return rc;
     }
-    if (std::getenv("NSK_SVD_DEBUG")) std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d path=%d\n",
-                                                   static_cast<long long>(s), static_cast<long long>(n), b, host[0],
-                                                   host[2]);
+    if (std::getenv("NSK_SVD_DEBUG")) {
+      std::fprintf(stderr, "nsk svd: s=%lld n=%lld b=%d sweeps=%d path=%d rotations/sweep:", static_cast<long long>(s),
+                   static_cast<long long>(n), b, host[0], host[2]);
+      int cnt[MAX_SWEEPS];
+      const int ns = host[0] < MAX_SWEEPS ? host[0] + 1 : MAX_SWEEPS;
+      if (ns > 0 && cudaMemcpy(cnt, B.counter, sizeof(int) * ns, cudaMemcpyDeviceToHost) == cudaSuccess)
+        for (int i = 0; i < ns; ++i) std::fprintf(stderr, " %d", cnt[i]);
+      std::fprintf(stderr, "\n");
+    }
     if (n >= 2 && host[0] >= MAX_SWEEPS) return fail(ENOCONV, "svd: one-sided Jacobi did not converge");
     if (host[1]) return fail(ENOCONV, "svd: non-finite singular values (input contains NaN/Inf)");
     return OK;

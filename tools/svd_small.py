@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_2206_00975_b200 as nsk  # noqa: E402
 
-SHAPES = ((400, 100, False), (4096, 64, False), (300, 150, True), (1024, 256, False))
+SHAPES = ((400, 100, False), (4096, 64, False), (300, 150, True), (1024, 256, False), (1024, 512, False))
 
 
 def make(s, n, cplx):
