@@ -141,14 +141,17 @@ int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out)
     });
     // Bank-balanced slot order for the kernel's shared-memory gather: slot t is
     // read by lane t % 32, and the value of row r_lo sits at double offset
-    // r_lo + r_lo / 32, i.e. in 8-byte bank pair (r_lo + r_lo / 32) % 16.  Fill
-    // each half-warp (16 consecutive slots) with distinct bank pairs where the
+    // r_lo + 2 (r_lo / 64) in the 2048-row kernel with 16-byte loads
+    // (srht_kernel16, the usual path for m >= 2048) and at r_lo + r_lo / 32 in
+    // the 8-byte kernels, i.e. in 8-byte bank pair (offset % 16).  Fill each
+    // half-warp (16 consecutive slots) with distinct bank pairs where the
     // sample allows it, taking rows in increasing r_lo within each class.
     if (lb == 10) {
+      const bool v16 = m >= 2048;
       std::vector<std::vector<int32_t>> cls(16);
       for (int32_t r : order) {
-        const int64_t lo = op->idx[static_cast<size_t>(r)] & mask;
-        cls[static_cast<size_t>((lo + (lo >> 5)) & 15)].push_back(r);
+        const int64_t lo = op->idx[static_cast<size_t>(r)] & (v16 ? 2047 : mask);
+        cls[static_cast<size_t>((v16 ? lo + 2 * (lo >> 6) : lo + (lo >> 5)) & 15)].push_back(r);
       }
       std::vector<size_t> head(16, 0);
       std::vector<int32_t> balanced;

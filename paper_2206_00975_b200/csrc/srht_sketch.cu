@@ -223,6 +223,154 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
   }
 }
 
+// 16-byte variant of the 2048-row kernel (A 16-byte aligned, lda even): lane l
+// holds rows 2l + b + 64 t (b < 2, t < 32) as x[2t + b], so a block is 32
+// LDG.128 instead of 64 LDG.64, row bit 0 and bits 6-10 are register stages,
+// and both shared-memory passes move double2: row r sits at r + 2 (r >> 6), the
+// transposed read gives lane l the 64 contiguous rows [64 l, 64 l + 64) (lane
+// stride 528 B: conflict-free quarter-warps), bits 1-5 are the second set of
+// register stages.  Half the LSU / MIO instructions of srht_kernel<NQ, 11>.
+template <int NQ>
+__global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParams p) {
+  constexpr int L = 2048, PAD = L + 64;
+  extern __shared__ __align__(16) double zbuf[];  // [WARPS_PER_CTA][PAD]
+  __shared__ uint32_t sslot[NQ * 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x) {
+    const uint32_t v = t < p.nslots ? p.slot[t] : 0u;
+    const uint32_t rlo = v & (L - 1), rhi = v >> 11;
+    sslot[t] = (rlo + 2 * (rlo >> 6)) | (rhi << 12);
+  }
+  __syncthreads();
+
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * WARPS_PER_CTA + wib;
+  int64_t it = warp * p.per;
+  int64_t end = it + p.per;
+  if (end > p.total) end = p.total;
+  double* z = zbuf + wib * PAD;
+  double2* zv = reinterpret_cast<double2*>(z);
+
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  int seg = 0;
+  int64_t col = it < end ? it / p.nb : -1, blk = it < end ? it - col * p.nb : 0;
+  int64_t cur_col = col;
+  double x[64];
+  uint32_t smk[4];  // [1024-row half][b]: word of mask lane (2 lane + b) % 32, pre-shifted by lane / 16
+  const int mlane0 = (2 * lane) & 31, msh = lane >> 4;
+  if (it < end) {
+    const double2* a = reinterpret_cast<const double2*>(p.A + col * p.lda + blk * L) + lane;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const double2 v = __ldcs(a + 32 * t);
+      x[2 * t] = v.x;
+      x[2 * t + 1] = v.y;
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      smk[h] = __ldg(p.mask + ((p.jhi0 + blk) * 2 + (h >> 1)) * 32 + mlane0 + (h & 1)) >> msh;
+  }
+
+  for (; it < end; ++it) {
+    if (p.pf > 0 && lane == 0 && it + p.pf < end) {  // stage block it + pf in L2 (one bulk prefetch)
+      int64_t c3 = col, b3 = blk + p.pf;
+      while (b3 >= p.nb) {
+        b3 -= p.nb;
+        ++c3;
+      }
+      const double* a3 = p.A + c3 * p.lda + b3 * L;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a3), "r"(static_cast<unsigned>(L * 8))
+                   : "memory");
+    }
+    if (col != cur_col) {  // column boundary: flush segment 0
+      double* P = p.P + (warp * 2 + seg) * (NQ * 32);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        P[q * 32 + lane] = acc[q];
+        acc[q] = 0.0;
+      }
+      seg = 1;
+      cur_col = col;
+    }
+    const int64_t jhi = p.jhi0 + blk;
+    // D: row 2l + b + 64 t is bit (l / 16) + 2 (t % 16) of mask word (t / 16, lane (2l + b) % 32).
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const uint32_t flip = ((~smk[(t >> 4) * 2 + b]) >> (2 * (t & 15))) & 1u;
+        double& v = x[2 * t + b];
+        v = __hiloint2double(__double2hiint(v) ^ static_cast<int>(flip << 31), __double2loint(v));
+      }
+    // Row bit 0, then bits 6..10 (register index t).
+#pragma unroll
+    for (int t = 0; t < 32; ++t) bfly(x[2 * t], x[2 * t + 1]);
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if ((t & h) == 0) {
+          bfly(x[2 * t], x[2 * (t + h)]);
+          bfly(x[2 * t + 1], x[2 * (t + h) + 1]);
+        }
+#pragma unroll
+    for (int t = 0; t < 32; ++t) zv[lane + 33 * t] = make_double2(x[2 * t], x[2 * t + 1]);
+    __syncwarp();
+    // Lane now holds rows 64 lane + j in x[j].
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double2 v = zv[33 * lane + j];
+      x[2 * j] = v.x;
+      x[2 * j + 1] = v.y;
+    }
+    // Row bits 1..5.
+#pragma unroll
+    for (int h = 2; h < 64; h <<= 1)
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if ((j & h) == 0) bfly(x[j], x[j + h]);
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) zv[33 * lane + j] = make_double2(x[2 * j], x[2 * j + 1]);
+    int64_t c2 = col, b2 = blk + 1;
+    if (b2 == p.nb) {
+      b2 = 0;
+      ++c2;
+    }
+    if (it + 1 < end) {  // prefetch the next block into the now free registers
+      const double2* a2 = reinterpret_cast<const double2*>(p.A + c2 * p.lda + b2 * L) + lane;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const double2 v = __ldcs(a2 + 32 * t);
+        x[2 * t] = v.x;
+        x[2 * t + 1] = v.y;
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        smk[h] = __ldg(p.mask + ((p.jhi0 + b2) * 2 + (h >> 1)) * 32 + mlane0 + (h & 1)) >> msh;
+    }
+    __syncwarp();
+    // Sampled second stage: acc += (-1)^popc(r_hi & j_hi) Z[r_lo].
+    const uint32_t jh12 = static_cast<uint32_t>(jhi) << 12;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t v = sslot[q * 32 + lane];
+      const double zz = z[v & 0xfffu];
+      const int par = static_cast<int>(__popc(v & jh12) << 31);
+      acc[q] += __hiloint2double(__double2hiint(zz) ^ par, __double2loint(zz));
+    }
+    __syncwarp();
+    col = c2;
+    blk = b2;
+  }
+  if (cur_col >= 0) {
+    double* P = p.P + (warp * 2 + seg) * (NQ * 32);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) P[q * 32 + lane] = acc[q];
+  }
+}
+
 // SA[row(t), c] = scale * sum over the warps that touched column c, in warp
 // order.  One CTA per column: the warp range and segments are uniform, the
 // threads walk the slots (coalesced partial reads, several sums in flight).
@@ -288,8 +436,25 @@ int launch_srht_lb(SrhtParams p, int64_t warps, cudaStream_t st) {
 }
 
 template <int NQ>
+int launch_srht16(SrhtParams p, int64_t warps, cudaStream_t st) {
+  const int64_t ctas = (warps + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+  const size_t smem = sizeof(double) * WARPS_PER_CTA * (2048 + 64);
+  auto kern = srht_kernel16<NQ>;
+  NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  KernelTimer tm(st, "srht_kernel16");
+  kern<<<static_cast<unsigned>(ctas), WARPS_PER_CTA * 32, smem, st>>>(p);
+  tm.stop();
+  count_launch();
+  NSK_CUDA_OK(cudaGetLastError());
+  return OK;
+}
+
+// lb: 10, 11, or 12 = the 16-byte variant of 11
+template <int NQ>
 int launch_srht(SrhtParams p, int64_t warps, int lb, cudaStream_t st) {
-  return lb == 11 ? launch_srht_lb<NQ, 11>(p, warps, st) : launch_srht_lb<NQ, 10>(p, warps, st);
+  return lb == 12 ? launch_srht16<NQ>(p, warps, st)
+       : lb == 11 ? launch_srht_lb<NQ, 11>(p, warps, st)
+                  : launch_srht_lb<NQ, 10>(p, warps, st);
 }
 
 }  // namespace
@@ -335,8 +500,13 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
     const char* pfe = std::getenv("NSK_SRHT_PF");
     SrhtParams p{A, lda, n, nb, rows.row0 / L, total, per, tb->sign_mask, tb->srht_slot + base, ns,
                  part.as<double>(), pfe ? std::atoi(pfe) : 2};
-    int rc = NQ == 8 ? launch_srht<8>(p, warps, lb, st)
-                     : (NQ == 16 ? launch_srht<16>(p, warps, lb, st) : launch_srht<32>(p, warps, lb, st));
+    // 2048-row blocks by 16-byte loads when every block start is 16-byte aligned (NSK_SRHT_V16=0: 8-byte kernel)
+    const char* v16e = std::getenv("NSK_SRHT_V16");
+    const bool v16 = lb == 11 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda % 2 == 0) &&
+                     !(v16e && v16e[0] == '0');
+    const int lbk = v16 ? 12 : lb;
+    int rc = NQ == 8 ? launch_srht<8>(p, warps, lbk, st)
+                     : (NQ == 16 ? launch_srht<16>(p, warps, lbk, st) : launch_srht<32>(p, warps, lbk, st));
     if (rc != OK) return rc;
     srht_reduce<<<static_cast<unsigned>(n), 256, 0, st>>>(part.as<double>(), nb, per, ns, NQ * 32,
                                                           tb->srht_row + base, scale, SA, ldsa);
