@@ -60,6 +60,10 @@ int build_sign_mask(PhiloxKey key, int64_t m, uint32_t** out) {
 namespace {
 
 constexpr int WARPS_PER_CTA = 4;
+#ifndef SRHT_GATHER_BATCH
+#define SRHT_GATHER_BATCH 8
+#endif
+constexpr int SRHT_HI_BITS = 20;  // r_hi and j_hi bits (host-checked: m / 2048 < 2^20)
 
 struct SrhtParams {
   const double* A;
@@ -233,13 +237,33 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
 template <int NQ>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParams p) {
   constexpr int L = 2048, PAD = L + 64;
-  extern __shared__ __align__(16) double zbuf[];  // [WARPS_PER_CTA][PAD]
-  __shared__ uint32_t sslot[NQ * 32];
+  extern __shared__ __align__(16) double zbuf[];  // [WARPS_PER_CTA][PAD], then saddr [WARPS_PER_CTA][NQ * 32]
+  // gpar[k][lane] bit q = bit k of r_hi of slot q * 32 + lane: the parity word of a block,
+  // pb bit q = popc(r_hi & j_hi) & 1, is the XOR of gpar[k] over the set bits k of j_hi and is
+  // carried from block to block (XOR over the bits of j_hi ^ previous j_hi, ~2 per step).
+  __shared__ uint32_t gpar[SRHT_HI_BITS * 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < NQ * 32; t += blockDim.x) {
-    const uint32_t v = t < p.nslots ? p.slot[t] : 0u;
-    const uint32_t rlo = v & (L - 1), rhi = v >> 11;
-    sslot[t] = (rlo + 2 * (rlo >> 6)) | (rhi << 12);
+  double* z = zbuf + wib * PAD;
+  double2* zv = reinterpret_cast<double2*>(z);
+  // Per warp: the shared-memory byte address of each slot's row in this warp's z.
+  uint32_t* saddr = reinterpret_cast<uint32_t*>(zbuf + WARPS_PER_CTA * PAD) + wib * (NQ * 32);
+  {
+    const uint32_t zb = static_cast<uint32_t>(__cvta_generic_to_shared(z));
+    uint32_t rh[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int t = q * 32 + lane;
+      const uint32_t v = t < p.nslots ? p.slot[t] : 0u;
+      const uint32_t rlo = v & (L - 1);
+      rh[q] = v >> 11;
+      saddr[t] = zb + 8u * (rlo + 2 * (rlo >> 6));
+    }
+    for (int k = wib; k < SRHT_HI_BITS; k += WARPS_PER_CTA) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) w |= ((rh[q] >> k) & 1u) << q;
+      gpar[k * 32 + lane] = w;
+    }
   }
   __syncthreads();
 
@@ -247,8 +271,6 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
   int64_t it = warp * p.per;
   int64_t end = it + p.per;
   if (end > p.total) end = p.total;
-  double* z = zbuf + wib * PAD;
-  double2* zv = reinterpret_cast<double2*>(z);
 
   double acc[NQ];
 #pragma unroll
@@ -257,7 +279,8 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
   int64_t col = it < end ? it / p.nb : -1, blk = it < end ? it - col * p.nb : 0;
   int64_t cur_col = col;
   double x[64];
-  uint32_t smk[4];  // [1024-row half][b]: word of mask lane (2 lane + b) % 32, pre-shifted by lane / 16
+  uint32_t smk[4];  // [1024-row half][b]: word of mask lane (2 lane + b) % 32 (bit lane / 16 + 2 (t % 16))
+  uint32_t pb = 0, jprev = 0;
   const int mlane0 = (2 * lane) & 31, msh = lane >> 4;
   if (it < end) {
     const double2* a = reinterpret_cast<const double2*>(p.A + col * p.lda + blk * L) + lane;
@@ -269,7 +292,7 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
     }
 #pragma unroll
     for (int h = 0; h < 4; ++h)
-      smk[h] = __ldg(p.mask + ((p.jhi0 + blk) * 2 + (h >> 1)) * 32 + mlane0 + (h & 1)) >> msh;
+      smk[h] = __ldg(p.mask + ((p.jhi0 + blk) * 2 + (h >> 1)) * 32 + mlane0 + (h & 1));
   }
 
   for (; it < end; ++it) {
@@ -294,12 +317,16 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
       cur_col = col;
     }
     const int64_t jhi = p.jhi0 + blk;
+    for (uint32_t d = static_cast<uint32_t>(jhi) ^ jprev; d; d &= d - 1) pb ^= gpar[(__ffs(d) - 1) * 32 + lane];
+    jprev = static_cast<uint32_t>(jhi);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) smk[h] = ~(smk[h] >> msh);  // a set bit now means flip (rng.hpp:57)
     // D: row 2l + b + 64 t is bit (l / 16) + 2 (t % 16) of mask word (t / 16, lane (2l + b) % 32).
 #pragma unroll
     for (int t = 0; t < 32; ++t)
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
-        const uint32_t flip = ((~smk[(t >> 4) * 2 + b]) >> (2 * (t & 15))) & 1u;
+        const uint32_t flip = (smk[(t >> 4) * 2 + b] >> (2 * (t & 15))) & 1u;
         double& v = x[2 * t + b];
         v = __hiloint2double(__double2hiint(v) ^ static_cast<int>(flip << 31), __double2loint(v));
       }
@@ -348,17 +375,26 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
       }
 #pragma unroll
       for (int h = 0; h < 4; ++h)
-        smk[h] = __ldg(p.mask + ((p.jhi0 + b2) * 2 + (h >> 1)) * 32 + mlane0 + (h & 1)) >> msh;
+        smk[h] = __ldg(p.mask + ((p.jhi0 + b2) * 2 + (h >> 1)) * 32 + mlane0 + (h & 1));
     }
     __syncwarp();
-    // Sampled second stage: acc += (-1)^popc(r_hi & j_hi) Z[r_lo].
-    const uint32_t jh12 = static_cast<uint32_t>(jhi) << 12;
+    // Sampled second stage: acc += (-1)^popc(r_hi & j_hi) Z[r_lo], the parity from pb.
+    // Batches of GB slots: all addresses, then all rows, then the sums, so the two shared-memory
+    // latencies are paid once per batch instead of once per slot.
+    constexpr int GB = SRHT_GATHER_BATCH;
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const uint32_t v = sslot[q * 32 + lane];
-      const double zz = z[v & 0xfffu];
-      const int par = static_cast<int>(__popc(v & jh12) << 31);
-      acc[q] += __hiloint2double(__double2hiint(zz) ^ par, __double2loint(zz));
+    for (int q0 = 0; q0 < NQ; q0 += GB) {
+      uint32_t ad[GB];
+      double zz[GB];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) ad[u] = saddr[(q0 + u) * 32 + lane];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(zz[u]) : "r"(ad[u]) : "memory");
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int par = static_cast<int>((pb << (31 - (q0 + u))) & 0x80000000u);
+        acc[q0 + u] += __hiloint2double(__double2hiint(zz[u]) ^ par, __double2loint(zz[u]));
+      }
     }
     __syncwarp();
     col = c2;
@@ -438,7 +474,7 @@ int launch_srht_lb(SrhtParams p, int64_t warps, cudaStream_t st) {
 template <int NQ>
 int launch_srht16(SrhtParams p, int64_t warps, cudaStream_t st) {
   const int64_t ctas = (warps + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-  const size_t smem = sizeof(double) * WARPS_PER_CTA * (2048 + 64);
+  const size_t smem = sizeof(double) * WARPS_PER_CTA * (2048 + 64) + sizeof(uint32_t) * WARPS_PER_CTA * NQ * 32;
   auto kern = srht_kernel16<NQ>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   KernelTimer tm(st, "srht_kernel16");

@@ -49,13 +49,15 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("warp-block read, %2d warps/SM: %.1f GB/s\n", wps, n * 8 / (ms * 1e-3) / 1e9);
   }
-  for (int r = 0; r < 2; ++r) {
-    cudaEventRecord(e0);
-    grid_read<<<148 * 8, 256>>>((const double2*)a, n / 2, o);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
+  for (int cps : {2, 4, 8, 16, 32}) {  // the read-only ceiling: plain grid-stride 16-byte loads
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(e0);
+      grid_read<<<148 * cps, 256>>>((const double2*)a, n / 2, o);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("grid-stride 16-byte read, %2d CTAs of 256 per SM: %.1f GB/s\n", cps, n * 8 / (ms * 1e-3) / 1e9);
   }
-  cudaEventElapsedTime(&ms, e0, e1);
-  printf("grid-stride double4 read: %.1f GB/s\n", n * 8 / (ms * 1e-3) / 1e9);
   return 0;
 }
