@@ -9,10 +9,13 @@
 // B200 design (HBM-bound, one pass over A):
 //   * split j = j_lo + 1024 j_hi and idx = r_lo + 1024 r_hi, so the sign
 //     factorises: (-1)^popc(r_lo & j_lo) * (-1)^popc(r_hi & j_hi).
-//   * one warp owns a (column, j_hi) block of 1024 contiguous rows (8 KiB):
-//     coalesced 256 B loads, 5 butterfly stages in registers (row bits 5-9),
-//     a padded shared-memory transpose, 5 more stages (row bits 0-4): a full
-//     length-1024 FWHT with no block-wide barrier.
+//   * one warp owns a (column, j_hi) block of 2048 contiguous rows (16 KiB;
+//     1024 when the shard is not 2048-row aligned): coalesced loads, butterfly
+//     stages in registers on the row bits held by the register index, a padded
+//     shared-memory transpose, the remaining stages: a full length-2048 FWHT
+//     with no block-wide barrier.  srht_kernel16 (A 16-byte aligned, lda even)
+//     moves 16 bytes per access everywhere (LDG.128, STS.128 / LDS.128);
+//     srht_kernel<NQ, LB> is the 8-byte form for every other case.
 //   * the warp then gathers the s sampled rows r_lo from shared memory (the
 //     output slots are pre-sorted by r_lo so the gather is nearly
 //     sequential) and accumulates (-1)^popc(r_hi & j_hi) Z[r_lo] in registers.
@@ -535,7 +538,7 @@ int srht_apply(const Operator& op, const RowMap& rows, int64_t n, const double* 
     NSK_CUDA_OK(part.alloc(sizeof(double) * warps * 2 * NQ * 32, st));
     const char* pfe = std::getenv("NSK_SRHT_PF");
     SrhtParams p{A, lda, n, nb, rows.row0 / L, total, per, tb->sign_mask, tb->srht_slot + base, ns,
-                 part.as<double>(), pfe ? std::atoi(pfe) : 2};
+                 part.as<double>(), pfe ? std::atoi(pfe) : 1};  // 1 vs 2 blocks ahead: 0.3727 vs 0.3744 ms at configs[1]
     // 2048-row blocks by 16-byte loads when every block start is 16-byte aligned (NSK_SRHT_V16=0: 8-byte kernel)
     const char* v16e = std::getenv("NSK_SRHT_V16");
     const bool v16 = lb == 11 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (lda % 2 == 0) &&

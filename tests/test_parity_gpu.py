@@ -141,6 +141,29 @@ def test_srht_apply_parity(nsk, oracle, s, m, n):
     assert rel(got, ref) <= SA_TOL
 
 
+@pytest.mark.parametrize("s,m,n", [(1024, 1 << 15, 7), (300, 1 << 13, 40), (2500, 1 << 16, 3)])
+def test_srht_block_kernels_parity(nsk, oracle, monkeypatch, s, m, n):
+    """Every SRHT block kernel against the oracle: 2048-row blocks by 16-byte loads (srht_kernel16, the
+    default for 16-byte-aligned A with an even leading dimension), the 8-byte 2048-row kernel (reached by
+    an odd leading dimension, by a base address that is 8 mod 16, and by NSK_SRHT_V16=0) and 1024-row
+    blocks (NSK_SRHT_LB=10)."""
+    import torch
+    A = oracle.random_real(m, n, 21)
+    ref = oracle.apply(oracle.draw("srht", s, m, 9000002), A)
+    S = nsk.SketchOperator.draw("srht", s, m, 9000002)
+    assert rel(host(nsk.apply(S, dev(A)).data), ref) <= SA_TOL
+    buf = torch.zeros((n, m + 1), dtype=torch.float64, device="cuda").t()  # ld m + 1 (odd)
+    buf[:m].copy_(torch.from_numpy(A))
+    assert rel(host(nsk.apply(S, buf[:m]).data), ref) <= SA_TOL, "odd leading dimension"
+    buf = torch.zeros((n, m + 2), dtype=torch.float64, device="cuda").t()  # ld m + 2, base 8 mod 16
+    buf[1:m + 1].copy_(torch.from_numpy(A))
+    assert rel(host(nsk.apply(S, buf[1:m + 1]).data), ref) <= SA_TOL, "base address 8 mod 16"
+    monkeypatch.setenv("NSK_SRHT_V16", "0")
+    assert rel(host(nsk.apply(S, dev(A)).data), ref) <= SA_TOL, "NSK_SRHT_V16=0"
+    monkeypatch.setenv("NSK_SRHT_LB", "10")
+    assert rel(host(nsk.apply(S, dev(A)).data), ref) <= SA_TOL, "NSK_SRHT_LB=10"
+
+
 @pytest.mark.parametrize("s,m,n", [(400, 2000, 20), (4096, 100000, 8), (1024, 50000, 3), (64, 1000, 17),
                                    (30000, 70000, 2)])
 def test_countsketch_apply_parity(nsk, oracle, s, m, n):
