@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, LB == 10 ? 3 : 2) srht_ker
 template <int NQ>
 __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParams p) {
   constexpr int L = 2048, PAD = L + 64;
-  extern __shared__ __align__(16) double zbuf[];  // [WARPS_PER_CTA][PAD], then saddr [WARPS_PER_CTA][NQ * 32]
+  extern __shared__ __align__(16) double zbuf[];  // [WARPS_PER_CTA][PAD], then saddr [WARPS_PER_CTA][NQ * 16]
   // gpar[k][lane] bit q = bit k of r_hi of slot q * 32 + lane: the parity word of a block,
   // pb bit q = popc(r_hi & j_hi) & 1, is the XOR of gpar[k] over the set bits k of j_hi and is
   // carried from block to block (XOR over the bits of j_hi ^ previous j_hi, ~2 per step).
@@ -248,19 +248,21 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* z = zbuf + wib * PAD;
   double2* zv = reinterpret_cast<double2*>(z);
-  // Per warp: the shared-memory byte address of each slot's row in this warp's z.
-  uint32_t* saddr = reinterpret_cast<uint32_t*>(zbuf + WARPS_PER_CTA * PAD) + wib * (NQ * 32);
+  // Per warp: the byte offset in z of each slot's row, two 16-bit offsets per word (slots 2h, 2h + 1).
+  uint32_t* saddr = reinterpret_cast<uint32_t*>(zbuf + WARPS_PER_CTA * PAD) + wib * (NQ * 16);
+  const uint32_t zb = static_cast<uint32_t>(__cvta_generic_to_shared(z));
   {
-    const uint32_t zb = static_cast<uint32_t>(__cvta_generic_to_shared(z));
-    uint32_t rh[NQ];
+    uint32_t rh[NQ], off[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int t = q * 32 + lane;
       const uint32_t v = t < p.nslots ? p.slot[t] : 0u;
       const uint32_t rlo = v & (L - 1);
       rh[q] = v >> 11;
-      saddr[t] = zb + 8u * (rlo + 2 * (rlo >> 6));
+      off[q] = 8u * (rlo + 2 * (rlo >> 6));
     }
+#pragma unroll
+    for (int h = 0; h < NQ / 2; ++h) saddr[h * 32 + lane] = off[2 * h] | (off[2 * h + 1] << 16);
     for (int k = wib; k < SRHT_HI_BITS; k += WARPS_PER_CTA) {
       uint32_t w = 0;
 #pragma unroll
@@ -390,7 +392,11 @@ __global__ void __launch_bounds__(WARPS_PER_CTA * 32, 2) srht_kernel16(SrhtParam
       uint32_t ad[GB];
       double zz[GB];
 #pragma unroll
-      for (int u = 0; u < GB; ++u) ad[u] = saddr[(q0 + u) * 32 + lane];
+      for (int u = 0; u < GB; u += 2) {
+        const uint32_t w2 = saddr[((q0 + u) >> 1) * 32 + lane];
+        ad[u] = zb + (w2 & 0xffffu);
+        ad[u + 1] = zb + (w2 >> 16);
+      }
 #pragma unroll
       for (int u = 0; u < GB; ++u) asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(zz[u]) : "r"(ad[u]) : "memory");
 #pragma unroll
@@ -477,7 +483,7 @@ int launch_srht_lb(SrhtParams p, int64_t warps, cudaStream_t st) {
 template <int NQ>
 int launch_srht16(SrhtParams p, int64_t warps, cudaStream_t st) {
   const int64_t ctas = (warps + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-  const size_t smem = sizeof(double) * WARPS_PER_CTA * (2048 + 64) + sizeof(uint32_t) * WARPS_PER_CTA * NQ * 32;
+  const size_t smem = sizeof(double) * WARPS_PER_CTA * (2048 + 64) + sizeof(uint32_t) * WARPS_PER_CTA * NQ * 16;
   auto kern = srht_kernel16<NQ>;
   NSK_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   KernelTimer tm(st, "srht_kernel16");
