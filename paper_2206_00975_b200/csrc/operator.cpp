@@ -153,24 +153,55 @@ int draw_operator(int kind, int64_t s, int64_t m, uint64_t seed, Operator** out)
         const int64_t lo = op->idx[static_cast<size_t>(r)] & (v16 ? 2047 : mask);
         cls[static_cast<size_t>((v16 ? lo + 2 * (lo >> 6) : lo + (lo >> 5)) & 15)].push_back(r);
       }
+      // Spread every class evenly over the ceil(s / 16) half-warps: half-warp h takes
+      // ceil(remaining_c / half-warps left) rows of class c, trimmed or topped up to 16 by
+      // the classes whose share is furthest from a whole row.  A half-warp costs as many
+      // wavefronts as its largest class multiplicity (97 -> 80 for the 64 half-warps of
+      // configs[1]; 76 is the bound set by the largest class).
       std::vector<size_t> head(16, 0);
       std::vector<int32_t> balanced;
       balanced.reserve(order.size());
-      int64_t left = s;
-      while (left > 0) {
-        int took = 0;
-        for (int c = 0; c < 16 && took < 16 && left > 0; ++c)
-          if (head[static_cast<size_t>(c)] < cls[static_cast<size_t>(c)].size()) {
+      const int64_t nh = (s + 15) / 16;
+      for (int64_t h = 0; h < nh; ++h) {
+        const double hl = static_cast<double>(nh - h);
+        int64_t cnt[16], take[16], sum = 0, avail = 0;
+        for (int c = 0; c < 16; ++c) {
+          cnt[c] = static_cast<int64_t>(cls[static_cast<size_t>(c)].size() - head[static_cast<size_t>(c)]);
+          take[c] = (cnt[c] + (nh - h) - 1) / (nh - h);
+          sum += take[c];
+          avail += cnt[c];
+        }
+        while (sum > 16) {
+          int best = -1;
+          double bv = 0.0;
+          for (int c = 0; c < 16; ++c)
+            if (take[c] > 0) {
+              const double v = static_cast<double>(cnt[c]) / hl - static_cast<double>(take[c] - 1);
+              if (best < 0 || v < bv) {
+                best = c;
+                bv = v;
+              }
+            }
+          --take[best];
+          --sum;
+        }
+        while (sum < 16 && sum < avail) {
+          int best = -1;
+          double bv = 0.0;
+          for (int c = 0; c < 16; ++c)
+            if (cnt[c] > take[c]) {
+              const double v = static_cast<double>(cnt[c]) / hl - static_cast<double>(take[c]);
+              if (best < 0 || v > bv) {
+                best = c;
+                bv = v;
+              }
+            }
+          ++take[best];
+          ++sum;
+        }
+        for (int c = 0; c < 16; ++c)
+          for (int64_t t = 0; t < take[c]; ++t)
             balanced.push_back(cls[static_cast<size_t>(c)][head[static_cast<size_t>(c)]++]);
-            ++took;
-            --left;
-          }
-        for (int c = 0; c < 16 && took < 16 && left > 0; ++c)  // pad the half-warp with leftovers
-          while (took < 16 && left > 0 && head[static_cast<size_t>(c)] < cls[static_cast<size_t>(c)].size()) {
-            balanced.push_back(cls[static_cast<size_t>(c)][head[static_cast<size_t>(c)]++]);
-            ++took;
-            --left;
-          }
       }
       order.swap(balanced);
     }
