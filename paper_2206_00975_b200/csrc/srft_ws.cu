@@ -28,8 +28,12 @@
 // restaged only after the samplers have seen V_FULL of the tile that last
 // used it.  Shared memory: two tile buffers and V (64 KiB each, swizzled so
 // every access is 4 wavefronts per warp) and the w_1024 twiddles.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 #include <mutex>
 #include "fft32.cuh"
@@ -113,8 +117,12 @@ __global__ void build_srft_sgn_kernel(const uint32_t* __restrict__ bits, int64_t
   }
 }
 
-__global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
-  extern __shared__ __align__(16) double2 smx[];
+// TMA: the tile is staged by four 3-D tensor boxes {8 doubles, 256 rows, 1 column} issued by one
+// sampler thread (no LSU work: the cp.async form costs 32 instructions per sampler thread and tile and
+// twice the ideal shared-memory wavefronts, one per 64-byte row segment).
+template <bool TMA>
+__global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p, const __grid_constant__ CUtensorMap tmA) {
+  extern __shared__ __align__(128) double2 smx[];
   double2* BUF = smx;             // 2 x [XL][4]: staged tile (row k2, sequence i), then its transpose
   double2* V = BUF + 2 * XL * XS; // [XL][4] bins
   double2* tw = V + XL * XS;      // [k][a]: w_1024^{a k} (a warp's 8 row classes: one wavefront)
@@ -127,8 +135,8 @@ __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
   for (int e = threadIdx.x; e < XL; e += XT)
     tw[e] = unit_phase(static_cast<uint64_t>((e >> 5) * (e & 31)), 2.0 / XL);
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full)), "r"(128));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + 1)), "r"(128));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full)), "r"(TMA ? 1 : 128));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(full + 1)), "r"(TMA ? 1 : 128));
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -208,9 +216,26 @@ __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p) {
   }
   // stage tile (cc, TT): chunk ch = ts + 128 j is row ch / 4, sequence ch % 4
   auto stage = [&](int64_t cc, int64_t TT, int bf) {
-    const double* src = p.A + cc * p.lda + XKT * TT;
     double2* RAW = BUF + bf * (XL * XS);
     uint64_t* bar = full + bf;
+    if constexpr (TMA) {
+      if (ts == 0) {
+        // the buffer's last generic-proxy accesses (the previous tile's transpose) precede the async writes
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)),
+                     "r"(static_cast<uint32_t>(sizeof(double2) * XL * XS))
+                     : "memory");
+#pragma unroll
+        for (int h = 0; h < XL / 256; ++h)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+              "[%5];\n" ::"r"(su32(RAW + h * 256 * XS)),
+              "l"(&tmA), "r"(static_cast<int>(XKT * TT)), "r"(256 * h), "r"(static_cast<int>(cc)), "r"(su32(bar))
+              : "memory");
+      }
+      return;
+    }
+    const double* src = p.A + cc * p.lda + XKT * TT;
 #pragma unroll 8
     for (int j = 0; j < 32; ++j) {
       const int ch = ts + 128 * j, row = ch >> 2, i = ch & 3;
@@ -363,6 +388,28 @@ int build_srft_sgn(const uint32_t* sign_bits, int64_t m, uint64_t** out) {
 
 namespace {
 
+bool encode_tile_map(const double* A, int64_t lda, int64_t P, int64_t n, CUtensorMap* out) {
+  static PFN_cuTensorMapEncodeTiled encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<PFN_cuTensorMapEncodeTiled>(nullptr);
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }();
+  if (!encode || P > 0xffffffffLL || n > 0x7fffffffLL) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(XL), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(P) * sizeof(double),
+                                 static_cast<cuuint64_t>(lda) * sizeof(double)};
+  const cuuint32_t box[3] = {XKT, 256, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(A), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // The warp-specialised apply over one length-m sequence per column (the whole operator, or a cyclic
 // shard with its own tables and the shard twiddle `post`).
 int srft_ws_run(int64_t m, int64_t s, int64_t n, const double* A, int64_t lda, const uint64_t* sgn,
@@ -376,8 +423,16 @@ int srft_ws_run(int64_t m, int64_t s, int64_t n, const double* A, int64_t lda, c
   const int64_t jmax = chunk / tiles + 2;
   // two tile buffers, V, twiddles, slot steps, 2 mbarriers
   const size_t smem = sizeof(double2) * (3 * XL * XS + XL + XNQ * 128) + 16;
-  NSK_CUDA_OK(cudaFuncSetAttribute(srft_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  NSK_CUDA_OK(cudaFuncSetAttribute(srft_ws_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
+  NSK_CUDA_OK(cudaFuncSetAttribute(srft_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  // A as {k1 (P, contiguous), k2 (1024, stride P), column (n, stride lda)}: tile T of column c is the
+  // boxes {8, 256, 1} at (8 T, 256 h, c).  NSK_SRFT_TMA=0 or a failed encode: cp.async staging.
+  CUtensorMap tm_a;
+  std::memset(&tm_a, 0, sizeof(tm_a));
+  const char* te = std::getenv("NSK_SRFT_TMA");
+  const bool tma = !(te && te[0] == '0') && encode_tile_map(A, lda, P, n, &tm_a);
   const double scale = 0.5 / std::sqrt(static_cast<double>(s));  // unnormalised DFT / sqrt(s); pairs carry 2
   for (int64_t b = 0; b < s; b += XNQ * 128) {
     const int ns = static_cast<int>((s - b) < XNQ * 128 ? (s - b) : XNQ * 128);
@@ -394,7 +449,10 @@ int srft_ws_run(int64_t m, int64_t s, int64_t n, const double* A, int64_t lda, c
     }
     WsParams p{A, lda, m, P, tiles, total, chunk, jmax, sgn, freq + b, ns, anc.as<double2>(), part.as<double2>()};
     KernelTimer tm(st, "srft_ws_kernel");
-    srft_ws_kernel<<<static_cast<unsigned>(G), XT, smem, st>>>(p);
+    if (tma)
+      srft_ws_kernel<true><<<static_cast<unsigned>(G), XT, smem, st>>>(p, tm_a);
+    else
+      srft_ws_kernel<false><<<static_cast<unsigned>(G), XT, smem, st>>>(p, tm_a);
     tm.stop();
     count_launch();
     NSK_CUDA_OK(cudaGetLastError());
