@@ -117,9 +117,9 @@ __global__ void build_srft_sgn_kernel(const uint32_t* __restrict__ bits, int64_t
   }
 }
 
-// TMA (opt-in, see srft_ws_run): the tile is staged by four 3-D tensor boxes {8 doubles, 256 rows,
-// 1 column} issued by one sampler thread (no LSU work: the cp.async form costs 32 instructions per
-// sampler thread and tile and twice the ideal shared-memory wavefronts, one per 64-byte row segment).
+// TMA: the tile is staged by four 3-D tensor boxes {8 doubles, 256 rows, 1 column} issued by one
+// sampler thread (no LSU work: the cp.async form costs 32 instructions per sampler thread and tile and
+// twice the ideal shared-memory wavefronts, one per 64-byte row segment).
 template <bool TMA>
 __global__ void __launch_bounds__(XT, 1) srft_ws_kernel(WsParams p, const __grid_constant__ CUtensorMap tmA) {
   extern __shared__ __align__(128) double2 smx[];
@@ -428,13 +428,11 @@ int srft_ws_run(int64_t m, int64_t s, int64_t n, const double* A, int64_t lda, c
   NSK_CUDA_OK(cudaFuncSetAttribute(srft_ws_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
   // A as {k1 (P, contiguous), k2 (1024, stride P), column (n, stride lda)}: tile T of column c is the
-  // boxes {8, 256, 1} at (8 T, 256 h, c).  Opt-in (NSK_SRFT_TMA=1): it removes 21% of the kernel's
-  // shared-memory wavefronts and the samplers' 32 cp.async per thread and tile, but the FFT warps are
-  // the critical path, and it measured 0.7514 ms against 0.7472 ms for cp.async staging at configs[1].
+  // boxes {8, 256, 1} at (8 T, 256 h, c).  NSK_SRFT_TMA=0 or a failed encode: cp.async staging.
   CUtensorMap tm_a;
   std::memset(&tm_a, 0, sizeof(tm_a));
   const char* te = std::getenv("NSK_SRFT_TMA");
-  const bool tma = te && te[0] == '1' && encode_tile_map(A, lda, P, n, &tm_a);
+  const bool tma = !(te && te[0] == '0') && encode_tile_map(A, lda, P, n, &tm_a);
   const double scale = 0.5 / std::sqrt(static_cast<double>(s));  // unnormalised DFT / sqrt(s); pairs carry 2
   for (int64_t b = 0; b < s; b += XNQ * 128) {
     const int ns = static_cast<int>((s - b) < XNQ * 128 ? (s - b) : XNQ * 128);

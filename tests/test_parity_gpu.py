@@ -119,10 +119,6 @@ def test_srft_stream_parity(nsk, oracle, monkeypatch, s, m, n):
     got, _ = gpu_apply(nsk, "srft", s, m, 93, A)
     ref = oracle.apply(oracle.draw("srft", s, m, 93), A)
     assert rel(got, ref) <= SA_TOL
-    monkeypatch.setenv("NSK_SRFT_TMA", "1")  # the same kernel with its tiles staged by TMA tensor boxes
-    other, _ = gpu_apply(nsk, "srft", s, m, 93, A)
-    assert rel(other, ref) <= SA_TOL, "NSK_SRFT_TMA=1"
-    monkeypatch.delenv("NSK_SRFT_TMA")
     for env in ("NSK_SRFT_WS", "NSK_SRTT_NOTILE"):  # cumulative: shared-memory tiles, then strided FFT
         monkeypatch.setenv(env, "0" if env == "NSK_SRFT_WS" else "1")
         other, _ = gpu_apply(nsk, "srft", s, m, 93, A)
