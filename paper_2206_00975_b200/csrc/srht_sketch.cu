@@ -430,14 +430,23 @@ __global__ void __launch_bounds__(256) srht_reduce(const double* __restrict__ P,
     double v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = 0.0;
-    for (int64_t w = w0; w <= w1; ++w) {
-      const int seg = w * per >= c * nb ? 0 : 1;  // the warp's first item lies in column c
-      const double* Pw = P + (w * 2 + seg) * slot_stride;
+    for (int64_t wb = w0; wb <= w1; wb += 4) {  // four warps' partials in flight, summed in warp order
+      double t4[4][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + 256 * u;
-        if (t < nslots) v[u] += Pw[t];
+      for (int j = 0; j < 4; ++j) {
+        const int64_t w = wb + j;
+        const int seg = w * per >= c * nb ? 0 : 1;  // the warp's first item lies in column c
+        const double* Pw = P + (w * 2 + seg) * slot_stride;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + 256 * u;
+          t4[j][u] = (w <= w1 && t < nslots) ? __ldcg(Pw + t) : 0.0;
+        }
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] += t4[j][u];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
